@@ -1,0 +1,221 @@
+/* gsmart.h — C ABI of the B200-native gSmart hot path.
+ *
+ * Method: gSmart, "An Efficient SPARQL Query Engine Using Sparse Matrix
+ * Algebra" (arXiv 2106.14038; /root/reference/PAPER.md, cited as P:L<line>).
+ * The library answers SPARQL basic graph patterns (BGPs) over an RDF
+ * triple set with the paper's matrix-algebra method: LSpM storage (§6.2),
+ * degree-driven planning (§6.1.2), grouped incident-edge evaluation (§5) as
+ * label-filtered boolean SpMVs over candidate bitmaps, tree-based binding
+ * storage (§7.1) with pre-pruning (§7.2.2) and bottom-up tree pruning
+ * (§8.1 steps 3-4), and returns the solution rows.  All steps of
+ * gsmart_build_lspm and gsmart_execute run as CUDA kernels for sm_100a; there
+ * is no CPU fallback (a missing GPU is GSMART_E_CUDA).
+ *
+ * Call order (P:L263-L289 phase order):
+ *   gsmart_create -> gsmart_load_triples -> gsmart_build_lspm
+ *   -> gsmart_plan(query graph) -> gsmart_execute -> gsmart_result_*
+ *
+ * Conventions
+ *  - Every call returns gsmart_status; nothing throws or aborts across the ABI.
+ *    After an error, gsmart_last_error(ctx) gives a message.  A failed CUDA
+ *    call poisons the context (all later calls return GSMART_E_CUDA).
+ *  - Ids: entities are 0-based < n_entities, predicates 1-based
+ *    <= n_predicates.  Triples are a set: duplicates are removed
+ *    (reading R5 of DESIGN.md).
+ *  - Ownership: input pointers are borrowed for the duration of the call only.
+ *    ctx / plan / result objects are library-owned and released with their
+ *    *_destroy / *_free call.  Pointers returned by gsmart_result_* stay valid
+ *    until gsmart_result_free.  A plan is immutable and reusable.  A ctx is not
+ *    thread-safe: one ctx per GPU per process.
+ *  - Query semantics ("the conjunction of these triple patterns"):
+ *    solutions are all mappings of the query's variables to entity ids such
+ *    that every pattern is a triple of the set (homomorphism, reading R6).
+ *    Rows list the bindings of the variable vertices in ascending vertex
+ *    index, sorted lexicographically ascending; rows are distinct.
+ *  - An empty result is GSMART_OK with 0 rows.  A constant id >= n_entities
+ *    or absent from the data yields an empty result, not an error.  A query
+ *    with no variables yields one empty row if all its patterns hold, else 0.
+ */
+#ifndef GSMART_H
+#define GSMART_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSMART_ABI_VERSION 1
+
+typedef enum {
+  GSMART_OK = 0,
+  GSMART_E_INVALID_ARG = -1,     /* bad pointer, size, id, or query shape */
+  GSMART_E_STATE = -2,           /* call-order violation (e.g. execute before build) */
+  GSMART_E_OOM = -3,             /* device allocation failed */
+  GSMART_E_CUDA = -4,            /* CUDA error / no device; ctx is poisoned */
+  GSMART_E_NCCL = -5,            /* collective failure (world > 1) */
+  GSMART_E_UNSUPPORTED = -6,     /* variable predicate, direction-driven plan with constants, too many levels */
+  GSMART_E_RESULT_OVERFLOW = -7  /* rows (or a trie level) > max_result_rows; n_rows still reported */
+} gsmart_status;
+
+/* pointer kinds for gsmart_load_triples */
+#define GSMART_PTR_HOST 1u
+#define GSMART_PTR_DEVICE 2u
+/* LSpM formats (P:L411 LSpM_CSR, P:L432 LSpM_CSC) */
+#define GSMART_CSR 1u
+#define GSMART_CSC 2u
+/* traversal */
+#define GSMART_DEGREE 0u     /* degree-driven, §6.1.2 (supported) */
+#define GSMART_DIRECTION 1u  /* direction-driven, §6.1.1 (GSMART_E_UNSUPPORTED in this version) */
+/* execute flags */
+#define GSMART_COUNT_ONLY 1u      /* stop after pruning: n_rows only, no row enumeration */
+#define GSMART_KEEP_ON_DEVICE 2u  /* do not copy rows to host (use gsmart_result_rows_device) */
+#define GSMART_NO_REFINE 4u       /* skip the backward group re-evaluation */
+#define GSMART_PROFILE 8u         /* per-kernel CUDA-event timing into gsmart_stats */
+
+typedef struct gsmart_ctx gsmart_ctx;
+typedef struct gsmart_plan_s gsmart_plan_t;
+typedef struct gsmart_result gsmart_result;
+
+typedef struct {
+  int device;                 /* CUDA device ordinal */
+  int rank, world;            /* world >= 1; world > 1 = 1-D row partition over ranks */
+  const void* nccl_unique_id; /* 128 bytes from gsmart_get_nccl_id on rank 0; NULL if world == 1 */
+  void* stream;               /* cudaStream_t to run on, or NULL: the library creates one */
+  uint64_t max_result_rows;   /* capacity for rows and for each trie level; 0 = 2^31 - 1 */
+} gsmart_config;
+
+/* ABI version and a build string (static storage). */
+int gsmart_abi_version(void);
+const char* gsmart_build_info(void);
+
+/* NCCL bootstrap: rank 0 fills 128 bytes to broadcast (e.g. via torch.distributed). */
+gsmart_status gsmart_get_nccl_id(void* out128);
+
+/* Context on cfg->device.  Fails with GSMART_E_CUDA if no usable sm_100 device. */
+gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** out);
+void gsmart_destroy(gsmart_ctx* ctx);
+/* Message of the last error on ctx (static storage if ctx is NULL). */
+const char* gsmart_last_error(const gsmart_ctx* ctx);
+
+/* Copy n triples (s[i], p[i], o[i]) into device memory owned by ctx
+ * (§6.2.1 steps 1-2 input: encoded ids).  flags: GSMART_PTR_HOST or
+ * GSMART_PTR_DEVICE for where s/p/o live.  Ids are validated (s,o <
+ * n_entities, 1 <= p <= n_predicates) -> GSMART_E_INVALID_ARG.  Replaces any
+ * previously loaded triples and invalidates the LSpM.  n may be 0.
+ * n_entities < 2^31, n_predicates <= 65535. */
+gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s, const uint32_t* p,
+                                  const uint32_t* o, uint64_t n, uint32_t n_entities,
+                                  uint32_t n_predicates, uint32_t flags);
+
+/* Build the LSpM (§6.2) on the GPU: keep only triples whose
+ * predicate is in keep_preds (host array of n_keep ids; n_keep = 0 keeps all —
+ * P:L408 "Read necessary RDF triples where predicates appear in the
+ * queries"), de-duplicate, and store CSR (rows = subjects) and/or CSC (rows =
+ * objects) as row_ptr[N+1] (uint32), col[M] (uint32) and pred[M] (uint8 when
+ * n_predicates <= 255, else uint16), entries sorted by (row, pred, col), so
+ * every (row, predicate) pair is one contiguous range.  Empty rows have
+ * row_ptr[i] == row_ptr[i+1] (the paper's Mr/Pr row elimination).
+ * formats: GSMART_CSR | GSMART_CSC (execute needs both).  Requires kept
+ * M < 2^32.  GSMART_E_STATE if no triples were loaded. */
+gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep_preds, uint32_t n_keep,
+                                uint32_t formats);
+
+/* Device view of one built LSpM format (for inspection / parity tests).
+ * Pointers are device pointers owned by ctx, valid until the next load/build. */
+typedef struct {
+  uint32_t n_rows;          /* = n_entities */
+  uint64_t nnz;             /* M after keep + de-duplication */
+  uint32_t pred_bytes;      /* 1 or 2 */
+  const uint32_t* row_ptr;  /* [n_rows + 1] */
+  const uint32_t* col;      /* [nnz] */
+  const void* pred;         /* [nnz] uint8 or uint16 */
+} gsmart_lspm_view;
+gsmart_status gsmart_lspm_get(const gsmart_ctx* ctx, uint32_t format, gsmart_lspm_view* out);
+
+/* Query graph (vertices = variables / constants, edges = patterns). */
+typedef struct { uint32_t is_const, const_id; } gsmart_qvertex; /* vertex index = array position */
+typedef struct { uint32_t src, pred, dst; } gsmart_qedge;       /* pattern src --pred--> dst */
+typedef struct {
+  uint32_t n_vertices; const gsmart_qvertex* v;
+  uint32_t n_edges; const gsmart_qedge* e;
+} gsmart_query;
+
+/* Plan (host only, microseconds; ctx may be NULL).  Degree-driven traversal
+ * (§6.1.2): constant-incident patterns become seeds (light
+ * queries); roots by max unevaluated edges, then max
+ * unevaluated out-edges, then lowest index; groups = all unevaluated incident
+ * edges of each popped vertex.  Also derives the trie order (variables in
+ * first-visit order), tree and closing edges.  Errors:
+ * GSMART_E_INVALID_ARG (vertex index out of range, pred == 0, a variable in
+ * no pattern, > 32 variables, > 32 edges), GSMART_E_UNSUPPORTED
+ * (traversal == GSMART_DIRECTION). */
+gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uint32_t traversal,
+                          gsmart_plan_t** out);
+/* JSON description (roots, seeds, groups, levels, pi, tree/closing edges,
+ * paths).  Writes at most cap bytes (NUL-terminated when cap > 0) and sets
+ * *need to the full length + 1. */
+gsmart_status gsmart_plan_describe(const gsmart_plan_t* plan, char* buf, size_t cap, size_t* need);
+void gsmart_plan_free(gsmart_plan_t* plan);
+
+/* Execute plan on the built LSpM: seeds -> grouped incident-edge evaluation
+ * (forward, then backward re-evaluation unless GSMART_NO_REFINE) -> trie
+ * expansion with pre-pruning and closing-edge checks -> bottom-up prune ->
+ * row enumeration + lexicographic sort.  Collective when world > 1.
+ * Synchronises the ctx stream before returning. */
+gsmart_status gsmart_execute(gsmart_ctx* ctx, const gsmart_plan_t* plan, uint32_t flags,
+                             gsmart_result** out);
+
+/* n_rows, n_cols (= number of variables) and var_of_col[n_cols] (query vertex
+ * index of each column; host memory owned by the result). */
+gsmart_status gsmart_result_shape(const gsmart_result* r, uint64_t* n_rows, uint32_t* n_cols,
+                                  const uint32_t** var_of_col);
+/* Host rows, row-major uint32[n_rows * n_cols], sorted, distinct (rank 0 when
+ * world > 1).  Copied from the device on first call if KEEP_ON_DEVICE. */
+gsmart_status gsmart_result_rows(gsmart_result* r, const uint32_t** rows);
+/* Device rows (same layout) — valid unless GSMART_COUNT_ONLY. */
+gsmart_status gsmart_result_rows_device(const gsmart_result* r, const uint32_t** rows_dev);
+/* Candidate bitmap of query vertex `vertex` after the filter schedule:
+ * device pointer to ceil(n_entities/32) uint32 words, bit (i & 31) of word
+ * (i >> 5) set iff entity i is a candidate. */
+gsmart_status gsmart_result_candidates(const gsmart_result* r, uint32_t vertex,
+                                       const uint32_t** bits_dev, uint32_t* n_words);
+/* Trie level k (0 = root level) after pruning: variable vertex, node count and
+ * device pointers parent[n] (index into level k-1; undefined for k = 0) and
+ * bind[n] (entity id).  Children of a node are contiguous, parent[] is
+ * non-decreasing. */
+gsmart_status gsmart_result_level(const gsmart_result* r, uint32_t k, uint32_t* vertex,
+                                  uint64_t* n, const uint32_t** parent_dev,
+                                  const uint32_t** bind_dev);
+
+#define GSMART_MAX_LEVELS 32
+#define GSMART_NKERNELS 16
+typedef struct {
+  double ms_total;              /* host wall time of gsmart_execute */
+  double ms_kernel[GSMART_NKERNELS]; /* per kernel class (GSMART_PROFILE), see kernel_names */
+  uint64_t launches[GSMART_NKERNELS];
+  uint64_t bytes[GSMART_NKERNELS];   /* algorithmic bytes per kernel class */
+  uint64_t edges_evaluated;     /* LSpM entries read whose label matched (seed + filter + expansion) */
+  uint64_t filter_rows;         /* rows (candidate bits) processed by the group filter */
+  uint64_t filter_entries;      /* LSpM entries scanned by the group filter */
+  uint64_t seed_entries;        /* segment entries scattered by seeds */
+  uint64_t expand_entries;      /* segment entries examined by the expansion */
+  uint64_t closing_checks;      /* closing-edge membership tests */
+  uint32_t n_levels;
+  uint64_t level_nodes[GSMART_MAX_LEVELS];   /* F_k before pruning */
+  uint64_t level_alive[GSMART_MAX_LEVELS];   /* F_k after pruning */
+  uint64_t allgather_bytes;     /* world > 1 */
+  const char* kernel_names[GSMART_NKERNELS];
+} gsmart_stats;
+gsmart_status gsmart_result_stats(const gsmart_result* r, gsmart_stats* out);
+void gsmart_result_free(gsmart_result* r);
+
+/* Utility for bindings without a CUDA runtime of their own: synchronous copy
+ * of `bytes` from device memory `src_dev` (on ctx's device) into host `dst`. */
+gsmart_status gsmart_copy_to_host(gsmart_ctx* ctx, void* dst, const void* src_dev, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSMART_H */

@@ -1,0 +1,116 @@
+// Device-side primitives of the gSmart hot path (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define GSM_FULL 0xffffffffu
+
+namespace gsm {
+
+constexpr int MAXG = 16;          // max edges per direction in one group evaluation
+constexpr int MAXL = 32;          // max trie levels (= variables)
+constexpr int MAXC = 16;          // max closing edges per level
+constexpr uint32_t SHORT_ROW = 32;     // rows <= this: one lane scans it (group filter)
+constexpr uint32_t HEAVY_ROW = 16384;  // rows > this: split into chunks across CTAs
+constexpr uint32_t HEAVY_CHUNK = 16384;
+constexpr uint32_t EXP_CHUNK = 256;    // expansion work item = <= 256 segment entries
+
+// counters (uint64) in the ctx stats array
+enum Ctr { C_FILTER_ROWS = 0, C_FILTER_SCANNED, C_FILTER_MATCHED, C_SEED, C_EXPAND, C_CLOSING,
+           C_HEAVY, C_NCTR };
+
+// One LSpM format on the device: entries of row r are [rp[r], rp[r+1]) sorted by (pred, col).
+template <typename PT>
+struct Fmt {
+  const uint32_t* __restrict__ rp;
+  const uint32_t* __restrict__ col;
+  const PT* __restrict__ pred;
+};
+
+__device__ __forceinline__ uint32_t bit_of(const uint32_t* __restrict__ bm, uint32_t i) {
+  return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+// [lo, hi) = entries of row r with label l (binary search on the sorted pred run).
+template <typename PT>
+__device__ __forceinline__ void label_range(const Fmt<PT>& f, uint32_t r, uint32_t l, uint32_t& lo,
+                                            uint32_t& hi) {
+  uint32_t a = __ldg(f.rp + r), e = __ldg(f.rp + r + 1), z = e;
+  while (a < z) {
+    uint32_t m = (a + z) >> 1;
+    if ((uint32_t)__ldg(f.pred + m) < l) a = m + 1; else z = m;
+  }
+  lo = a; z = e;
+  while (a < z) {
+    uint32_t m = (a + z) >> 1;
+    if ((uint32_t)__ldg(f.pred + m) <= l) a = m + 1; else z = m;
+  }
+  hi = a;
+}
+
+// Is (r, l, target) an entry?  (membership of target in seg_l(r))
+template <typename PT>
+__device__ __forceinline__ bool has_entry(const Fmt<PT>& f, uint32_t r, uint32_t l, uint32_t target) {
+  uint32_t lo, hi;
+  label_range(f, r, l, lo, hi);
+  while (lo < hi) {
+    uint32_t m = (lo + hi) >> 1;
+    uint32_t c = __ldg(f.col + m);
+    if (c < target) lo = m + 1; else if (c > target) hi = m; else return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim.x <= 1024, multiple of 32).
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem /* >= 32 */, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(GSM_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? smem[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(GSM_FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) smem[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  T warp_off = wid ? smem[wid - 1] : T(0);
+  if (total) *total = smem[nw - 1];
+  T r = warp_off + x - v;
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_reduce_sum(T v, T* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(GSM_FULL, v, o);
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (wid == 0) {
+    r = lane < nw ? smem[lane] : T(0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(GSM_FULL, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+}  // namespace gsm

@@ -1,0 +1,817 @@
+// sm_100a kernels of the gSmart hot path (§5-§8).
+// Every kernel here is HBM/L2-bound integer/boolean work: no tensor cores
+// (not a dense contraction — BASELINE.json north_star).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "kernels.h"
+
+namespace gsm {
+
+static inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 1u << 30) {
+  uint64_t g = (n + block - 1) / block;
+  if (g == 0) g = 1;
+  return (unsigned)(g > cap ? cap : g);
+}
+
+// =====================================================================================
+// Scans (reduce-then-scan; tile = 256 threads x 8 items)
+// =====================================================================================
+constexpr int SB = 256, SI = 8, ST = SB * SI;
+
+__global__ void __launch_bounds__(SB) k_scan_reduce(const uint32_t* __restrict__ in, uint64_t n,
+                                                   unsigned long long* __restrict__ partial) {
+  __shared__ unsigned long long sm[32];
+  uint64_t base = (uint64_t)blockIdx.x * ST + (uint64_t)threadIdx.x * SI;
+  unsigned long long s = 0;
+#pragma unroll
+  for (int i = 0; i < SI; i++)
+    if (base + i < n) s += in[base + i];
+  s = block_reduce_sum<unsigned long long>(s, sm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// single block: exclusive scan of np partials in place (carry loop), total -> *total
+__global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __restrict__ partial, uint64_t np,
+                                                        unsigned long long* __restrict__ total) {
+  __shared__ unsigned long long sm[32];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < np; base += blockDim.x) {
+    uint64_t i = base + threadIdx.x;
+    unsigned long long v = i < np ? partial[i] : 0ull, tot;
+    unsigned long long ex = block_exclusive_scan<unsigned long long>(v, sm, &tot);
+    if (i < np) partial[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(SB) k_scan_apply(const uint32_t* in, uint32_t* out, uint64_t n,
+                                                  const unsigned long long* __restrict__ partial) {
+  __shared__ unsigned long long sm[32];
+  uint64_t base = (uint64_t)blockIdx.x * ST + (uint64_t)threadIdx.x * SI;
+  uint32_t v[SI];
+  unsigned long long s = 0;
+#pragma unroll
+  for (int i = 0; i < SI; i++) {
+    v[i] = base + i < n ? in[base + i] : 0u;
+    s += v[i];
+  }
+  unsigned long long ex = block_exclusive_scan<unsigned long long>(s, sm, nullptr) + partial[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SI; i++) {
+    if (base + i < n) out[base + i] = (uint32_t)ex;
+    ex += v[i];
+  }
+}
+
+size_t scan_tmp_bytes(uint64_t n) {
+  uint64_t np = (n + ST - 1) / ST;
+  return (np + 1) * sizeof(unsigned long long) + 256;
+}
+
+cudaError_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total_dev,
+                               void* tmp, cudaStream_t st, int* launches) {
+  uint64_t np = (n + ST - 1) / ST;
+  if (np == 0) np = 1;
+  auto* partial = (unsigned long long*)tmp;
+  k_scan_reduce<<<(unsigned)np, SB, 0, st>>>(in, n, partial);
+  k_scan_partials<<<1, 1024, 0, st>>>(partial, np, total_dev);
+  k_scan_apply<<<(unsigned)np, SB, 0, st>>>(in, out, n, partial);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a1 — LSpM build (§6.2): key pack -> radix sort -> unique -> unpack + row counts
+// key = row << sh_row | pred << sh_pred | col ; bit drop_bit set = filtered out
+// =====================================================================================
+__global__ void k_pack_keys(const uint32_t* __restrict__ rowv, const uint32_t* __restrict__ p,
+                            const uint32_t* __restrict__ colv, uint64_t n, const uint8_t* __restrict__ keep,
+                            int sh_row, int sh_pred, int drop_bit, uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t r = __ldg(rowv + i), l = __ldg(p + i), c = __ldg(colv + i);
+    uint64_t k = ((uint64_t)r << sh_row) | ((uint64_t)l << sh_pred) | (uint64_t)c;
+    if (!__ldg(keep + l)) k |= 1ull << drop_bit;
+    keys[i] = k;
+  }
+}
+
+cudaError_t launch_pack_keys(const uint32_t* rowv, const uint32_t* p, const uint32_t* colv, uint64_t n,
+                             const uint8_t* keep, int sh_row, int sh_pred, int drop_bit, uint64_t* keys,
+                             cudaStream_t st) {
+  k_pack_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(rowv, p, colv, n, keep, sh_row, sh_pred, drop_bit, keys);
+  return cudaGetLastError();
+}
+
+size_t sort_keys_tmp_bytes(uint64_t n, int end_bit) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)n, 0,
+                                 end_bit);
+  return bytes;
+}
+
+cudaError_t sort_keys_u64(void* tmp, size_t tmp_bytes, const uint64_t* in, uint64_t* out, uint64_t n, int end_bit,
+                          cudaStream_t st) {
+  return cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, in, out, (int64_t)n, 0, end_bit, st);
+}
+
+__global__ void k_unique_flags(const uint64_t* __restrict__ keys, uint64_t n, int drop_bit,
+                               uint32_t* __restrict__ flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    bool keepk = !((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k);
+    flags[i] = keepk ? 1u : 0u;
+  }
+}
+
+cudaError_t launch_unique_flags(const uint64_t* keys, uint64_t n, int drop_bit, uint32_t* flags, cudaStream_t st) {
+  k_unique_flags<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, drop_bit, flags);
+  return cudaGetLastError();
+}
+
+template <typename PT>
+__global__ void k_unpack(const uint64_t* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ pos,
+                         int drop_bit, int sh_row, int sh_pred, uint32_t* __restrict__ col, PT* __restrict__ pred,
+                         uint32_t* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t pmask = (1ull << (sh_row - sh_pred)) - 1, cmask = (1ull << sh_pred) - 1;
+  // all lanes iterate the same number of times (warp-aggregated row counting)
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
+    uint64_t i = base + threadIdx.x;
+    bool valid = false;
+    uint32_t row = 0xffffffffu;
+    if (i < n) {
+      uint64_t k = keys[i];
+      valid = !((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k);
+      if (valid) {
+        uint32_t q = pos[i];
+        row = (uint32_t)(k >> sh_row);
+        col[q] = (uint32_t)(k & cmask);
+        pred[q] = (PT)((k >> sh_pred) & pmask);
+      }
+    }
+    uint32_t peers = __match_any_sync(GSM_FULL, row);
+    uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
+    int leader = __ffs(peers) - 1;
+    if (valid && (threadIdx.x & 31) == leader) atomicAdd(counts + row, cnt);
+  }
+}
+
+cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int sh_row,
+                          int sh_pred, uint32_t* col, void* pred, int pred_bytes, uint32_t* counts,
+                          cudaStream_t st) {
+  unsigned g = grid_for(n, 256, 148 * 32);
+  if (pred_bytes == 1)
+    k_unpack<uint8_t><<<g, 256, 0, st>>>(keys, n, pos, drop_bit, sh_row, sh_pred, col, (uint8_t*)pred, counts);
+  else
+    k_unpack<uint16_t><<<g, 256, 0, st>>>(keys, n, pos, drop_bit, sh_row, sh_pred, col, (uint16_t*)pred, counts);
+  return cudaGetLastError();
+}
+
+__global__ void k_heavy_stats(const uint32_t* __restrict__ rp, uint32_t n_rows, unsigned long long* out2) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+    uint32_t len = rp[r + 1] - rp[r];
+    if (len > HEAVY_ROW) {
+      atomicAdd(out2, 1ull);
+      atomicAdd(out2 + 1, (unsigned long long)((len + HEAVY_CHUNK - 1) / HEAVY_CHUNK));
+    }
+  }
+}
+
+cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned long long* out2, cudaStream_t st) {
+  k_heavy_stats<<<grid_for(n_rows, 256, 148 * 16), 256, 0, st>>>(rp, n_rows, out2);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// bitmaps
+// =====================================================================================
+// all-ones over bits [0, n_bits), zero beyond (padding words included)
+__global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
+    uint64_t lo = (uint64_t)w * 32;
+    uint32_t v;
+    if (lo >= n_bits) v = 0u;
+    else if (lo + 32 <= n_bits) v = 0xffffffffu;
+    else v = (1u << (n_bits - lo)) - 1u;
+    bm[w] = v;
+  }
+}
+
+cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st) {
+  k_fill_ones<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(bm, n_words, n_bits);
+  return cudaGetLastError();
+}
+
+__global__ void k_and_inplace(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n_words) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x)
+    dst[w] &= __ldg(src + w);
+}
+
+cudaError_t launch_and_inplace(uint32_t* dst, const uint32_t* src, uint32_t n_words, cudaStream_t st) {
+  k_and_inplace<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(dst, src, n_words);
+  return cudaGetLastError();
+}
+
+__global__ void k_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag) {
+  if (*flag) return;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < n_words; w += (uint64_t)gridDim.x * blockDim.x)
+    bm[w] = 0;
+}
+
+cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag, cudaStream_t st) {
+  k_zero_if_flag<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(bm, n_words, flag);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a3 — constant seeding ("light" edges): bits |= {col : (c, l, col)}
+// =====================================================================================
+template <typename PT>
+__global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __restrict__ bits,
+                               unsigned long long* ctr) {
+  __shared__ uint32_t s_lo, s_hi;
+  if (threadIdx.x == 0) {
+    uint32_t lo, hi;
+    label_range(f, c, l, lo, hi);
+    s_lo = lo; s_hi = hi;
+    if (blockIdx.x == 0) atomicAdd(ctr + C_SEED, (unsigned long long)(hi - lo));
+  }
+  __syncthreads();
+  const uint32_t lo = s_lo, hi = s_hi;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = lo + warp * 32; base < hi; base += nwarps * 32) {
+    uint32_t k = base + lane;
+    bool valid = k < hi;
+    uint32_t id = valid ? __ldg(f.col + k) : 0u;
+    uint32_t word = valid ? (id >> 5) : 0xffffffffu;
+    uint32_t peers = __match_any_sync(GSM_FULL, word);
+    uint32_t orv = __reduce_or_sync(peers, valid ? (1u << (id & 31)) : 0u);
+    if (valid && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
+  }
+}
+
+template <typename PT>
+__host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
+  Fmt<PT> f;
+  f.rp = a.rp; f.col = a.col; f.pred = (const PT*)a.pred;
+  return f;
+}
+
+cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
+                                unsigned long long* ctr, int sm_count, cudaStream_t st) {
+  unsigned g = (unsigned)sm_count * 4;
+  if (pred_bytes == 1) k_seed_scatter<uint8_t><<<g, 256, 0, st>>>(fmt_of<uint8_t>(f), c, label, bits, ctr);
+  else k_seed_scatter<uint16_t><<<g, 256, 0, st>>>(fmt_of<uint16_t>(f), c, label, bits, ctr);
+  return cudaGetLastError();
+}
+
+template <typename PT>
+__global__ void k_guard(Fmt<PT> f, uint32_t s, uint32_t l, uint32_t o, int* flag) {
+  if (!has_entry(f, s, l, o)) *flag = 0;
+}
+
+cudaError_t launch_guard(FmtAny f, int pred_bytes, uint32_t s, uint32_t label, uint32_t o, int* flag,
+                         cudaStream_t st) {
+  if (pred_bytes == 1) k_guard<uint8_t><<<1, 1, 0, st>>>(fmt_of<uint8_t>(f), s, label, o, flag);
+  else k_guard<uint16_t><<<1, 1, 0, st>>>(fmt_of<uint16_t>(f), s, label, o, flag);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a4 — grouped incident-edge evaluation (§5, Eqs. 17/21): for every candidate row i
+// of the center x and every group edge e = (l, dir, w):
+//   y_e(i) = OR_{j in seg^dir_l(i)} cand_w(j)      (self-loop: j == i)
+//   cand_x(i) <- cand_x(i) AND (AND_e y_e(i))
+// One warp owns one 32-bit bitmap word (32 consecutive rows) in each direction:
+//  - rows <= SHORT_ROW entries: each lane scans its own row (entries sorted by
+//    (pred, col): stop once every edge is satisfied or labels pass the max);
+//  - longer rows: the whole warp scans the row with coalesced 32-entry strides;
+//  - rows > HEAVY_ROW: deferred to chunked CTAs (k_filter_heavy) + finalize.
+// =====================================================================================
+template <typename PT>
+struct FilterArgsT {
+  Fmt<PT> f[2];
+  GEdge e[2][MAXG];
+  uint32_t ne[2];
+  uint32_t minl[2], maxl[2];
+  uint32_t* cand;
+  uint32_t n_words;
+  uint32_t* heavy_rows;
+  uint32_t* heavy_chunks;
+  uint32_t* heavy_sat;
+  uint32_t* heavy_count;
+  unsigned long long* ctr;
+};
+
+template <typename PT>
+__device__ __forceinline__ uint32_t match_entry(const FilterArgsT<PT>& a, int d, uint32_t l, uint32_t c,
+                                                uint32_t row, uint32_t sat, uint32_t& matched) {
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < MAXG; j++) {
+    if (j >= (int)a.ne[d]) break;
+    if (l == a.e[d][j].label && !((sat >> j) & 1u)) {
+      matched++;
+      bool ok = a.e[d][j].self ? (c == row) : (bit_of(a.e[d][j].nbr, c) != 0);
+      if (ok) s |= 1u << j;
+    }
+  }
+  return s;
+}
+
+template <typename PT>
+__global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long n_rows = 0, n_scanned = 0;
+  uint32_t n_matched = 0;
+  for (uint32_t w = warp; w < a.n_words; w += nwarps) {
+    const uint32_t m = a.cand[w];
+    if (m == 0) continue;
+    const uint32_t row = (w << 5) + lane;
+    bool ok = (m >> lane) & 1u;
+#pragma unroll
+    for (int d = 0; d < 2; d++) {
+      if (a.ne[d] == 0) continue;
+      const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
+      uint32_t b = 0, e = 0, sat = 0;
+      bool medium = false;
+      if (ok) {
+        b = __ldg(a.f[d].rp + row);
+        e = __ldg(a.f[d].rp + row + 1);
+        n_rows++;
+        uint32_t len = e - b;
+        if (len > HEAVY_ROW) {
+          // defer: provisional keep; chunks OR their satisfied edges into heavy_sat[slot]
+          uint32_t slot = atomicAdd(a.heavy_count, 1u);
+          uint32_t nch = (len + HEAVY_CHUNK - 1) / HEAVY_CHUNK;
+          uint32_t c0 = atomicAdd(a.heavy_count + 1, nch);
+          a.heavy_rows[slot] = row | ((uint32_t)d << 31);
+          for (uint32_t c = 0; c < nch; c++) {
+            a.heavy_chunks[2 * (c0 + c)] = slot;
+            a.heavy_chunks[2 * (c0 + c) + 1] = c;
+          }
+          sat = need;
+        } else if (len > SHORT_ROW) {
+          medium = true;
+        } else {
+          for (uint32_t k = b; k < e && sat != need; k++) {
+            uint32_t l = __ldg(a.f[d].pred + k);
+            n_scanned++;
+            if (l < a.minl[d]) continue;
+            if (l > a.maxl[d]) break;
+            sat |= match_entry(a, d, l, __ldg(a.f[d].col + k), row, sat, n_matched);
+          }
+        }
+      }
+      // warp-cooperative scan of medium rows, one row at a time
+      uint32_t mm = __ballot_sync(GSM_FULL, medium);
+      while (mm) {
+        const int src = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const uint32_t rb = __shfl_sync(GSM_FULL, b, src), re = __shfl_sync(GSM_FULL, e, src);
+        const uint32_t rrow = (w << 5) + src;
+        uint32_t wsat = 0;
+        for (uint32_t base = rb; base < re; base += 32) {
+          uint32_t k = base + lane;
+          uint32_t s = 0;
+          if (k < re) {
+            uint32_t l = __ldg(a.f[d].pred + k);
+            n_scanned++;
+            if (l >= a.minl[d] && l <= a.maxl[d])
+              s = match_entry(a, d, l, __ldg(a.f[d].col + k), rrow, wsat, n_matched);
+          }
+          wsat |= __reduce_or_sync(GSM_FULL, s);
+          if (wsat == need) break;
+        }
+        if ((int)lane == src) sat = wsat;
+      }
+      ok = ok && (sat == need);
+    }
+    const uint32_t nw = __ballot_sync(GSM_FULL, ok);
+    if (lane == 0 && nw != m) a.cand[w] = nw;
+  }
+  // one atomic per warp per counter
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
+    n_scanned += __shfl_down_sync(GSM_FULL, n_scanned, o);
+    n_matched += __shfl_down_sync(GSM_FULL, n_matched, o);
+  }
+  if (lane == 0) {
+    if (n_rows) atomicAdd(a.ctr + C_FILTER_ROWS, n_rows);
+    if (n_scanned) atomicAdd(a.ctr + C_FILTER_SCANNED, n_scanned);
+    if (n_matched) atomicAdd(a.ctr + C_FILTER_MATCHED, (unsigned long long)n_matched);
+  }
+}
+
+// heavy-row chunks: CTA per chunk, OR of satisfied edge bits into heavy_sat[slot]
+template <typename PT>
+__global__ void __launch_bounds__(256) k_filter_heavy(FilterArgsT<PT> a) {
+  __shared__ uint32_t s_sat;
+  const uint32_t nch = a.heavy_count[1];
+  for (uint32_t it = blockIdx.x; it < nch; it += gridDim.x) {
+    const uint32_t slot = a.heavy_chunks[2 * it], c = a.heavy_chunks[2 * it + 1];
+    const uint32_t rec = a.heavy_rows[slot];
+    const uint32_t row = rec & 0x7fffffffu;
+    const int d = (int)(rec >> 31);
+    const uint32_t b0 = a.f[d].rp[row], e0 = a.f[d].rp[row + 1];
+    const uint32_t b = b0 + c * HEAVY_CHUNK, e = min(e0, b + HEAVY_CHUNK);
+    if (threadIdx.x == 0) s_sat = 0;
+    __syncthreads();
+    uint32_t sat = 0, matched = 0;
+    for (uint32_t k = b + threadIdx.x; k < e; k += blockDim.x) {
+      uint32_t l = __ldg(a.f[d].pred + k);
+      if (l >= a.minl[d] && l <= a.maxl[d]) sat |= match_entry(a, d, l, __ldg(a.f[d].col + k), row, 0u, matched);
+    }
+    sat = __reduce_or_sync(GSM_FULL, sat);
+    if ((threadIdx.x & 31) == 0 && sat) atomicOr(&s_sat, sat);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_sat) atomicOr(a.heavy_sat + slot, s_sat);
+      atomicAdd(a.ctr + C_HEAVY, (unsigned long long)(e - b));
+      atomicAdd(a.ctr + C_FILTER_SCANNED, (unsigned long long)(e - b));
+    }
+    __syncthreads();
+  }
+}
+
+template <typename PT>
+__global__ void k_filter_finalize(FilterArgsT<PT> a) {
+  const uint32_t nr = a.heavy_count[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+    const uint32_t rec = a.heavy_rows[i];
+    const uint32_t row = rec & 0x7fffffffu;
+    const int d = (int)(rec >> 31);
+    const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
+    if (a.heavy_sat[i] != need) atomicAnd(a.cand + (row >> 5), ~(1u << (row & 31)));
+  }
+}
+
+template <typename PT>
+static FilterArgsT<PT> to_t(const FilterArgs& a) {
+  FilterArgsT<PT> t;
+  for (int d = 0; d < 2; d++) {
+    t.f[d] = fmt_of<PT>(a.f[d]);
+    t.ne[d] = a.ne[d];
+    t.minl[d] = 0xffffffffu; t.maxl[d] = 0;
+    for (int j = 0; j < MAXG; j++) {
+      t.e[d][j] = a.e[d][j];
+      if (j < (int)a.ne[d]) {
+        t.minl[d] = min(t.minl[d], a.e[d][j].label);
+        t.maxl[d] = max(t.maxl[d], a.e[d][j].label);
+      }
+    }
+  }
+  t.cand = a.cand; t.n_words = a.n_words;
+  t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
+  t.heavy_count = a.heavy_count; t.ctr = a.ctr;
+  return t;
+}
+
+template <typename PT>
+static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_t st, int* launches) {
+  FilterArgsT<PT> t = to_t<PT>(a);
+  // 8 warps per CTA; enough CTAs for ~16 resident warps/SM-worth of words, grid-stride beyond
+  uint64_t want = ((uint64_t)a.n_words + 7) / 8;
+  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
+  k_group_filter<PT><<<g, 256, 0, st>>>(t);
+  k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
+  k_filter_finalize<PT><<<(unsigned)sm_count, 256, 0, st>>>(t);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_count, cudaStream_t st,
+                                int* launches) {
+  return pred_bytes == 1 ? group_filter_t<uint8_t>(a, sm_count, st, launches)
+                         : group_filter_t<uint16_t>(a, sm_count, st, launches);
+}
+
+// =====================================================================================
+// a5 — compaction: bitmap -> ascending ids (popc per thread, block scan, tile offsets)
+// tile = 256 threads x 8 words
+// =====================================================================================
+constexpr int CW = 8, CB = 256, CT = CB * CW;
+
+__global__ void __launch_bounds__(CB) k_bitmap_count(const uint32_t* __restrict__ bm, uint32_t n_words,
+                                                    uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t sm[32];
+  uint64_t base = (uint64_t)blockIdx.x * CT + threadIdx.x * CW;
+  uint32_t c = 0;
+  if (base + CW <= n_words) {
+    uint4 a = *reinterpret_cast<const uint4*>(bm + base);
+    uint4 b = *reinterpret_cast<const uint4*>(bm + base + 4);
+    c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) + __popc(b.z) +
+        __popc(b.w);
+  } else {
+    for (int i = 0; i < CW; i++)
+      if (base + i < n_words) c += __popc(bm[base + i]);
+  }
+  c = block_reduce_sum<uint32_t>(c, sm);
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(CB) k_bitmap_emit(const uint32_t* __restrict__ bm, uint32_t n_words,
+                                                   const uint32_t* __restrict__ tile_off, uint32_t* __restrict__ ids) {
+  __shared__ uint32_t sm[32];
+  uint64_t base = (uint64_t)blockIdx.x * CT + threadIdx.x * CW;
+  uint32_t wv[CW];
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < CW; i++) {
+    wv[i] = base + i < n_words ? bm[base + i] : 0u;
+    c += __popc(wv[i]);
+  }
+  uint32_t off = block_exclusive_scan<uint32_t>(c, sm, nullptr) + tile_off[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < CW; i++) {
+    uint32_t x = wv[i];
+    while (x) {
+      int b = __ffs(x) - 1;
+      x &= x - 1;
+      ids[off++] = (uint32_t)((base + i) * 32 + b);
+    }
+  }
+}
+
+size_t compact_tmp_bytes(uint32_t n_words) {
+  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT + 1;
+  return ((nt * sizeof(uint32_t) + 255) / 256) * 256 + scan_tmp_bytes(nt) + 512;
+}
+
+cudaError_t compact_count(const uint32_t* bm, uint32_t n_words, unsigned long long* count_dev, void* tmp,
+                          cudaStream_t st, int* launches) {
+  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT;
+  if (nt == 0) nt = 1;
+  uint32_t* tile = (uint32_t*)tmp;
+  void* stmp = (char*)tmp + ((nt * sizeof(uint32_t) + 255) / 256) * 256;
+  k_bitmap_count<<<(unsigned)nt, CB, 0, st>>>(bm, n_words, tile);
+  if (launches) *launches += 1;
+  return scan_exclusive_u32(tile, tile, nt, count_dev, stmp, st, launches);
+}
+
+cudaError_t compact_emit(const uint32_t* bm, uint32_t n_words, uint32_t* ids, void* tmp, cudaStream_t st,
+                         int* launches) {
+  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT;
+  if (nt == 0) nt = 1;
+  k_bitmap_emit<<<(unsigned)nt, CB, 0, st>>>(bm, n_words, (const uint32_t*)tmp, ids);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a6/a7 — tree expansion (§7.1, Alg. 1 l.5 / Alg. 2 l.7): level k children of each
+// level k-1 node n are the entries c of seg^dir_label(b_parent(n)) (or the candidate
+// list for a free level) with cand_v(c) (pre-pruning: bindings that failed the
+// grouped evaluation never enter the trie, §7.2.2) and every closing edge present.
+// count -> scan -> emit over work items of <= EXP_CHUNK entries.
+// =====================================================================================
+__device__ __forceinline__ uint32_t ancestor_bind(const LevelTab& t, uint32_t k, uint32_t n, uint32_t j) {
+  while (k > j) {
+    n = __ldg(t.parent[k] + n);
+    k--;
+  }
+  return __ldg(t.bind[j] + n);
+}
+
+template <typename PT>
+__global__ void k_expand_seg(ExpandArgs a) {
+  Fmt<PT> f = fmt_of<PT>(a.f[a.dir & 1]);
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < a.n_parents; n += gridDim.x * blockDim.x) {
+    uint32_t beg = 0, len = a.list_len;
+    if (a.tree) {
+      uint32_t b = ancestor_bind(a.tab, a.k - 1, n, a.parent_level);
+      uint32_t lo, hi;
+      label_range(f, b, a.label, lo, hi);
+      beg = lo; len = hi - lo;
+    }
+    a.seg_beg[n] = beg;
+    a.seg_len[n] = len;
+    a.item_off[n] = (len + EXP_CHUNK - 1) / EXP_CHUNK;
+  }
+}
+
+cudaError_t launch_expand_seg(const ExpandArgs& a, int pred_bytes, cudaStream_t st) {
+  unsigned g = grid_for(a.n_parents, 256, 148 * 32);
+  if (pred_bytes == 1) k_expand_seg<uint8_t><<<g, 256, 0, st>>>(a);
+  else k_expand_seg<uint16_t><<<g, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void k_items_fill(ExpandArgs a) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < a.n_parents; n += gridDim.x * blockDim.x) {
+    uint32_t cnt = (a.seg_len[n] + EXP_CHUNK - 1) / EXP_CHUNK, off = a.item_off[n];
+    for (uint32_t i = 0; i < cnt; i++) a.item_node[off + i] = n;
+  }
+}
+
+cudaError_t launch_items_fill(const ExpandArgs& a, cudaStream_t st) {
+  k_items_fill<<<grid_for(a.n_parents, 256, 148 * 32), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename PT, bool EMIT>
+__global__ void __launch_bounds__(256) k_expand_pass(ExpandArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  Fmt<PT> fsrc = fmt_of<PT>(a.f[a.dir & 1]);
+  Fmt<PT> fc[2] = {fmt_of<PT>(a.f[0]), fmt_of<PT>(a.f[1])};
+  unsigned long long n_exam = 0, n_close = 0;
+  for (uint32_t it = warp; it < a.n_items; it += nwarps) {
+    const uint32_t n = a.item_node[it];
+    const uint32_t chunk = it - a.item_off[n];
+    const uint32_t sb = a.seg_beg[n], sl = a.seg_len[n];
+    const uint32_t beg = sb + chunk * EXP_CHUNK, end = min(sb + sl, beg + EXP_CHUNK);
+    // closing-edge targets: binding of the other endpoint (lane j computes closing j)
+    uint32_t tgt = 0;
+    if (lane < a.ncl && a.cl[lane].self == 0) tgt = ancestor_bind(a.tab, a.k - 1, n, a.cl[lane].other_level);
+    uint32_t out = 0;
+    if (EMIT) out = a.item_cnt[it];
+    for (uint32_t base = beg; base < end; base += 32) {
+      const uint32_t kk = base + lane;
+      const bool valid = kk < end;
+      uint32_t child = 0;
+      bool keep = false;
+      if (valid) {
+        child = a.tree ? __ldg(fsrc.col + kk) : __ldg(a.list + kk);
+        keep = bit_of(a.cand, child) != 0;
+        n_exam++;
+      }
+      for (uint32_t j = 0; j < a.ncl; j++) {
+        const uint32_t t = __shfl_sync(GSM_FULL, tgt, j);
+        if (keep) {
+          const ClosingDev c = a.cl[j];
+          keep = has_entry(fc[c.dir & 1], child, c.label, c.self ? child : t);
+          n_close++;
+        }
+      }
+      const uint32_t bal = __ballot_sync(GSM_FULL, keep);
+      if (EMIT && keep) {
+        const uint32_t pos = out + __popc(bal & lanemask_lt());
+        a.out_parent[pos] = n;
+        a.out_bind[pos] = child;
+      }
+      out += __popc(bal);
+    }
+    if (!EMIT && lane == 0) a.item_cnt[it] = out;
+  }
+  if (!EMIT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n_exam += __shfl_down_sync(GSM_FULL, n_exam, o);
+      n_close += __shfl_down_sync(GSM_FULL, n_close, o);
+    }
+    if (lane == 0) {
+      if (n_exam) atomicAdd(a.ctr + C_EXPAND, n_exam);
+      if (n_close) atomicAdd(a.ctr + C_CLOSING, n_close);
+    }
+  }
+}
+
+cudaError_t launch_expand_pass(const ExpandArgs& a, int pred_bytes, bool emit, int sm_count, cudaStream_t st) {
+  uint64_t want = ((uint64_t)a.n_items + 7) / 8;
+  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
+  if (pred_bytes == 1) {
+    if (emit) k_expand_pass<uint8_t, true><<<g, 256, 0, st>>>(a);
+    else k_expand_pass<uint8_t, false><<<g, 256, 0, st>>>(a);
+  } else {
+    if (emit) k_expand_pass<uint16_t, true><<<g, 256, 0, st>>>(a);
+    else k_expand_pass<uint16_t, false><<<g, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a8 — bottom-up tree pruning (§8.1 steps 3-4): a node survives iff some
+// child survives; the last level is all alive.  Byte stores are race-benign.
+// =====================================================================================
+__global__ void k_prune_mark(const uint32_t* __restrict__ parent, const uint8_t* __restrict__ alive, uint32_t n,
+                             uint8_t* __restrict__ alive_prev) {
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x)
+    if (!alive || alive[m]) alive_prev[parent[m]] = 1;
+}
+
+cudaError_t launch_prune_mark(const uint32_t* parent, const uint8_t* alive, uint32_t n, uint8_t* alive_prev,
+                              cudaStream_t st) {
+  k_prune_mark<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(parent, alive, n, alive_prev);
+  return cudaGetLastError();
+}
+
+__global__ void k_u8_to_u32(const uint8_t* in, uint32_t* out, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
+}
+
+cudaError_t launch_u8_to_u32(const uint8_t* in, uint32_t* out, uint32_t n, cudaStream_t st) {
+  k_u8_to_u32<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_compact_level(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ bind,
+                                const uint8_t* __restrict__ alive, const uint32_t* __restrict__ newpos,
+                                const uint32_t* __restrict__ newidx_prev, uint32_t n, uint32_t* __restrict__ out_parent,
+                                uint32_t* __restrict__ out_bind) {
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    if (alive && !alive[m]) continue;
+    uint32_t q = newpos ? newpos[m] : m;
+    out_bind[q] = bind[m];
+    if (parent && out_parent) out_parent[q] = newidx_prev ? newidx_prev[parent[m]] : parent[m];
+  }
+}
+
+cudaError_t launch_compact_level(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
+                                 const uint32_t* newpos, const uint32_t* newidx_prev, uint32_t n,
+                                 uint32_t* out_parent, uint32_t* out_bind, cudaStream_t st) {
+  k_compact_level<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(parent, bind, alive, newpos, newidx_prev, n,
+                                                              out_parent, out_bind);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// a9 — row enumeration (one row per surviving leaf) and lexicographic sort
+// =====================================================================================
+struct ColMap {
+  uint32_t c[MAXL];
+};
+
+__global__ void k_enumerate(LevelTab t, uint32_t L, ColMap cm, uint32_t n_last, uint32_t n_cols,
+                            uint32_t* __restrict__ rows) {
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n_last; m += gridDim.x * blockDim.x) {
+    uint32_t idx = m;
+    uint32_t* r = rows + (uint64_t)m * n_cols;
+    for (int k = (int)L - 1; k >= 0; k--) {
+      r[cm.c[k]] = __ldg(t.bind[k] + idx);
+      if (k > 0) idx = __ldg(t.parent[k] + idx);
+    }
+  }
+}
+
+cudaError_t launch_enumerate(const LevelTab& tab, uint32_t n_levels, const uint32_t* col_of_level, uint32_t n_last,
+                             uint32_t n_cols, uint32_t* rows, cudaStream_t st) {
+  ColMap cm;
+  for (uint32_t k = 0; k < MAXL; k++) cm.c[k] = k < n_levels ? col_of_level[k] : 0;
+  k_enumerate<<<grid_for(n_last, 256, 148 * 32), 256, 0, st>>>(tab, n_levels, cm, n_last, n_cols, rows);
+  return cudaGetLastError();
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_col(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
+                             uint32_t n_cols, uint32_t c, uint32_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = rows[(uint64_t)perm[i] * n_cols + c];
+}
+
+__global__ void k_gather_rows(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
+                              uint32_t n_cols, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * n_cols;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = i / n_cols, c = i - r * n_cols;
+    out[i] = rows[(uint64_t)perm[r] * n_cols + c];
+  }
+}
+
+size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0, 32);
+  (void)n_cols;
+  return 4 * ((n * 4 + 255) / 256) * 256 + cub_bytes + 256;
+}
+
+// LSD radix over columns (stable), last column first.
+cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, int key_bits,
+                      void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches) {
+  size_t seg = ((n * 4 + 255) / 256) * 256;
+  uint32_t* perm = (uint32_t*)tmp;
+  uint32_t* perm2 = (uint32_t*)((char*)tmp + seg);
+  uint32_t* keys = (uint32_t*)((char*)tmp + 2 * seg);
+  uint32_t* keys2 = (uint32_t*)((char*)tmp + 3 * seg);
+  void* ctmp = (char*)tmp + 4 * seg;
+  size_t cbytes = tmp_bytes - 4 * seg;
+  unsigned g = grid_for(n, 256, 148 * 32);
+  k_iota<<<g, 256, 0, st>>>(perm, n);
+  int nl = 1;
+  for (int c = (int)n_cols - 1; c >= 0; c--) {
+    k_gather_col<<<g, 256, 0, st>>>(rows, perm, n, n_cols, (uint32_t)c, keys);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(ctmp, cbytes, keys, keys2, perm, perm2, (int64_t)n, 0,
+                                                    key_bits, st);
+    if (e != cudaSuccess) return e;
+    std::swap(perm, perm2);
+    nl += 2;
+  }
+  k_gather_rows<<<grid_for(n * n_cols, 256, 148 * 32), 256, 0, st>>>(rows, perm, n, n_cols, rows_out);
+  if (launches) *launches += nl + 1;
+  return cudaGetLastError();
+}
+
+}  // namespace gsm

@@ -1,0 +1,36 @@
+#include "nccl_shim.h"
+
+#include <dlfcn.h>
+#include <mutex>
+
+namespace gsm {
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool ok = false;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define LOAD(field, sym)                                      \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, sym)); \
+  if (!api.field) return;
+    LOAD(GetUniqueId, "ncclGetUniqueId");
+    LOAD(CommInitRank, "ncclCommInitRank");
+    LOAD(CommDestroy, "ncclCommDestroy");
+    LOAD(AllGather, "ncclAllGather");
+    LOAD(Send, "ncclSend");
+    LOAD(Recv, "ncclRecv");
+    LOAD(AllReduce, "ncclAllReduce");
+    LOAD(GroupStart, "ncclGroupStart");
+    LOAD(GroupEnd, "ncclGroupEnd");
+    LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+    ok = true;
+  });
+  return ok ? &api : nullptr;
+}
+
+}  // namespace gsm

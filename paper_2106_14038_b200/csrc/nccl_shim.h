@@ -1,0 +1,22 @@
+// NCCL loaded at run time (dlopen) so the library has no link-time NCCL
+// dependency: single-GPU use and CPU-only tests never touch NCCL, and inside a
+// torch process the already-loaded libnccl.so.2 is reused.
+#pragma once
+#include <nccl.h>
+
+namespace gsm {
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+// nullptr if libnccl.so.2 cannot be loaded
+const NcclApi* nccl_api();
+}  // namespace gsm

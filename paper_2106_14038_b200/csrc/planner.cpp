@@ -1,0 +1,224 @@
+// Host query planner: degree-driven traversal (§6.1.2)
+// plus the trie order / tree edges / closing edges the level-synchronous
+// executor needs.  Host microseconds; no device work.
+#include <algorithm>
+#include <functional>
+#include <cstdio>
+#include <set>
+#include <sstream>
+
+#include "internal.h"
+
+namespace gsm {
+
+gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* P, std::string* err) {
+  if (!q || (q->n_vertices && !q->v) || (q->n_edges && !q->e)) { *err = "null query arrays"; return GSMART_E_INVALID_ARG; }
+  if (traversal == GSMART_DIRECTION) { *err = "direction-driven traversal not supported in this version"; return GSMART_E_UNSUPPORTED; }
+  if (traversal != GSMART_DEGREE) { *err = "unknown traversal"; return GSMART_E_INVALID_ARG; }
+  const uint32_t n = q->n_vertices, ne = q->n_edges;
+  if (ne > 32) { *err = "more than 32 patterns"; return GSMART_E_INVALID_ARG; }
+  P->n_vertices = n;
+  P->vertices.assign(q->v, q->v + n);
+  P->edges.assign(q->e, q->e + ne);
+  for (uint32_t k = 0; k < ne; k++) {
+    const auto& e = q->e[k];
+    if (e.src >= n || e.dst >= n) { *err = "pattern vertex index out of range"; return GSMART_E_INVALID_ARG; }
+    if (e.pred == 0 || e.pred > 65535) { *err = "predicate id must be in [1, 65535]"; return GSMART_E_INVALID_ARG; }
+  }
+  std::vector<bool> is_c(n), used(n, false);
+  P->col_of.assign(n, -1);
+  for (uint32_t i = 0; i < n; i++) {
+    is_c[i] = q->v[i].is_const != 0;
+    if (!is_c[i]) { P->col_of[i] = (int32_t)P->vars.size(); P->vars.push_back(i); }
+  }
+  if (P->vars.size() > GSMART_MAX_LEVELS) { *err = "more than 32 variables"; return GSMART_E_INVALID_ARG; }
+  for (uint32_t k = 0; k < ne; k++) { used[q->e[k].src] = used[q->e[k].dst] = true; }
+  for (uint32_t v : P->vars)
+    if (!used[v]) { *err = "variable vertex occurs in no pattern"; return GSMART_E_INVALID_ARG; }
+
+  // Step 1 (constants variant): W = constants, F = constant-incident edges.
+  std::vector<bool> W(n, false), F(ne, false), const_adj(n, false);
+  for (uint32_t i = 0; i < n; i++) W[i] = is_c[i];
+  for (uint32_t k = 0; k < ne; k++) {
+    const auto& e = q->e[k];
+    bool cs = is_c[e.src], cd = is_c[e.dst];
+    if (cs && cd) { F[k] = true; P->guards.push_back({k, q->v[e.src].const_id, e.pred, q->v[e.dst].const_id}); }
+    else if (cs) { F[k] = true; P->seeds.push_back({k, e.dst, e.pred, q->v[e.src].const_id, OUT}); const_adj[e.dst] = true; }
+    else if (cd) { F[k] = true; P->seeds.push_back({k, e.src, e.pred, q->v[e.dst].const_id, IN}); const_adj[e.src] = true; }
+  }
+  auto unev = [&](uint32_t v) {
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < ne; k++) if (!F[k] && (q->e[k].src == v || q->e[k].dst == v)) c++;
+    return c;
+  };
+  auto unev_out = [&](uint32_t v) {
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < ne; k++) if (!F[k] && q->e[k].src == v) c++;
+    return c;
+  };
+  auto n_unev = [&]() { uint32_t c = 0; for (uint32_t k = 0; k < ne; k++) c += !F[k]; return c; };
+
+  std::vector<uint32_t> depth(n, 0);
+  std::vector<int32_t> first_parent(n, -1);
+  while (n_unev() > 0) {
+    // Step 2: root = max unevaluated edges (among constant neighbours first,
+    // P:L398), then max unevaluated out-edges, then lowest index (R16).
+    int32_t best = -1; bool best_pref = false; uint32_t bu = 0, bo = 0;
+    for (uint32_t v = 0; v < n; v++) {
+      if (W[v]) continue;
+      uint32_t u = unev(v);
+      if (u == 0) continue;
+      uint32_t o = unev_out(v);
+      bool pref = const_adj[v];
+      bool better = best < 0 || (pref && !best_pref) ||
+                    (pref == best_pref && (u > bu || (u == bu && o > bo)));
+      if (better) { best = (int32_t)v; best_pref = pref; bu = u; bo = o; }
+    }
+    uint32_t root = (uint32_t)best;
+    P->roots.push_back(root);
+    W[root] = true; depth[root] = 0; first_parent[root] = -1;
+    std::vector<uint32_t> S{root};
+    while (!S.empty()) {                       // Step 3
+      uint32_t v = S.back(); S.pop_back();
+      Group g; g.center = v; g.level = depth[v];
+      for (uint32_t k = 0; k < ne; k++) {      // Step 4: all unevaluated incident edges
+        if (F[k]) continue;
+        const auto& e = q->e[k];
+        if (e.src == v) g.edges.push_back({k, e.pred, OUT, e.dst});
+        else if (e.dst == v) g.edges.push_back({k, e.pred, IN, e.src});
+      }
+      for (auto& ge : g.edges) F[ge.edge] = true;
+      std::vector<uint32_t> fresh;
+      for (auto& ge : g.edges) {
+        uint32_t w = ge.nbr;
+        if (!W[w]) { W[w] = true; depth[w] = depth[v] + 1; first_parent[w] = (int32_t)v; fresh.push_back(w); }
+      }
+      // push ascending (unevaluated, unevaluated-out, index): the largest pops first (R16)
+      std::sort(fresh.begin(), fresh.end(), [&](uint32_t a, uint32_t b) {
+        uint32_t ua = unev(a), ub = unev(b);
+        if (ua != ub) return ua < ub;
+        uint32_t oa = unev_out(a), ob = unev_out(b);
+        if (oa != ob) return oa < ob;
+        return a < b;
+      });
+      for (uint32_t w : fresh) S.push_back(w);
+      if (!g.edges.empty()) P->groups.push_back(std::move(g));
+    }
+  }
+
+  // Trie order pi: roots and first-discovered neighbours in group order; each
+  // later pattern between two visited variables is a closing edge of the one
+  // visited later (self-loops: of the variable itself).
+  std::vector<int32_t> pos(n, -1);
+  auto add_level = [&](uint32_t v, int32_t tree_edge, uint32_t parent, uint32_t label, uint32_t dir) {
+    Level L; L.var = v; L.tree_edge = tree_edge;
+    L.parent_level = tree_edge >= 0 ? (uint32_t)pos[parent] : 0;
+    L.label = label; L.dir = dir;
+    pos[v] = (int32_t)P->levels.size();
+    P->levels.push_back(L);
+  };
+  std::set<uint32_t> root_set(P->roots.begin(), P->roots.end());
+  for (auto& g : P->groups) {
+    uint32_t v = g.center;
+    if (pos[v] < 0) add_level(v, -1, 0, 0, 0);   // a root
+    for (auto& ge : g.edges) {
+      uint32_t w = ge.nbr;
+      if (w == v) {
+        P->levels[pos[v]].closing.push_back({ge.edge, ge.label, (uint32_t)pos[v], OUT});
+      } else if (pos[w] < 0) {
+        add_level(w, (int32_t)ge.edge, v, ge.label, ge.dir);
+      } else {
+        uint32_t later = pos[w] > pos[v] ? w : v, other = later == w ? v : w;
+        const auto& e = q->e[ge.edge];
+        P->levels[pos[later]].closing.push_back({ge.edge, ge.label, (uint32_t)pos[other],
+                                                 e.src == later ? (uint32_t)OUT : (uint32_t)IN});
+      }
+    }
+  }
+  for (uint32_t v : P->vars)
+    if (pos[v] < 0) add_level(v, -1, 0, 0, 0);   // only light edges: a free level
+
+  // Paths (Ex. 7.1): DFS branches over group edges from each root.
+  std::vector<int32_t> gidx(n, -1);
+  for (size_t i = 0; i < P->groups.size(); i++) gidx[P->groups[i].center] = (int32_t)i;
+  for (uint32_t r : P->roots) {
+    std::vector<std::vector<uint32_t>> out;
+    std::vector<uint32_t> acc{r};
+    std::function<void(uint32_t)> walk = [&](uint32_t v) {
+      std::vector<uint32_t> kids;
+      if (gidx[v] >= 0)
+        for (auto& ge : P->groups[gidx[v]].edges) if (ge.nbr != v) kids.push_back(ge.nbr);
+      if (kids.empty()) { out.push_back(acc); return; }
+      for (uint32_t w : kids) {
+        acc.push_back(w);
+        if (first_parent[w] == (int32_t)v && gidx[w] >= 0) walk(w);
+        else out.push_back(acc);
+        acc.pop_back();
+      }
+    };
+    walk(r);
+    P->paths.push_back(out);
+  }
+  (void)root_set;
+  return GSMART_OK;
+}
+
+static void jarr(std::ostringstream& o, const std::vector<uint32_t>& v) {
+  o << "[";
+  for (size_t i = 0; i < v.size(); i++) o << (i ? "," : "") << v[i];
+  o << "]";
+}
+
+std::string describe_plan(const gsmart_plan_t& p) {
+  std::ostringstream o;
+  o << "{\"traversal\":\"degree\",\"roots\":";
+  jarr(o, p.roots);
+  o << ",\"seeds\":[";
+  for (size_t i = 0; i < p.seeds.size(); i++) {
+    auto& s = p.seeds[i];
+    o << (i ? "," : "") << "{\"edge\":" << s.edge << ",\"var\":" << s.var << ",\"label\":" << s.label
+      << ",\"const\":" << s.cid << ",\"dir\":\"" << (s.dir == OUT ? "out" : "in") << "\"}";
+  }
+  o << "],\"guards\":[";
+  for (size_t i = 0; i < p.guards.size(); i++) o << (i ? "," : "") << p.guards[i].edge;
+  o << "],\"groups\":[";
+  for (size_t i = 0; i < p.groups.size(); i++) {
+    auto& g = p.groups[i];
+    o << (i ? "," : "") << "{\"center\":" << g.center << ",\"level\":" << g.level << ",\"edges\":[";
+    for (size_t j = 0; j < g.edges.size(); j++) {
+      auto& e = g.edges[j];
+      o << (j ? "," : "") << "{\"edge\":" << e.edge << ",\"label\":" << e.label << ",\"dir\":\""
+        << (e.dir == OUT ? "out" : "in") << "\",\"nbr\":" << e.nbr << "}";
+    }
+    o << "]}";
+  }
+  o << "],\"pi\":[";
+  for (size_t i = 0; i < p.levels.size(); i++) o << (i ? "," : "") << p.levels[i].var;
+  o << "],\"levels\":[";
+  for (size_t i = 0; i < p.levels.size(); i++) {
+    auto& L = p.levels[i];
+    o << (i ? "," : "") << "{\"var\":" << L.var << ",\"tree_edge\":" << L.tree_edge;
+    if (L.tree_edge >= 0)
+      o << ",\"parent_level\":" << L.parent_level << ",\"label\":" << L.label << ",\"dir\":\""
+        << (L.dir == OUT ? "out" : "in") << "\"";
+    o << ",\"closing\":[";
+    for (size_t j = 0; j < L.closing.size(); j++) {
+      auto& c = L.closing[j];
+      o << (j ? "," : "") << "{\"edge\":" << c.edge << ",\"label\":" << c.label << ",\"other_level\":"
+        << c.other_level << ",\"dir\":\"" << (c.dir == OUT ? "out" : "in") << "\"}";
+    }
+    o << "]}";
+  }
+  o << "],\"paths\":[";
+  for (size_t i = 0; i < p.paths.size(); i++) {
+    o << (i ? "," : "") << "[";
+    for (size_t j = 0; j < p.paths[i].size(); j++) { o << (j ? "," : ""); jarr(o, p.paths[i][j]); }
+    o << "]";
+  }
+  o << "],\"vars\":";
+  jarr(o, p.vars);
+  o << "}";
+  return o.str();
+}
+
+}  // namespace gsm

@@ -1,0 +1,129 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads, exports
+every symbol include/gsmart.h declares, plans queries (host-only planner),
+and fails loudly (GSMART_E_CUDA) instead of falling back when no device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from oracle import reference as R
+from synth import fixtures, tiny, lubm
+from synth.query import Query
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def G():
+    from conftest import build_product
+    build_product()
+    import paper_2106_14038_b200.gsmart as g
+    return g
+
+
+def _declared_functions():
+    txt = open(os.path.join(ROOT, "include", "gsmart.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(gsmart_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported(G):
+    lib = ctypes.CDLL(G.LIB_PATH)
+    decl = _declared_functions()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(decl) == set(G.EXPORTED)
+
+
+def test_abi_version_and_build_info(G):
+    assert G.gsmart_abi_version() == 1
+    assert "sm_100a" in G.gsmart_build_info()
+
+
+def test_no_gpu_fails_loudly(G):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(G.GsmartError) as ei:
+        G.gsmart_create(0)
+    assert ei.value.name == "E_CUDA"
+
+
+def _pydesc(q):
+    """oracle planner -> the describe() JSON shape, for comparison."""
+    pl = R.plan_degree(q)
+    D = {0: "out", 1: "in"}
+    return {
+        "roots": pl["roots"],
+        "seeds": pl["seeds"],
+        "groups": [{"center": c, "edges": [(k, D[d], w) for k, d, w in g]} for c, g in pl["groups"]],
+        "level": pl["level"],
+        "pi": pl["pi"],
+        "tree": {v: (k, p, D[d]) for v, (k, p, d) in pl["tree"].items()},
+        "closing": {v: sorted((k, o, D[d]) for k, o, d in cl) for v, cl in pl["closing"].items()},
+        "paths": [sorted(map(tuple, pl["paths"][r])) for r in pl["roots"]],
+    }
+
+
+def _cdesc(G, q):
+    h = G.gsmart_plan(None, q)
+    try:
+        d = G.gsmart_plan_describe(h)
+    finally:
+        G.gsmart_plan_free(h)
+    pi = d["pi"]
+    tree, closing = {}, {}
+    for L in d["levels"]:
+        v = L["var"]
+        if L["tree_edge"] >= 0:
+            tree[v] = (L["tree_edge"], pi[L["parent_level"]], L["dir"])
+        closing[v] = sorted((c["edge"], pi[c["other_level"]], c["dir"]) for c in L["closing"])
+    return {
+        "roots": d["roots"],
+        "seeds": [s["edge"] for s in d["seeds"]] + [],
+        "groups": [{"center": g["center"], "edges": [(e["edge"], e["dir"], e["nbr"]) for e in g["edges"]]}
+                   for g in d["groups"]],
+        "level": [g["level"] for g in d["groups"]],
+        "pi": pi,
+        "tree": tree,
+        "closing": closing,
+        "paths": [sorted(map(tuple, p)) for p in d["paths"]],
+    }, d
+
+
+def test_plan_fig2_matches_paper(G, golden_fig):
+    c, d = _cdesc(G, fixtures.fig2_query())
+    assert c["roots"] == [golden_fig["root"]]                     # Ex. 6.2
+    assert len(c["groups"]) == 2
+    assert max(c["level"]) + 1 == golden_fig["edge_levels_L0"]    # Ex. 6.5
+    assert sorted(c["paths"][0]) == sorted(tuple(p) for p in golden_fig["paths"])  # Ex. 7.1
+
+
+def test_plan_parity_with_oracle_planner(G):
+    """The product's C++ planner and the oracle's independent Python planner
+    agree on every field for random queries (cycles, constants, self-loops,
+    multi-edges, disconnected parts) and the LUBM templates."""
+    qs = [tiny.random_case(s)[3] for s in range(400)]
+    qs += lubm.queries(lubm.generate(1))
+    qs.append(fixtures.fig2_query())
+    for q in qs:
+        c, _ = _cdesc(G, q)
+        p = _pydesc(q)
+        guards = [k for k, (a, _, b) in enumerate(q.edges) if q.is_const(a) and q.is_const(b)]
+        assert sorted(c["seeds"] + guards) == p["seeds"], q
+        for key in ("roots", "groups", "level", "pi", "tree", "closing", "paths"):
+            assert c[key] == p[key], (key, q, c[key], p[key])
+
+
+def test_plan_errors(G):
+    with pytest.raises(G.GsmartError) as e:
+        G.gsmart_plan(None, Query((None,), ((0, 1, 1),)))       # vertex out of range
+    assert e.value.name == "E_INVALID_ARG"
+    with pytest.raises(G.GsmartError) as e:
+        G.gsmart_plan(None, Query((None, None), ((0, 0, 0),)))  # pred 0, var 1 unused
+    assert e.value.name == "E_INVALID_ARG"
+    with pytest.raises(G.GsmartError) as e:
+        G.gsmart_plan(None, fixtures.fig2_query(), traversal=G.GSMART_DIRECTION)
+    assert e.value.name == "E_UNSUPPORTED"

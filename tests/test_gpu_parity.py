@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by
+element on the same seeded inputs.  Integer/boolean path => bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import reference as R
+from oracle.coracle import oracle_bgp, OracleIndex
+from synth import fixtures, tiny, lubm
+from synth.query import Query
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from conftest import build_product
+    build_product()
+    import paper_2106_14038_b200.gsmart as g
+    return g
+
+
+@pytest.fixture(scope="module")
+def eng(G):
+    e = G.Engine(0)
+    yield e
+    e.close()
+
+
+def _rows(a):
+    return [tuple(int(x) for x in r) for r in np.asarray(a).tolist()]
+
+
+def _bits_to_set(words, n):
+    b = np.unpackbits(words.view(np.uint8), bitorder="little")[:n]
+    return set(np.nonzero(b)[0].tolist())
+
+
+def _cands(G, eng, q, flags):
+    """rows + candidate sets per variable from one execute."""
+    pl = G.gsmart_plan(eng.ctx, q)
+    r = G.gsmart_execute(eng.ctx, pl, flags)
+    try:
+        rows = G.gsmart_result_rows(r)
+        cs = {}
+        for v in q.variables:
+            ptr, nw = G.gsmart_result_candidates(r, v)
+            cs[v] = G.gsmart_copy_to_host(eng.ctx, ptr, nw * 4)
+        st = G.gsmart_result_stats(r)
+    finally:
+        G.gsmart_result_free(r)
+        G.gsmart_plan_free(pl)
+    return rows, cs, st
+
+
+# ------------------------------------------------------------------ worked example
+def test_fig12_rows_and_level0(G, eng, golden_fig):
+    s, p, o = fixtures.fig1_triples()
+    eng.load(s, p, o, 8, 4)
+    q = fixtures.fig2_query()
+    rows, cs, _ = _cands(G, eng, q, G.GSMART_NO_REFINE)
+    assert _rows(rows) == [tuple(r) for r in golden_fig["solution_rows"]]
+    root = golden_fig["root"]
+    assert sorted(_bits_to_set(cs[root], 8)) == golden_fig["level0_candidates"]  # Ex. 7.2
+    rows2, cs2, st = _cands(G, eng, q, 0)
+    assert _rows(rows2) == [tuple(r) for r in golden_fig["solution_rows"]]
+    assert sorted(_bits_to_set(cs2[root], 8)) == [1]
+    assert st["level_alive"][-1] == 2
+
+
+# ------------------------------------------------------------------ a1 LSpM arrays
+@pytest.mark.parametrize("seed,N,P,M,keep", [(1, 50, 4, 400, None), (2, 3000, 300, 40000, None),
+                                             (3, 1000, 7, 20000, [2, 5]), (4, 1, 1, 5, None),
+                                             (5, 100, 3, 0, None)])
+def test_lspm_arrays_match_definition(G, eng, seed, N, P, M, keep):
+    s, p, o = tiny.random_graph(seed, N, P, M, skew=1.1 if M > 1000 else 0.0)
+    # duplicates on purpose
+    s = np.concatenate([s, s[: M // 3]]); p = np.concatenate([p, p[: M // 3]]); o = np.concatenate([o, o[: M // 3]])
+    eng.load(s, p, o, N, P, keep=keep)
+    for fmt, name in ((G.GSMART_CSR, "csr"), (G.GSMART_CSC, "csc")):
+        v = G.gsmart_lspm_get(eng.ctx, fmt)
+        ref = R.lspm_arrays(s, p, o, N, keep=keep, fmt=name)
+        assert v["nnz"] == len(ref["col"])
+        rp = G.gsmart_copy_to_host(eng.ctx, v["row_ptr"], (N + 1) * 4)
+        col = G.gsmart_copy_to_host(eng.ctx, v["col"], v["nnz"] * 4)
+        dt = np.uint8 if v["pred_bytes"] == 1 else np.uint16
+        pred = G.gsmart_copy_to_host(eng.ctx, v["pred"], v["nnz"] * v["pred_bytes"], dtype=dt)
+        np.testing.assert_array_equal(rp.astype(np.uint64), ref["row_ptr"])
+        np.testing.assert_array_equal(col, ref["col"])
+        np.testing.assert_array_equal(pred.astype(np.uint32), ref["pred"])
+
+
+# ------------------------------------------------------------------ random tiny cases
+@pytest.mark.parametrize("chunk", range(5))
+def test_random_tiny_rows_and_candidates(G, eng, chunk):
+    for seed in range(chunk * 200, (chunk + 1) * 200):
+        (s, p, o), n, P, q = tiny.random_case(seed)
+        eng.load(s, p, o, n, P)
+        exp = R.brute_force(s, p, o, n, q)
+        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+            rows, cs, _ = _cands(G, eng, q, flags)
+            assert _rows(rows) == exp, (seed, q)
+            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine)
+            for v in q.variables:
+                got = _bits_to_set(cs[v], n)
+                assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
+
+
+# ------------------------------------------------------------------ larger, skewed graphs
+def _data_queries(rng, s, p, o, n_q):
+    """random connected queries whose constants come from the data (non-empty-ish)."""
+    out = []
+    for _ in range(n_q):
+        q = tiny.random_query(rng, int(max(s.max(), o.max())) + 1, int(p.max()),
+                              n_vars=int(rng.integers(2, 5)), n_consts=int(rng.integers(0, 2)),
+                              extra_edges=int(rng.integers(0, 2)))
+        # replace constants by a random subject/object that exists
+        verts = list(q.vertices)
+        for i, c in enumerate(verts):
+            if c is not None:
+                verts[i] = int(s[rng.integers(0, len(s))]) if rng.random() < 0.5 else int(o[rng.integers(0, len(o))])
+        out.append(Query(tuple(verts), q.edges))
+    return out
+
+
+@pytest.mark.parametrize("seed,N,P,M,skew", [(11, 2000, 3, 150000, 1.3), (12, 20000, 6, 200000, 0.0),
+                                             (13, 500, 2, 120000, 1.6)])
+def test_skewed_graphs_vs_oracle(G, eng, seed, N, P, M, skew):
+    """Hub rows beyond the warp-cooperative threshold and beyond HEAVY_ROW
+    (16384 entries) exercise all three group-filter paths and chunked expansion."""
+    s, p, o = tiny.random_graph(seed, N, P, M, skew=skew)
+    eng.load(s, p, o, N, P)
+    ix = OracleIndex(s, p, o)
+    rng = np.random.default_rng(seed)
+    for q in _data_queries(rng, s, p, o, 25):
+        exp = ix.query(q)
+        if len(exp) > 3_000_000:
+            continue
+        with eng.plan(q) as pl:
+            got = pl.run()
+        assert got.shape == exp.shape and np.array_equal(got, exp), q
+
+
+# ------------------------------------------------------------------ LUBM-shaped
+@pytest.mark.parametrize("U", [1, 10, 100])
+def test_lubm_queries_vs_oracle(G, eng, U):
+    d = lubm.generate(U)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    for q in lubm.queries(d):
+        exp = ix.query(q)
+        got = eng.query(q)
+        assert got.shape == exp.shape and np.array_equal(got, exp), q.name
+    # generator-analytic count (L2 = number of courses) and tree-DP closed form
+    L2 = [q for q in lubm.queries(d) if q.name == "L2"][0]
+    assert eng.query(L2, flags=G.GSMART_COUNT_ONLY) == d.n_courses
+
+
+def test_lubm_device_input_and_keep_set(G, eng):
+    import torch
+    d = lubm.generate(3)
+    qs = lubm.queries(d)
+    keep = sorted({e[1] for q in qs for e in q.edges})
+    eng.load(d.s.cuda(), d.p.cuda(), d.o.cuda(), d.n_entities, d.n_predicates, keep=keep)
+    ix = OracleIndex(d.s.numpy(), d.p.numpy(), d.o.numpy())
+    for q in qs:
+        assert np.array_equal(eng.query(q), ix.query(q)), q.name
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_cases(G, eng):
+    s, p, o = fixtures.fig1_triples()
+    eng.load(s, p, o, 8, 4)
+    # constant outside [0, N): empty, not an error
+    assert eng.query(Query((None, 99), ((0, 1, 1),))).shape == (0, 1)
+    # no variables: guard true / false
+    assert eng.query(Query((0, 1), ((0, 1, 1),))).shape == (1, 0)
+    assert eng.query(Query((0, 1), ((0, 2, 1),))).shape == (0, 0)
+    # self-loop with no data: empty
+    assert eng.query(Query((None,), ((0, 1, 0),))).shape == (0, 1)
+    # disconnected variables (cross product)
+    q = Query((None, None, 2, 7), ((2, 2, 0), (3, 3, 1)))
+    assert _rows(eng.query(q)) == R.brute_force(s, p, o, 8, q)
+    # COUNT_ONLY / KEEP_ON_DEVICE
+    q = fixtures.fig2_query()
+    assert eng.query(q, flags=G.GSMART_COUNT_ONLY) == 2
+    with eng.plan(q) as pl:
+        r = G.gsmart_execute(eng.ctx, pl.h, G.GSMART_KEEP_ON_DEVICE)
+        ptr = G.gsmart_result_rows_device(r)
+        host = G.gsmart_copy_to_host(eng.ctx, ptr, 2 * 4 * 4).reshape(2, 4)
+        assert _rows(host) == [(2, 0, 1, 0), (2, 0, 1, 5)]
+        assert _rows(G.gsmart_result_rows(r)) == [(2, 0, 1, 0), (2, 0, 1, 5)]
+        G.gsmart_result_free(r)
+
+
+def test_result_overflow_and_empty_load(G):
+    e = G.Engine(0, max_result_rows=1)
+    s, p, o = fixtures.fig1_triples()
+    e.load(s, p, o, 8, 4)
+    with pytest.raises(G.GsmartError) as ei:
+        e.query(fixtures.fig2_query())
+    assert ei.value.name == "E_RESULT_OVERFLOW"
+    e.close()
+    e = G.Engine(0)
+    e.load([], [], [], 10, 3)
+    assert e.query(Query((None, None), ((0, 1, 1),))).shape == (0, 2)
+    e.close()
+
+
+def test_call_order_and_bad_ids(G):
+    e = G.Engine.__new__(G.Engine)
+    e.ctx = G.gsmart_create(0)
+    with pytest.raises(G.GsmartError) as ei:
+        G.gsmart_build_lspm(e.ctx)
+    assert ei.value.name == "E_STATE"
+    with pytest.raises(G.GsmartError) as ei:
+        G.gsmart_load_triples(e.ctx, [0], [5], [1], 4, 3)   # predicate > n_predicates
+    assert ei.value.name == "E_INVALID_ARG"
+    e.close()
+
+
+def test_pruned_trie_invariants(G, eng):
+    """a8: after bottom-up pruning every internal node has >= 1 child, parent[]
+    is non-decreasing, and the last level holds exactly the rows."""
+    d = lubm.generate(2)
+    eng.load(d.s.numpy(), d.p.numpy(), d.o.numpy(), d.n_entities, d.n_predicates)
+    for q in lubm.queries(d):
+        with eng.plan(q) as pl:
+            r = G.gsmart_execute(eng.ctx, pl.h, 0)
+            n_rows = G.gsmart_result_shape(r)[0]
+            st = G.gsmart_result_stats(r)
+            L = st["n_levels"]
+            prev_n = None
+            for k in range(L):
+                v, n, par, bnd = G.gsmart_result_level(r, k)
+                assert n == st["level_alive"][k]
+                if k > 0 and n:
+                    parent = G.gsmart_copy_to_host(eng.ctx, par, n * 4)
+                    assert np.all(np.diff(parent.astype(np.int64)) >= 0)
+                    assert set(parent.tolist()) == set(range(prev_n)), q.name  # every node has a child
+                prev_n = n
+            assert prev_n == n_rows or L == 0
+            G.gsmart_result_free(r)
