@@ -419,6 +419,9 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
     for k in plan["seeds"]:
         a, l, b = q.edges[k]
         ca, cb = q.vertices[a], q.vertices[b]
+        if (ca is not None and ca >= N) or (cb is not None and cb >= N):
+            ok = False   # a constant absent from the data: empty answer (R12)
+            continue
         if ca is not None and cb is not None:
             ok = ok and ((ca, l, cb) in T)
             continue

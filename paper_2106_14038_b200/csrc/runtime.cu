@@ -533,7 +533,11 @@ struct Exec {
       if (sd.label > ctx->P) *empty = true;
     for (auto& g : plan->guards)
       if (g.label > ctx->P) *empty = true;
-    if (*empty) return GSMART_OK;
+    if (*empty) {  // a constant outside the data: every candidate set is empty (R12)
+      if (!plan->vars.empty())
+        CU(cudaMemsetAsync(R->d_cand, 0, (size_t)Wpad * plan->vars.size() * 4, ctx->st));
+      return GSMART_OK;
+    }
     std::vector<int> nseed(plan->n_vertices, 0);
     for (auto& sd : plan->seeds) nseed[sd.var]++;
     prof.begin(K_BITMAP);
