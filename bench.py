@@ -220,11 +220,20 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(flags=0, stats=None):
-        for pl in plans:
-            r = G.gsmart_execute(eng.ctx, pl, flags | G.GSMART_KEEP_ON_DEVICE)
+        # the query batch runs concurrently (gsmart_execute_batch: one stream + workspace per query)
+        for r in G.gsmart_execute_batch(eng.ctx, plans, flags | G.GSMART_KEEP_ON_DEVICE):
             if stats is not None:
                 stats.append(G.gsmart_result_stats(r))
             G.gsmart_result_free(r)
+
+    def latency(q_idx, reps=7):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = G.gsmart_execute(eng.ctx, plans[q_idx], G.GSMART_KEEP_ON_DEVICE)
+            ts.append(1000 * (time.perf_counter() - t0))
+            G.gsmart_result_free(r)
+        return statistics.median(ts)
 
     for _ in range(args.warmup):
         step()
@@ -281,9 +290,8 @@ def main():
     launches_per_step = sum(sum(st["launches"].values()) for st in prof_stats) / max(1, len(prof_stats) // len(qs))
     per_query = {}
     for i, q in enumerate(qs):
-        per_query[q.name] = {"ms_median": statistics.median(
-            [prof_stats[j]["ms_total"] for j in range(i, len(prof_stats), len(qs))]),
-            "rows": None, "edges": E[i]}
+        per_query[q.name] = {"latency_ms": latency(i),  # alone, host wall time of gsmart_execute
+                             "rows": None, "edges": E[i]}
 
     # ---- e2e: host triples -> load -> build -> batch -> rows on host
     e2e_times = []

@@ -167,6 +167,16 @@ void gsmart_plan_free(gsmart_plan_t* plan);
 gsmart_status gsmart_execute(gsmart_ctx* ctx, const gsmart_plan_t* plan, uint32_t flags,
                              gsmart_result** out);
 
+/* Execute n independent plans as one batch: up to 16 run concurrently, each on
+ * its own CUDA stream with its own workspace, so small (latency-bound) queries
+ * overlap on the GPU.  out[i] receives plan i's result, identical to what
+ * gsmart_execute(plans[i]) returns.  The batch starts after work already
+ * queued on the ctx stream and has completed when the call returns.  On
+ * error every out[i] is NULL and the first failing status is returned.
+ * Results of a ctx must be freed before gsmart_destroy. */
+gsmart_status gsmart_execute_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint32_t n,
+                                   uint32_t flags, gsmart_result** out);
+
 /* n_rows, n_cols (= number of variables) and var_of_col[n_cols] (query vertex
  * index of each column; host memory owned by the result). */
 gsmart_status gsmart_result_shape(const gsmart_result* r, uint64_t* n_rows, uint32_t* n_cols,

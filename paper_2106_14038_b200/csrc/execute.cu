@@ -1,0 +1,668 @@
+// C-ABI implementation, part 2: the executor (a3-a9; §4 main
+// computation + §8 post-processing, re-designed level-synchronous).
+//
+// An execute runs on one Slot (stream + workspace).  Host work is split into
+// phases so that a batch of plans (gsmart_execute_batch) keeps every slot's
+// stream busy while the host waits on only two events per plan:
+//   start()        seeds -> grouped incident-edge evaluation -> trie expansion,
+//                  all asynchronous; sizes are copied to pinned memory + event;
+//   after_expand() reads sizes; on a workspace overflow grows it and re-launches
+//                  the expansion (rare), else launches phase 2;
+//   phase2()       pruning -> level compaction -> rows -> sort (async);
+//   finalize()     after the stream drained: alive counts, counters, stats.
+#include <chrono>
+#include <cstring>
+
+#include "runtime.h"
+
+using namespace gsm;
+
+namespace gsm {
+
+static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
+  if (primary) {
+    s.st = ctx->st;
+  } else {
+    CU(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    s.own_stream = true;
+  }
+  CU(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  TRY(dalloc(ctx, &s.lb_status, LB_CAP_TILES, s.st));
+  TRY(dalloc(ctx, &s.lb_counters, LB_EPOCHS, s.st));
+  TRY(dalloc(ctx, &s.d_sz, 128, s.st));
+  TRY(dalloc(ctx, &s.d_ovf, 1, s.st));
+  TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
+  TRY(dalloc(ctx, &s.heavy_cnt, 2, s.st));
+  CU(cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st));
+  CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
+  CU(cudaMemsetAsync(s.heavy_cnt, 0, 8, s.st));
+  CU(cudaMallocHost(&s.h_pin, 256 * sizeof(unsigned long long)));
+  s.epoch = 0;
+  return GSMART_OK;
+}
+
+static void slot_free(gsmart_ctx* ctx, Slot& s) {
+  cudaStream_t st = s.st;
+  for (auto& b : s.lv) {
+    dfree(st, b.bind); dfree(st, b.parent); dfree(st, b.seg_beg); dfree(st, b.off); dfree(st, b.newidx);
+    dfree(st, b.alive);
+  }
+  for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
+  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
+  dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
+  cudaStreamSynchronize(st);
+  if (s.h_pin) cudaFreeHost(s.h_pin);
+  if (s.ev) cudaEventDestroy(s.ev);
+  if (s.own_stream) cudaStreamDestroy(s.st);
+  (void)ctx;
+}
+
+void slots_free(gsmart_ctx* ctx) {
+  for (auto& s : ctx->slots) slot_free(ctx, *s);
+  ctx->slots.clear();
+}
+
+static gsmart_status ensure_slots(gsmart_ctx* ctx, uint32_t n) {
+  while (ctx->slots.size() < n) {
+    auto s = std::make_unique<Slot>();
+    TRY(slot_init(ctx, *s, ctx->slots.empty()));
+    ctx->slots.push_back(std::move(s));
+  }
+  return GSMART_OK;
+}
+
+// heavy-row buffers sized from the LSpM's heavy-row statistics
+static gsmart_status slot_heavy(gsmart_ctx* ctx, Slot& s) {
+  if (s.heavy_gen == ctx->lspm_gen) return GSMART_OK;
+  dfree(s.st, s.heavy_rows); dfree(s.st, s.heavy_chunks); dfree(s.st, s.heavy_sat);
+  const uint64_t rows = std::max<uint64_t>(ctx->f[0].heavy_rows + ctx->f[1].heavy_rows, 1);
+  const uint64_t chunks = std::max<uint64_t>(ctx->f[0].heavy_chunks + ctx->f[1].heavy_chunks, 1);
+  TRY(dalloc(ctx, &s.heavy_rows, rows, s.st));
+  TRY(dalloc(ctx, &s.heavy_sat, rows, s.st));
+  TRY(dalloc(ctx, &s.heavy_chunks, 2 * chunks, s.st));
+  CU(cudaMemsetAsync(s.heavy_sat, 0, rows * 4, s.st));
+  CU(cudaMemsetAsync(s.heavy_cnt, 0, 8, s.st));
+  s.heavy_gen = ctx->lspm_gen;
+  return GSMART_OK;
+}
+
+// a fresh (epoch, zeroed counter) pair for one look-back launch
+static LBArgs next_lb(Slot& s) {
+  if (++s.epoch >= LB_EPOCHS) {
+    cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st);
+    cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st);
+    s.epoch = 1;
+  }
+  LBArgs a;
+  a.status = s.lb_status;
+  a.counter = s.lb_counters + s.epoch;
+  a.epoch = s.epoch;
+  a.cap_tiles = LB_CAP_TILES;
+  return a;
+}
+
+static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t need) {
+  auto& b = s.lv[k];
+  if (b.bind && b.cap >= need) return GSMART_OK;
+  uint64_t cap = std::max<uint64_t>(need, std::max<uint64_t>(2 * b.cap, 1u << 16));
+  cap = (cap + 1023) / 1024 * 1024;
+  dfree(s.st, b.bind); dfree(s.st, b.parent); dfree(s.st, b.seg_beg); dfree(s.st, b.off); dfree(s.st, b.newidx);
+  dfree(s.st, b.alive);
+  b = Slot::LvBuf();
+  TRY(dalloc(ctx, &b.bind, cap, s.st));
+  TRY(dalloc(ctx, &b.parent, cap, s.st));
+  TRY(dalloc(ctx, &b.seg_beg, cap, s.st));
+  TRY(dalloc(ctx, &b.off, cap + 1, s.st));
+  TRY(dalloc(ctx, &b.newidx, cap, s.st));
+  TRY(dalloc(ctx, &b.alive, cap, s.st));
+  b.cap = cap;
+  return GSMART_OK;
+}
+
+}  // namespace gsm
+
+namespace {
+
+struct Prof {
+  cudaStream_t st;
+  gsmart_stats* stats;
+  bool on;
+  struct Rec { int kid; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  int cur = -1;
+  cudaEvent_t cur_a = nullptr;
+  Prof(cudaStream_t s, gsmart_stats* r, bool enable) : st(s), stats(r), on(enable) {}
+  void begin(int kid) {
+    if (!on) return;
+    cur = kid;
+    cudaEventCreate(&cur_a);
+    cudaEventRecord(cur_a, st);
+  }
+  void end() {
+    if (!on || cur < 0) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    recs.push_back({cur, cur_a, b});
+    cur = -1;
+  }
+  void flush() {  // after the stream drained
+    for (auto& r : recs) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) stats->ms_kernel[r.kid] += ms;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    recs.clear();
+  }
+  ~Prof() { flush(); }
+};
+
+struct Exec {
+  enum State { S_NEW, S_EXPANDING, S_PHASE2, S_DONE };
+  gsmart_ctx* ctx;
+  Slot& sl;
+  const gsmart_plan_t* plan;
+  uint32_t flags;
+  gsmart_result* R;
+  Prof prof;
+  Scratch sc;
+  State state = S_NEW;
+  uint32_t W = 0, Wpad = 0, L = 0;
+  std::vector<int32_t> slot;  // vertex -> cand slot
+  FmtAny fa[2];
+  int launches[GSMART_NKERNELS] = {0};
+  uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
+  int attempts = 0;
+  std::vector<uint64_t> F;
+  std::chrono::steady_clock::time_point t0;
+
+  Exec(gsmart_ctx* c, Slot& s, const gsmart_plan_t* p, uint32_t fl, gsmart_result* r)
+      : ctx(c), sl(s), plan(p), flags(fl), R(r), prof(s.st, &r->stats, (fl & GSMART_PROFILE) != 0), sc(c, s.st) {
+    t0 = std::chrono::steady_clock::now();
+  }
+
+  uint32_t* cand(uint32_t vertex) { return R->d_cand + (uint64_t)slot[vertex] * Wpad; }
+
+  gsmart_status alloc_result(void** p, uint64_t bytes) {
+    TRY(dalloc(ctx, (char**)p, bytes, sl.st));
+    R->owned.push_back(*p);
+    return GSMART_OK;
+  }
+
+  // ---- a3: seeds (light edges) and guards.  The first seed of a variable is
+  // scattered into its bitmap; further seeds become constant-target filter edges.
+  gsmart_status seeds_and_guards(bool* empty) {
+    const uint32_t N = ctx->N;
+    *empty = false;
+    for (auto& sd : plan->seeds)
+      if (sd.cid >= N) *empty = true;
+    for (auto& g : plan->guards)
+      if (g.s >= N || g.o >= N) *empty = true;
+    if (*empty) {  // a constant outside the data: every candidate set is empty (R12)
+      if (!plan->vars.empty())
+        CU(cudaMemsetAsync(R->d_cand, 0, (size_t)Wpad * plan->vars.size() * 4, sl.st));
+      return GSMART_OK;
+    }
+    std::vector<std::vector<const Seed*>> by_var(plan->n_vertices);
+    for (auto& sd : plan->seeds) by_var[sd.var].push_back(&sd);
+    uint32_t ones = 0;
+    for (uint32_t v : plan->vars)
+      if (by_var[v].empty()) ones |= 1u << slot[v];
+    if (!plan->vars.empty()) {
+      prof.begin(K_BITMAP);
+      CU(launch_init_cands(R->d_cand, (uint32_t)plan->vars.size(), Wpad, N, ones, sl.st));
+      launches[K_BITMAP]++;
+      prof.end();
+    }
+    int* flag = (int*)(sl.d_ctr + 48);
+    if (!plan->guards.empty()) {
+      CU(cudaMemsetAsync(flag, 0xff, 4, sl.st));  // nonzero = guards hold
+      prof.begin(K_SEED);
+      for (auto& g : plan->guards) {
+        CU(launch_guard(fa[0], ctx->pred_bytes, g.s, g.label, g.o, flag, sl.st));
+        launches[K_SEED]++;
+      }
+      prof.end();
+    }
+    for (uint32_t v : plan->vars) {
+      const auto& ss = by_var[v];
+      if (ss.empty()) continue;
+      prof.begin(K_SEED);
+      CU(launch_seed_scatter(fa[ss[0]->dir == OUT ? 0 : 1], ctx->pred_bytes, ss[0]->cid, ss[0]->label, cand(v),
+                             sl.d_ctr, ctx->sm_count, sl.st));
+      launches[K_SEED]++;
+      prof.end();
+      if (ss.size() > 1) {
+        // (c -l-> v): v's CSC row must hold (l, c); (v -l-> c): v's CSR row must hold (l, c)
+        Group g;
+        g.center = v;
+        for (size_t i = 1; i < ss.size(); i++)
+          g.edges.push_back({ss[i]->edge, ss[i]->label, ss[i]->dir == OUT ? (uint32_t)IN : (uint32_t)OUT,
+                             0x80000000u | ss[i]->cid});
+        TRY(eval_group(g));
+      }
+    }
+    if (!plan->guards.empty() && !plan->vars.empty()) {
+      prof.begin(K_BITMAP);
+      CU(launch_zero_if_flag(R->d_cand, (uint64_t)Wpad * plan->vars.size(), flag, sl.st));
+      launches[K_BITMAP]++;
+      prof.end();
+    }
+    return GSMART_OK;
+  }
+
+  // ---- a4: grouped incident-edge evaluation of one group (§5 Eqs. 17/21).
+  // nbr with bit 31 set = constant target (extra seed).
+  gsmart_status eval_group(const Group& g) {
+    std::vector<const GroupEdge*> by[2];
+    for (auto& e : g.edges) by[e.dir == OUT ? 0 : 1].push_back(&e);
+    size_t done[2] = {0, 0};
+    while (done[0] < by[0].size() || done[1] < by[1].size()) {
+      FilterArgs a;
+      memset(&a, 0, sizeof a);
+      a.f[0] = fa[0];
+      a.f[1] = fa[1];
+      for (int d = 0; d < 2; d++) {
+        while (done[d] < by[d].size() && a.ne[d] < (uint32_t)MAXG) {
+          const GroupEdge* e = by[d][done[d]++];
+          GEdge& ge = a.e[d][a.ne[d]++];
+          ge.label = e->label;
+          if (e->nbr & 0x80000000u) {
+            ge.mode = GE_CONST;
+            ge.cval = e->nbr & 0x7fffffffu;
+          } else if (e->nbr == g.center) {
+            ge.mode = GE_SELF;
+          } else {
+            ge.mode = GE_PROBE;
+            ge.nbr = cand(e->nbr);
+          }
+        }
+        if (a.ne[d] && ctx->f[d].heavy_rows) a.heavy = 1;
+      }
+      a.cand = cand(g.center);
+      a.n_words = W;
+      a.heavy_rows = sl.heavy_rows;
+      a.heavy_chunks = sl.heavy_chunks;
+      a.heavy_sat = sl.heavy_sat;
+      a.heavy_count = sl.heavy_cnt;
+      a.ctr = sl.d_ctr;
+      prof.begin(K_FILTER);
+      CU(launch_group_filter(a, ctx->pred_bytes, ctx->sm_count, sl.st, &launches[K_FILTER]));
+      prof.end();
+      filter_main++;
+    }
+    return GSMART_OK;
+  }
+
+  // ---- a5/a6/a7: one expansion attempt over all levels (async), sizes -> pinned
+  gsmart_status launch_expansion() {
+    unsigned long long* dsz = sl.d_sz;
+    CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
+    CU(cudaMemsetAsync(sl.d_ovf, 0, 4, sl.st));
+    if (L > 1) CU(cudaMemsetAsync(sl.lv[0].alive, 0, sl.lv[0].cap, sl.st));
+    prof.begin(K_COMPACT);
+    CU(launch_bitmap_compact_lb(cand(plan->levels[0].var), W, sl.lv[0].bind, sl.lv[0].cap, dsz + 0, sl.d_ovf,
+                                next_lb(sl), ctx->sm_count, sl.st));
+    launches[K_COMPACT]++;
+    prof.end();
+    for (uint32_t k = 1; k < L; k++) {
+      const Level& Lv = plan->levels[k];
+      ExpArgs2 a;
+      memset(&a, 0, sizeof a);
+      for (uint32_t j = 0; j < k; j++) {
+        a.tab.parent[j] = sl.lv[j].parent;
+        a.tab.bind[j] = sl.lv[j].bind;
+      }
+      a.k = k;
+      a.d_nparent = dsz + (k - 1);
+      a.cap_par = sl.lv[k - 1].cap;
+      a.tree = Lv.tree_edge >= 0 ? 1 : 0;
+      a.parent_level = Lv.parent_level;
+      a.label = Lv.label;
+      a.dir = Lv.dir == OUT ? 0 : 1;
+      a.f[0] = fa[0];
+      a.f[1] = fa[1];
+      a.cand = cand(Lv.var);
+      for (auto& c : Lv.closing) {
+        ClosingDev& d = a.cl[a.ncl++];
+        d.label = c.label;
+        d.other_level = c.other_level;
+        d.dir = c.dir == OUT ? 0 : 1;
+        d.self = c.other_level == k ? 1u : 0u;
+      }
+      if (!a.tree) {
+        prof.begin(K_COMPACT);
+        CU(launch_bitmap_compact_lb(cand(Lv.var), W, sl.list[k], sl.list_cap[k], dsz + 64 + k, sl.d_ovf,
+                                    next_lb(sl), ctx->sm_count, sl.st));
+        launches[K_COMPACT]++;
+        prof.end();
+        a.list = sl.list[k];
+        a.d_list_len = dsz + 64 + k;
+      }
+      a.seg_beg = sl.lv[k - 1].seg_beg;
+      a.off = sl.lv[k - 1].off;
+      a.d_T = dsz + 32 + k;
+      a.out_parent = sl.lv[k].parent;
+      a.out_bind = sl.lv[k].bind;
+      a.out_alive = k + 1 < L ? sl.lv[k].alive : nullptr;
+      a.cap_out = sl.lv[k].cap;
+      a.d_nout = dsz + k;
+      a.overflow = sl.d_ovf;
+      a.ctr = sl.d_ctr;
+      a.lb = next_lb(sl);
+      prof.begin(K_EXPAND_SEG);
+      CU(launch_seg_scan(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      launches[K_EXPAND_SEG]++;
+      prof.end();
+      a.lb = next_lb(sl);
+      prof.begin(K_EXPAND_EMIT);
+      CU(launch_expand_lb(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      launches[K_EXPAND_EMIT]++;
+      prof.end();
+    }
+    CU(cudaMemcpyAsync(dsz + 127, sl.d_ovf, 4, cudaMemcpyDeviceToDevice, sl.st));
+    CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
+    CU(cudaEventRecord(sl.ev, sl.st));
+    state = S_EXPANDING;
+    return GSMART_OK;
+  }
+
+  gsmart_status start() {
+    const uint32_t N = ctx->N;
+    const uint32_t nvar = (uint32_t)plan->vars.size();
+    W = (N + 31) / 32;
+    Wpad = (W + 31) / 32 * 32;
+    L = (uint32_t)plan->levels.size();
+    R->n_words = W;
+    R->stride_words = Wpad;
+    slot.assign(plan->n_vertices, -1);
+    for (uint32_t i = 0; i < nvar; i++) slot[plan->vars[i]] = (int32_t)i;
+    R->cand_slot = slot;
+    for (int d = 0; d < 2; d++) {
+      fa[d].rp = ctx->f[d].rp;
+      fa[d].col = ctx->f[d].col;
+      fa[d].pred = ctx->f[d].pred;
+    }
+    TRY(slot_heavy(ctx, sl));
+    CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
+    if (nvar) TRY(alloc_result((void**)&R->d_cand, (uint64_t)Wpad * nvar * 4));
+
+    bool empty = false;
+    TRY(seeds_and_guards(&empty));
+    if (nvar == 0) {  // only guards (or nothing): one empty row iff all hold
+      uint64_t rows = 0;
+      if (!empty) {
+        int flag = 1;
+        if (!plan->guards.empty()) {
+          CU(cudaMemcpyAsync(&flag, sl.d_ctr + 48, 4, cudaMemcpyDeviceToHost, sl.st));
+          CU(cudaStreamSynchronize(sl.st));
+        }
+        rows = flag ? 1 : 0;
+      }
+      R->n_rows = rows;
+      R->host_valid = true;
+      state = S_DONE;
+      return GSMART_OK;
+    }
+    if (empty) {
+      R->n_rows = 0;
+      R->host_valid = true;
+      R->stats.n_levels = L;
+      for (auto& Lv : plan->levels) R->levels.push_back({Lv.var, 0, nullptr, nullptr});
+      state = S_DONE;
+      return GSMART_OK;
+    }
+    // forward groups, then backward re-evaluation (R-refine)
+    for (auto& g : plan->groups) TRY(eval_group(g));
+    if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
+      for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i]));
+    // expansion workspace
+    for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
+    for (uint32_t k = 1; k < L; k++) {
+      if (plan->levels[k].tree_edge < 0 && sl.list_cap[k] < (uint64_t)W * 32) {
+        dfree(sl.st, sl.list[k]);
+        TRY(dalloc(ctx, &sl.list[k], (uint64_t)W * 32, sl.st));
+        sl.list_cap[k] = (uint64_t)W * 32;
+      }
+      if (plan->levels[k].closing.size() > (size_t)MAXC)
+        FAIL(GSMART_E_UNSUPPORTED, "more than 16 closing edges on one level");
+    }
+    F.assign(L, 0);
+    R->stats.n_levels = L;
+    return launch_expansion();
+  }
+
+  // called once sl.ev completed
+  gsmart_status after_expand() {
+    const unsigned long long* hv = sl.h_pin;
+    const int ovf = (int)(hv[127] & 0xffffffffu);
+    if (ovf & 2) FAIL(GSMART_E_RESULT_OVERFLOW, "expansion entries of one level exceed 2^32");
+    const uint64_t cap = ctx->cap();
+    for (uint32_t k = 0; k < L; k++) {
+      F[k] = hv[k];
+      if (F[k] > cap) {
+        R->n_rows = F[k];
+        FAIL(GSMART_E_RESULT_OVERFLOW, "trie level " + std::to_string(k) + " exceeds max_result_rows");
+      }
+      if (F[k] > sl.lv[k].cap) {  // later levels are invalid: grow and re-run the expansion
+        TRY(slot_level(ctx, sl, k, F[k]));
+        if (++attempts > 2 * (int)L + 2) FAIL(GSMART_E_CUDA, "expansion capacity did not converge");
+        return launch_expansion();
+      }
+    }
+    for (uint32_t k = 0; k < L; k++) R->stats.level_nodes[k] = F[k];
+    return phase2();
+  }
+
+  // ---- a8 prune + compaction, a9 rows + sort (async)
+  gsmart_status phase2() {
+    state = S_PHASE2;
+    const uint64_t n_rows = F[L - 1];
+    unsigned long long* dsz = sl.d_sz;
+    R->levels.clear();
+    LevelTab pt;
+    memset(&pt, 0, sizeof pt);
+    R->n_rows = n_rows;
+    if (!n_rows) {
+      for (uint32_t k = 0; k < L; k++) R->levels.push_back({plan->levels[k].var, 0, nullptr, nullptr});
+      R->host_valid = (flags & GSMART_COUNT_ONLY) == 0;
+      R->count_only = (flags & GSMART_COUNT_ONLY) != 0;
+      return GSMART_OK;
+    }
+    prof.begin(K_PRUNE);
+    for (uint32_t k = L - 1; k >= 1; k--) {
+      CU(launch_prune_mark_d(sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
+                             ctx->sm_count, sl.st));
+      launches[K_PRUNE]++;
+    }
+    for (uint32_t k = 0; k < L; k++) {
+      gsmart_result::Lv lv{plan->levels[k].var, 0, nullptr, nullptr};
+      TRY(alloc_result((void**)&lv.bind, F[k] * 4));
+      if (k > 0) TRY(alloc_result((void**)&lv.parent, F[k] * 4));
+      CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind, k + 1 < L ? sl.lv[k].alive : nullptr,
+                                 dsz + k, k > 0 ? sl.lv[k - 1].newidx : nullptr, lv.parent, lv.bind,
+                                 k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), ctx->sm_count,
+                                 sl.st));
+      launches[K_PRUNE]++;
+      pt.parent[k] = lv.parent;
+      pt.bind[k] = lv.bind;
+      R->levels.push_back(lv);
+    }
+    prof.end();
+    CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
+    if (!(flags & GSMART_COUNT_ONLY)) {
+      const uint32_t nc = (uint32_t)plan->vars.size();
+      std::vector<uint32_t> col_of_level(L);
+      bool identity = true;
+      for (uint32_t k = 0; k < L; k++) {
+        col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
+        if (col_of_level[k] != k) identity = false;
+      }
+      uint32_t* rows = nullptr;
+      TRY(identity ? alloc_result((void**)&rows, n_rows * nc * 4) : sc.get(&rows, n_rows * nc));
+      prof.begin(K_ENUMERATE);
+      CU(launch_enumerate(pt, L, col_of_level.data(), (uint32_t)n_rows, nc, rows, sl.st));
+      launches[K_ENUMERATE]++;
+      prof.end();
+      if (identity) {
+        R->d_rows = rows;  // trie order == lexicographic order in variable-index order
+      } else {
+        TRY(alloc_result((void**)&R->d_rows, n_rows * nc * 4));
+        size_t tb = sort_rows_tmp_bytes(n_rows, nc);
+        void* tmp = nullptr;
+        TRY(sc.get((char**)&tmp, tb));
+        prof.begin(K_SORT_ROWS);
+        CU(sort_rows(rows, R->d_rows, n_rows, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
+        prof.end();
+      }
+    } else {
+      R->count_only = true;
+    }
+    return GSMART_OK;
+  }
+
+  // after the slot stream drained
+  gsmart_status finalize() {
+    prof.flush();
+    if (state == S_PHASE2 && R->n_rows) {
+      for (uint32_t k = 0; k < L && k < (uint32_t)R->levels.size(); k++) {
+        R->levels[k].n = sl.h_pin[128 + k];
+        R->stats.level_alive[k] = sl.h_pin[128 + k];
+      }
+    }
+    unsigned long long c[C_NCTR];
+    CU(cudaMemcpy(c, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost));
+    auto& st = R->stats;
+    st.filter_rows = c[C_FILTER_ROWS];
+    st.filter_entries = c[C_FILTER_SCANNED];
+    st.seed_entries = c[C_SEED];
+    st.expand_entries = c[C_EXPAND];
+    st.closing_checks = c[C_CLOSING];
+    st.edges_evaluated = c[C_FILTER_MATCHED] + c[C_SEED] + c[C_EXPAND];
+    const uint64_t pb = (uint64_t)ctx->pred_bytes;
+    // algorithmic bytes: what each step must move
+    uint64_t parents = 0, children = 0;
+    st.bytes[K_FILTER] = 8 * c[C_FILTER_ROWS] + pb * c[C_FILTER_SCANNED] + 4 * c[C_FILTER_MATCHED] +
+                         8ull * filter_main * W;
+    st.bytes[K_SEED] = 4 * c[C_SEED];
+    for (uint32_t k = 0; k + 1 < st.n_levels && k + 1 < GSMART_MAX_LEVELS; k++) parents += st.level_nodes[k];
+    for (uint32_t k = 1; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) children += st.level_nodes[k];
+    st.bytes[K_EXPAND_SEG] = 12 * parents;
+    st.bytes[K_EXPAND_EMIT] = 4 * c[C_EXPAND] + 9 * children + 8 * parents;
+    for (int i = 0; i < GSMART_NKERNELS; i++) st.launches[i] = (uint64_t)launches[i];
+    for (int i = 0; i < GSMART_NKERNELS; i++) st.kernel_names[i] = kKernelNames[i];
+    if (!(flags & (GSMART_KEEP_ON_DEVICE | GSMART_COUNT_ONLY)) && R->d_rows && R->n_rows) {
+      R->h_rows.resize(R->n_rows * R->n_cols);
+      CU(cudaMemcpy(R->h_rows.data(), R->d_rows, R->n_rows * R->n_cols * 4, cudaMemcpyDeviceToHost));
+      R->host_valid = true;
+    } else if (!R->n_rows && !(flags & GSMART_COUNT_ONLY)) {
+      R->host_valid = true;
+    }
+    st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    state = S_DONE;
+    return GSMART_OK;
+  }
+};
+
+gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan) {
+  if (!plan) FAIL(GSMART_E_INVALID_ARG, "null plan");
+  for (auto& e : plan->edges)
+    if (e.pred > ctx->P) FAIL(GSMART_E_INVALID_ARG, "query predicate id > n_predicates");
+  return GSMART_OK;
+}
+
+gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint32_t n, uint32_t flags,
+                        gsmart_result** out) {
+  for (uint32_t i = 0; i < n; i++) TRY(check_plan(ctx, plans[i]));
+  const uint32_t ns = std::min<uint32_t>(std::max<uint32_t>(n, 1), MAX_SLOTS);
+  TRY(ensure_slots(ctx, ns));
+  // fork: every slot stream starts after the work already queued on ctx->st
+  cudaEvent_t fork;
+  CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  CU(cudaEventRecord(fork, ctx->st));
+  for (uint32_t s = 1; s < ns; s++) CU(cudaStreamWaitEvent(ctx->slots[s]->st, fork, 0));
+  cudaEventDestroy(fork);
+  gsmart_status status = GSMART_OK;
+  for (uint32_t base = 0; base < n && status == GSMART_OK; base += ns) {
+    const uint32_t m = std::min(ns, n - base);
+    std::vector<std::unique_ptr<gsmart_result>> res(m);
+    std::vector<std::unique_ptr<Exec>> ex(m);
+    for (uint32_t i = 0; i < m; i++) {
+      res[i] = std::make_unique<gsmart_result>();
+      gsmart_result* R = res[i].get();
+      const gsmart_plan_t* p = plans[base + i];
+      R->ctx = ctx;
+      R->st = ctx->slots[i]->st;
+      R->n_cols = (uint32_t)p->vars.size();
+      R->var_of_col = p->vars;
+      R->count_only = (flags & GSMART_COUNT_ONLY) != 0;
+      for (int k = 0; k < GSMART_NKERNELS; k++) R->stats.kernel_names[k] = kKernelNames[k];
+      ex[i] = std::make_unique<Exec>(ctx, *ctx->slots[i], p, flags, R);
+    }
+    std::vector<gsmart_status> st(m, GSMART_OK);
+    for (uint32_t i = 0; i < m; i++) st[i] = ex[i]->start();
+    // wait on each expansion readback; re-launch on overflow; then phase 2
+    bool pending = true;
+    while (pending) {
+      pending = false;
+      for (uint32_t i = 0; i < m; i++) {
+        if (st[i] != GSMART_OK || ex[i]->state != Exec::S_EXPANDING) continue;
+        cudaError_t e = cudaEventSynchronize(ex[i]->sl.ev);
+        if (e != cudaSuccess) {
+          st[i] = cuda_fail(ctx, e, "expansion event", __LINE__);
+          continue;
+        }
+        st[i] = ex[i]->after_expand();
+        if (st[i] == GSMART_OK && ex[i]->state == Exec::S_EXPANDING) pending = true;
+      }
+    }
+    for (uint32_t i = 0; i < m; i++) {
+      cudaError_t e = cudaStreamSynchronize(ex[i]->sl.st);
+      if (e != cudaSuccess && st[i] == GSMART_OK) st[i] = cuda_fail(ctx, e, "execute sync", __LINE__);
+      if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
+      else ex[i]->prof.flush();
+    }
+    for (uint32_t i = 0; i < m; i++) {
+      ex[i].reset();  // frees stream-ordered scratch
+      if (st[i] == GSMART_OK || (st[i] == GSMART_E_RESULT_OVERFLOW && n == 1)) {
+        out[base + i] = res[i].release();
+      } else {
+        gsmart_result_free(res[i].release());
+      }
+      if (st[i] != GSMART_OK && status == GSMART_OK) status = st[i];
+    }
+  }
+  // join: later work on ctx->st sees the batch (already drained above)
+  return status;
+}
+
+}  // namespace
+
+extern "C" gsmart_status gsmart_execute(gsmart_ctx* ctx, const gsmart_plan_t* plan, uint32_t flags,
+                                        gsmart_result** out) {
+  if (!ctx || !plan || !out) return GSMART_E_INVALID_ARG;
+  *out = nullptr;
+  if (ctx->poisoned) return GSMART_E_CUDA;
+  if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
+  if (ctx->cfg.world > 1) FAIL(GSMART_E_UNSUPPORTED, "world > 1 execute is not available in this build");
+  CU(cudaSetDevice(ctx->cfg.device));
+  return run_batch(ctx, &plan, 1, flags, out);
+}
+
+extern "C" gsmart_status gsmart_execute_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint32_t n,
+                                              uint32_t flags, gsmart_result** out) {
+  if (!ctx || (n && (!plans || !out))) return GSMART_E_INVALID_ARG;
+  for (uint32_t i = 0; i < n; i++) out[i] = nullptr;
+  if (ctx->poisoned) return GSMART_E_CUDA;
+  if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
+  if (ctx->cfg.world > 1) FAIL(GSMART_E_UNSUPPORTED, "world > 1 execute is not available in this build");
+  CU(cudaSetDevice(ctx->cfg.device));
+  gsmart_status s = run_batch(ctx, plans, n, flags, out);
+  if (s != GSMART_OK)
+    for (uint32_t i = 0; i < n; i++) {
+      gsmart_result_free(out[i]);
+      out[i] = nullptr;
+    }
+  return s;
+}

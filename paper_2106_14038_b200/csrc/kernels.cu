@@ -202,6 +202,28 @@ __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
   }
 }
 
+// every variable's candidate bitmap in one launch: slot s is all-ones over
+// [0, n_bits) if bit s of ones_mask is set (no seed), else zero (seeded)
+__global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, uint32_t n_bits, uint32_t ones_mask) {
+  const uint64_t total = (uint64_t)n_slots * stride;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(i / stride), w = (uint32_t)(i - (uint64_t)s * stride);
+    uint32_t v = 0;
+    if ((ones_mask >> s) & 1u) {
+      const uint64_t lo = (uint64_t)w * 32;
+      v = lo >= n_bits ? 0u : (lo + 32 <= n_bits ? 0xffffffffu : ((1u << (n_bits - lo)) - 1u));
+    }
+    cand[i] = v;
+  }
+}
+
+cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
+                              uint32_t ones_mask, cudaStream_t st) {
+  k_init_cands<<<grid_for((uint64_t)n_slots * stride_words, 256, 148 * 16), 256, 0, st>>>(cand, n_slots, stride_words,
+                                                                                        n_bits, ones_mask);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st) {
   k_fill_ones<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(bm, n_words, n_bits);
   return cudaGetLastError();
@@ -254,13 +276,6 @@ __global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __re
     uint32_t orv = __reduce_or_sync(peers, valid ? (1u << (id & 31)) : 0u);
     if (valid && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
   }
-}
-
-template <typename PT>
-__host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
-  Fmt<PT> f;
-  f.rp = a.rp; f.col = a.col; f.pred = (const PT*)a.pred;
-  return f;
 }
 
 cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
@@ -318,7 +333,8 @@ __device__ __forceinline__ uint32_t match_entry(const FilterArgsT<PT>& a, int d,
     if (j >= (int)a.ne[d]) break;
     if (l == a.e[d][j].label && !((sat >> j) & 1u)) {
       matched++;
-      bool ok = a.e[d][j].self ? (c == row) : (bit_of(a.e[d][j].nbr, c) != 0);
+      const uint32_t mode = a.e[d][j].mode;
+      bool ok = mode == GE_PROBE ? (bit_of(a.e[d][j].nbr, c) != 0) : (c == (mode == GE_SELF ? row : a.e[d][j].cval));
       if (ok) s |= 1u << j;
     }
   }
@@ -442,15 +458,23 @@ __global__ void __launch_bounds__(256) k_filter_heavy(FilterArgsT<PT> a) {
   }
 }
 
+// single CTA: clear the bits of heavy rows that missed an edge, then reset the
+// heavy-row state for the next launch (no host memsets between launches)
 template <typename PT>
 __global__ void k_filter_finalize(FilterArgsT<PT> a) {
   const uint32_t nr = a.heavy_count[0];
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) {
     const uint32_t rec = a.heavy_rows[i];
     const uint32_t row = rec & 0x7fffffffu;
     const int d = (int)(rec >> 31);
     const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
     if (a.heavy_sat[i] != need) atomicAnd(a.cand + (row >> 5), ~(1u << (row & 31)));
+    a.heavy_sat[i] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.heavy_count[0] = 0;
+    a.heavy_count[1] = 0;
   }
 }
 
@@ -482,9 +506,12 @@ static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_
   uint64_t want = ((uint64_t)a.n_words + 7) / 8;
   unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
   k_group_filter<PT><<<g, 256, 0, st>>>(t);
-  k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
-  k_filter_finalize<PT><<<(unsigned)sm_count, 256, 0, st>>>(t);
-  if (launches) *launches += 3;
+  if (launches) *launches += 1;
+  if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
+    k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
+    k_filter_finalize<PT><<<1, 1024, 0, st>>>(t);
+    if (launches) *launches += 2;
+  }
   return cudaGetLastError();
 }
 
@@ -492,245 +519,6 @@ cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_coun
                                 int* launches) {
   return pred_bytes == 1 ? group_filter_t<uint8_t>(a, sm_count, st, launches)
                          : group_filter_t<uint16_t>(a, sm_count, st, launches);
-}
-
-// =====================================================================================
-// a5 — compaction: bitmap -> ascending ids (popc per thread, block scan, tile offsets)
-// tile = 256 threads x 8 words
-// =====================================================================================
-constexpr int CW = 8, CB = 256, CT = CB * CW;
-
-__global__ void __launch_bounds__(CB) k_bitmap_count(const uint32_t* __restrict__ bm, uint32_t n_words,
-                                                    uint32_t* __restrict__ tile_cnt) {
-  __shared__ uint32_t sm[32];
-  uint64_t base = (uint64_t)blockIdx.x * CT + threadIdx.x * CW;
-  uint32_t c = 0;
-  if (base + CW <= n_words) {
-    uint4 a = *reinterpret_cast<const uint4*>(bm + base);
-    uint4 b = *reinterpret_cast<const uint4*>(bm + base + 4);
-    c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) + __popc(b.z) +
-        __popc(b.w);
-  } else {
-    for (int i = 0; i < CW; i++)
-      if (base + i < n_words) c += __popc(bm[base + i]);
-  }
-  c = block_reduce_sum<uint32_t>(c, sm);
-  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = c;
-}
-
-__global__ void __launch_bounds__(CB) k_bitmap_emit(const uint32_t* __restrict__ bm, uint32_t n_words,
-                                                   const uint32_t* __restrict__ tile_off, uint32_t* __restrict__ ids) {
-  __shared__ uint32_t sm[32];
-  uint64_t base = (uint64_t)blockIdx.x * CT + threadIdx.x * CW;
-  uint32_t wv[CW];
-  uint32_t c = 0;
-#pragma unroll
-  for (int i = 0; i < CW; i++) {
-    wv[i] = base + i < n_words ? bm[base + i] : 0u;
-    c += __popc(wv[i]);
-  }
-  uint32_t off = block_exclusive_scan<uint32_t>(c, sm, nullptr) + tile_off[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < CW; i++) {
-    uint32_t x = wv[i];
-    while (x) {
-      int b = __ffs(x) - 1;
-      x &= x - 1;
-      ids[off++] = (uint32_t)((base + i) * 32 + b);
-    }
-  }
-}
-
-size_t compact_tmp_bytes(uint32_t n_words) {
-  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT + 1;
-  return ((nt * sizeof(uint32_t) + 255) / 256) * 256 + scan_tmp_bytes(nt) + 512;
-}
-
-cudaError_t compact_count(const uint32_t* bm, uint32_t n_words, unsigned long long* count_dev, void* tmp,
-                          cudaStream_t st, int* launches) {
-  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT;
-  if (nt == 0) nt = 1;
-  uint32_t* tile = (uint32_t*)tmp;
-  void* stmp = (char*)tmp + ((nt * sizeof(uint32_t) + 255) / 256) * 256;
-  k_bitmap_count<<<(unsigned)nt, CB, 0, st>>>(bm, n_words, tile);
-  if (launches) *launches += 1;
-  return scan_exclusive_u32(tile, tile, nt, count_dev, stmp, st, launches);
-}
-
-cudaError_t compact_emit(const uint32_t* bm, uint32_t n_words, uint32_t* ids, void* tmp, cudaStream_t st,
-                         int* launches) {
-  uint64_t nt = ((uint64_t)n_words + CT - 1) / CT;
-  if (nt == 0) nt = 1;
-  k_bitmap_emit<<<(unsigned)nt, CB, 0, st>>>(bm, n_words, (const uint32_t*)tmp, ids);
-  if (launches) *launches += 1;
-  return cudaGetLastError();
-}
-
-// =====================================================================================
-// a6/a7 — tree expansion (§7.1, Alg. 1 l.5 / Alg. 2 l.7): level k children of each
-// level k-1 node n are the entries c of seg^dir_label(b_parent(n)) (or the candidate
-// list for a free level) with cand_v(c) (pre-pruning: bindings that failed the
-// grouped evaluation never enter the trie, §7.2.2) and every closing edge present.
-// count -> scan -> emit over work items of <= EXP_CHUNK entries.
-// =====================================================================================
-__device__ __forceinline__ uint32_t ancestor_bind(const LevelTab& t, uint32_t k, uint32_t n, uint32_t j) {
-  while (k > j) {
-    n = __ldg(t.parent[k] + n);
-    k--;
-  }
-  return __ldg(t.bind[j] + n);
-}
-
-template <typename PT>
-__global__ void k_expand_seg(ExpandArgs a) {
-  Fmt<PT> f = fmt_of<PT>(a.f[a.dir & 1]);
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < a.n_parents; n += gridDim.x * blockDim.x) {
-    uint32_t beg = 0, len = a.list_len;
-    if (a.tree) {
-      uint32_t b = ancestor_bind(a.tab, a.k - 1, n, a.parent_level);
-      uint32_t lo, hi;
-      label_range(f, b, a.label, lo, hi);
-      beg = lo; len = hi - lo;
-    }
-    a.seg_beg[n] = beg;
-    a.seg_len[n] = len;
-    a.item_off[n] = (len + EXP_CHUNK - 1) / EXP_CHUNK;
-  }
-}
-
-cudaError_t launch_expand_seg(const ExpandArgs& a, int pred_bytes, cudaStream_t st) {
-  unsigned g = grid_for(a.n_parents, 256, 148 * 32);
-  if (pred_bytes == 1) k_expand_seg<uint8_t><<<g, 256, 0, st>>>(a);
-  else k_expand_seg<uint16_t><<<g, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-__global__ void k_items_fill(ExpandArgs a) {
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < a.n_parents; n += gridDim.x * blockDim.x) {
-    uint32_t cnt = (a.seg_len[n] + EXP_CHUNK - 1) / EXP_CHUNK, off = a.item_off[n];
-    for (uint32_t i = 0; i < cnt; i++) a.item_node[off + i] = n;
-  }
-}
-
-cudaError_t launch_items_fill(const ExpandArgs& a, cudaStream_t st) {
-  k_items_fill<<<grid_for(a.n_parents, 256, 148 * 32), 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename PT, bool EMIT>
-__global__ void __launch_bounds__(256) k_expand_pass(ExpandArgs a) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  Fmt<PT> fsrc = fmt_of<PT>(a.f[a.dir & 1]);
-  Fmt<PT> fc[2] = {fmt_of<PT>(a.f[0]), fmt_of<PT>(a.f[1])};
-  unsigned long long n_exam = 0, n_close = 0;
-  for (uint32_t it = warp; it < a.n_items; it += nwarps) {
-    const uint32_t n = a.item_node[it];
-    const uint32_t chunk = it - a.item_off[n];
-    const uint32_t sb = a.seg_beg[n], sl = a.seg_len[n];
-    const uint32_t beg = sb + chunk * EXP_CHUNK, end = min(sb + sl, beg + EXP_CHUNK);
-    // closing-edge targets: binding of the other endpoint (lane j computes closing j)
-    uint32_t tgt = 0;
-    if (lane < a.ncl && a.cl[lane].self == 0) tgt = ancestor_bind(a.tab, a.k - 1, n, a.cl[lane].other_level);
-    uint32_t out = 0;
-    if (EMIT) out = a.item_cnt[it];
-    for (uint32_t base = beg; base < end; base += 32) {
-      const uint32_t kk = base + lane;
-      const bool valid = kk < end;
-      uint32_t child = 0;
-      bool keep = false;
-      if (valid) {
-        child = a.tree ? __ldg(fsrc.col + kk) : __ldg(a.list + kk);
-        keep = bit_of(a.cand, child) != 0;
-        n_exam++;
-      }
-      for (uint32_t j = 0; j < a.ncl; j++) {
-        const uint32_t t = __shfl_sync(GSM_FULL, tgt, j);
-        if (keep) {
-          const ClosingDev c = a.cl[j];
-          keep = has_entry(fc[c.dir & 1], child, c.label, c.self ? child : t);
-          n_close++;
-        }
-      }
-      const uint32_t bal = __ballot_sync(GSM_FULL, keep);
-      if (EMIT && keep) {
-        const uint32_t pos = out + __popc(bal & lanemask_lt());
-        a.out_parent[pos] = n;
-        a.out_bind[pos] = child;
-      }
-      out += __popc(bal);
-    }
-    if (!EMIT && lane == 0) a.item_cnt[it] = out;
-  }
-  if (!EMIT) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      n_exam += __shfl_down_sync(GSM_FULL, n_exam, o);
-      n_close += __shfl_down_sync(GSM_FULL, n_close, o);
-    }
-    if (lane == 0) {
-      if (n_exam) atomicAdd(a.ctr + C_EXPAND, n_exam);
-      if (n_close) atomicAdd(a.ctr + C_CLOSING, n_close);
-    }
-  }
-}
-
-cudaError_t launch_expand_pass(const ExpandArgs& a, int pred_bytes, bool emit, int sm_count, cudaStream_t st) {
-  uint64_t want = ((uint64_t)a.n_items + 7) / 8;
-  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
-  if (pred_bytes == 1) {
-    if (emit) k_expand_pass<uint8_t, true><<<g, 256, 0, st>>>(a);
-    else k_expand_pass<uint8_t, false><<<g, 256, 0, st>>>(a);
-  } else {
-    if (emit) k_expand_pass<uint16_t, true><<<g, 256, 0, st>>>(a);
-    else k_expand_pass<uint16_t, false><<<g, 256, 0, st>>>(a);
-  }
-  return cudaGetLastError();
-}
-
-// =====================================================================================
-// a8 — bottom-up tree pruning (§8.1 steps 3-4): a node survives iff some
-// child survives; the last level is all alive.  Byte stores are race-benign.
-// =====================================================================================
-__global__ void k_prune_mark(const uint32_t* __restrict__ parent, const uint8_t* __restrict__ alive, uint32_t n,
-                             uint8_t* __restrict__ alive_prev) {
-  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x)
-    if (!alive || alive[m]) alive_prev[parent[m]] = 1;
-}
-
-cudaError_t launch_prune_mark(const uint32_t* parent, const uint8_t* alive, uint32_t n, uint8_t* alive_prev,
-                              cudaStream_t st) {
-  k_prune_mark<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(parent, alive, n, alive_prev);
-  return cudaGetLastError();
-}
-
-__global__ void k_u8_to_u32(const uint8_t* in, uint32_t* out, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
-}
-
-cudaError_t launch_u8_to_u32(const uint8_t* in, uint32_t* out, uint32_t n, cudaStream_t st) {
-  k_u8_to_u32<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(in, out, n);
-  return cudaGetLastError();
-}
-
-__global__ void k_compact_level(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ bind,
-                                const uint8_t* __restrict__ alive, const uint32_t* __restrict__ newpos,
-                                const uint32_t* __restrict__ newidx_prev, uint32_t n, uint32_t* __restrict__ out_parent,
-                                uint32_t* __restrict__ out_bind) {
-  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
-    if (alive && !alive[m]) continue;
-    uint32_t q = newpos ? newpos[m] : m;
-    out_bind[q] = bind[m];
-    if (parent && out_parent) out_parent[q] = newidx_prev ? newidx_prev[parent[m]] : parent[m];
-  }
-}
-
-cudaError_t launch_compact_level(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
-                                 const uint32_t* newpos, const uint32_t* newidx_prev, uint32_t n,
-                                 uint32_t* out_parent, uint32_t* out_bind, cudaStream_t st) {
-  k_compact_level<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(parent, bind, alive, newpos, newidx_prev, n,
-                                                              out_parent, out_bind);
-  return cudaGetLastError();
 }
 
 // =====================================================================================

@@ -42,16 +42,35 @@ struct FmtAny {
   const uint32_t* col;
   const void* pred;
 };
+template <typename PT>
+__host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
+  Fmt<PT> f;
+  f.rp = a.rp;
+  f.col = a.col;
+  f.pred = (const PT*)a.pred;
+  return f;
+}
+
+// decoupled look-back state of one launch (lookback.cuh)
+struct LBArgs {
+  unsigned long long* status;  // epoch-stamped tile status words [cap_tiles]
+  uint32_t* counter;           // zeroed tile counter of this launch
+  uint32_t epoch;              // 1..65535, distinct per launch
+  uint32_t cap_tiles;
+};
 cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
                                 unsigned long long* ctr, int sm_count, cudaStream_t st);
 cudaError_t launch_guard(FmtAny f, int pred_bytes, uint32_t s, uint32_t label, uint32_t o, int* flag,
                          cudaStream_t st);
 
 // ----------------------------------------------------------------- a4 grouped incident-edge filter
+enum GEdgeMode : uint32_t { GE_PROBE = 0, GE_SELF = 1, GE_CONST = 2 };
 struct GEdge {
-  const uint32_t* nbr;  // neighbour candidate bitmap (unused for self-loops)
+  const uint32_t* nbr;  // GE_PROBE: neighbour candidate bitmap
   uint32_t label;
-  uint32_t self;        // 1: self-loop pattern (entry must have col == row)
+  uint32_t mode;        // GE_PROBE: cand_w(col); GE_SELF: col == row (self-loop); GE_CONST: col == cval (seed)
+  uint32_t cval;
+  uint32_t pad;
 };
 struct FilterArgs {
   FmtAny f[2];              // CSR (OUT edges), CSC (IN edges)
@@ -62,22 +81,16 @@ struct FilterArgs {
   uint32_t* heavy_rows;     // records: row | dir << 31
   uint32_t* heavy_chunks;   // records: heavy-row slot, chunk index (2 x uint32)
   uint32_t* heavy_sat;      // per heavy-row slot: OR of satisfied-edge bits
-  uint32_t* heavy_count;    // [0] rows, [1] chunks
+  uint32_t* heavy_count;    // [0] rows, [1] chunks (zero between launches; finalize resets)
   unsigned long long* ctr;
+  int heavy;                // launch the heavy-row kernels
 };
+cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
+                              uint32_t ones_mask, cudaStream_t st);
 cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_count, cudaStream_t st,
                                 int* launches);
 
-// ----------------------------------------------------------------- a5 compaction
-// bitmap -> ascending id list in two calls sharing tmp: count (total to
-// *count_dev) then emit (ids sized from the count).
-size_t compact_tmp_bytes(uint32_t n_words);
-cudaError_t compact_count(const uint32_t* bm, uint32_t n_words, unsigned long long* count_dev, void* tmp,
-                          cudaStream_t st, int* launches);
-cudaError_t compact_emit(const uint32_t* bm, uint32_t n_words, uint32_t* ids, void* tmp, cudaStream_t st,
-                         int* launches);
-
-// ----------------------------------------------------------------- a6/a7 expansion
+// ----------------------------------------------------------------- trie tables
 struct LevelTab {
   const uint32_t* parent[MAXL];
   const uint32_t* bind[MAXL];
@@ -85,40 +98,46 @@ struct LevelTab {
 struct ClosingDev {
   uint32_t label, other_level, dir, self;
 };
-struct ExpandArgs {
+
+// ----------------------------------------------------------------- sync-free expansion (expand.cu)
+struct ExpArgs2 {
   LevelTab tab;
-  uint32_t k;               // level being built (>= 1); parents are level k-1
-  uint32_t n_parents;       // F_{k-1}
-  int tree;                 // 1: children = seg_label(dir)(binding at parent_level); 0: children = list
+  uint32_t k;                              // level being built (>= 1)
+  const unsigned long long* d_nparent;     // F_{k-1} (device)
+  uint64_t cap_par;                        // capacity of parent-side arrays (seg_beg, off)
+  int tree;
   uint32_t parent_level, label, dir;
   FmtAny f[2];
-  const uint32_t* list;     // free level: candidate id list
-  uint32_t list_len;
-  const uint32_t* cand;     // candidate bitmap of the level's variable
+  const uint32_t* list;                    // free level: candidate id list
+  const unsigned long long* d_list_len;
+  const uint32_t* cand;
   ClosingDev cl[MAXC];
   uint32_t ncl;
-  // work arrays
-  uint32_t* seg_beg;        // [n_parents]
-  uint32_t* seg_len;        // [n_parents]
-  uint32_t* item_off;       // [n_parents] (in: counts, out: exclusive offsets)
-  uint32_t* item_node;      // [n_items]
-  uint32_t n_items;
-  uint32_t* item_cnt;       // [n_items] (count pass; then exclusive offsets)
+  uint32_t* seg_beg;                       // [cap_par]
+  uint32_t* off;                           // [cap_par + 1]
+  unsigned long long* d_T;                 // total entries of level k
   uint32_t* out_parent;
   uint32_t* out_bind;
+  uint8_t* out_alive;                      // zeroed for emitted nodes (prune flags), may be null
+  uint64_t cap_out;
+  unsigned long long* d_nout;              // F_k (device)
+  int* overflow;                           // |= 1 capacity (retry), |= 2 fatal (> 2^32 entries)
   unsigned long long* ctr;
+  LBArgs lb;
 };
-cudaError_t launch_expand_seg(const ExpandArgs& a, int pred_bytes, cudaStream_t st);
-cudaError_t launch_items_fill(const ExpandArgs& a, cudaStream_t st);
-cudaError_t launch_expand_pass(const ExpandArgs& a, int pred_bytes, bool emit, int sm_count, cudaStream_t st);
+cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
+                                     unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
+                                     cudaStream_t st);
+cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
+cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
+cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
+                                uint8_t* alive_prev, int sm_count, cudaStream_t st);
+cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
+                                    const unsigned long long* d_n, const uint32_t* newidx_prev, uint32_t* out_parent,
+                                    uint32_t* out_bind, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
+                                    int sm_count, cudaStream_t st);
 
 // ----------------------------------------------------------------- a8 prune, a9 rows
-cudaError_t launch_prune_mark(const uint32_t* parent, const uint8_t* alive, uint32_t n, uint8_t* alive_prev,
-                              cudaStream_t st);
-cudaError_t launch_u8_to_u32(const uint8_t* in, uint32_t* out, uint32_t n, cudaStream_t st);
-cudaError_t launch_compact_level(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
-                                 const uint32_t* newpos, const uint32_t* newidx_prev, uint32_t n,
-                                 uint32_t* out_parent, uint32_t* out_bind, cudaStream_t st);
 cudaError_t launch_enumerate(const LevelTab& tab, uint32_t n_levels, const uint32_t* col_of_level,
                              uint32_t n_last, uint32_t n_cols, uint32_t* rows, cudaStream_t st);
 size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols);

@@ -1,0 +1,175 @@
+// Library-internal state shared by runtime.cu (context, load, build, results)
+// and execute.cu (slots, executor).  Product code.
+#pragma once
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gsmart.h"
+#include "internal.h"
+#include "kernels.h"
+#include "nccl_shim.h"
+
+namespace gsm {
+
+enum Kid {
+  K_BUILD_PACK = 0, K_BUILD_SORT, K_BUILD_UNIQUE, K_BUILD_ROWPTR, K_SEED, K_FILTER, K_BITMAP, K_COMPACT,
+  K_SCAN, K_EXPAND_SEG, K_EXPAND_COUNT, K_EXPAND_EMIT, K_PRUNE, K_ENUMERATE, K_SORT_ROWS, K_COLLECTIVE
+};
+extern const char* kKernelNames[GSMART_NKERNELS];
+
+struct Lspm {
+  uint32_t* rp = nullptr;
+  uint32_t* col = nullptr;
+  void* pred = nullptr;
+  uint64_t nnz = 0;
+  bool built = false;
+  unsigned long long heavy_rows = 0, heavy_chunks = 0;
+};
+
+inline int bits_for(uint64_t v) {  // bits to represent values in [0, v]
+  int b = 1;
+  while (b < 64 && (v >> b) != 0) b++;
+  return b;
+}
+
+constexpr uint32_t LB_CAP_TILES = 1u << 22;  // 4M tiles x 1024 entries = the 2^32-entry limit
+constexpr uint32_t LB_EPOCHS = 65536;
+constexpr uint32_t MAX_SLOTS = 16;
+
+// One concurrent execution lane: a stream plus everything an in-flight
+// execute writes (workspace, look-back state, counters, pinned readback).
+struct Slot {
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev = nullptr;
+  struct LvBuf {
+    uint64_t cap = 0;
+    uint32_t *bind = nullptr, *parent = nullptr, *seg_beg = nullptr, *off = nullptr, *newidx = nullptr;
+    uint8_t* alive = nullptr;
+  };
+  LvBuf lv[GSMART_MAX_LEVELS];
+  uint32_t* list[GSMART_MAX_LEVELS] = {};
+  uint64_t list_cap[GSMART_MAX_LEVELS] = {};
+  unsigned long long* lb_status = nullptr;
+  uint32_t* lb_counters = nullptr;
+  uint32_t epoch = 0;
+  unsigned long long* d_sz = nullptr;  // [0,32) F_k, [32,64) T_k, [64,96) list len, [96,128) alive, 127 overflow
+  int* d_ovf = nullptr;
+  unsigned long long* d_ctr = nullptr; // C_NCTR counters, then scratch (flag at 48)
+  unsigned long long* h_pin = nullptr; // 256 pinned slots
+  uint32_t *heavy_rows = nullptr, *heavy_chunks = nullptr, *heavy_sat = nullptr, *heavy_cnt = nullptr;
+  uint64_t heavy_gen = ~0ull;          // LSpM generation the heavy buffers were sized for
+};
+
+}  // namespace gsm
+
+struct gsmart_ctx {
+  gsmart_config cfg{};
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  bool poisoned = false;
+  std::string err;
+  int sm_count = 148;
+  uint32_t N = 0, P = 0;
+  uint64_t n_triples = 0;
+  uint32_t *d_s = nullptr, *d_p = nullptr, *d_o = nullptr;
+  int pred_bytes = 1;
+  gsm::Lspm f[2];
+  uint64_t lspm_gen = 0;
+  unsigned long long* d_ctr = nullptr;  // load/build scratch
+  unsigned long long* h_pin = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<std::unique_ptr<gsm::Slot>> slots;
+  uint64_t cap() const { return cfg.max_result_rows ? cfg.max_result_rows : 0x7fffffffull; }
+};
+
+struct gsmart_result {
+  gsmart_ctx* ctx = nullptr;
+  cudaStream_t st = nullptr;     // stream the result's memory is ordered on
+  uint64_t n_rows = 0;
+  uint32_t n_cols = 0;
+  std::vector<uint32_t> var_of_col;
+  uint32_t* d_rows = nullptr;
+  std::vector<uint32_t> h_rows;
+  bool host_valid = false;
+  bool count_only = false;
+  uint32_t* d_cand = nullptr;
+  uint32_t n_words = 0, stride_words = 0;
+  std::vector<int32_t> cand_slot;  // vertex -> slot or -1
+  struct Lv { uint32_t var; uint64_t n; uint32_t* parent; uint32_t* bind; };
+  std::vector<Lv> levels;
+  std::vector<void*> owned;        // device allocations to free
+  gsmart_stats stats{};
+};
+
+namespace gsm {
+
+extern thread_local std::string g_static_err;
+
+gsmart_status cuda_fail(gsmart_ctx* ctx, cudaError_t e, const char* what, int line);
+
+#define FAIL(code, msg) \
+  do {                  \
+    ctx->err = (msg);   \
+    return (code);      \
+  } while (0)
+
+#define CU(x)                                                         \
+  do {                                                                \
+    cudaError_t e_ = (x);                                             \
+    if (e_ != cudaSuccess) return gsm::cuda_fail(ctx, e_, #x, __LINE__); \
+  } while (0)
+
+#define TRY(x)                      \
+  do {                              \
+    gsmart_status s_ = (x);         \
+    if (s_ != GSMART_OK) return s_; \
+  } while (0)
+
+template <typename T>
+gsmart_status dalloc(gsmart_ctx* ctx, T** p, uint64_t count, cudaStream_t st) {
+  *p = nullptr;
+  size_t bytes = std::max<uint64_t>(count, 1) * sizeof(T);
+  bytes = (bytes + 255) / 256 * 256;
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocAsync", __LINE__);
+  return GSMART_OK;
+}
+template <typename T>
+gsmart_status dalloc(gsmart_ctx* ctx, T** p, uint64_t count) {
+  return dalloc(ctx, p, count, ctx->st);
+}
+
+inline void dfree(cudaStream_t st, void* p) {
+  if (p) cudaFreeAsync(p, st);
+}
+inline void dfree(gsmart_ctx* ctx, void* p) { dfree(ctx->st, p); }
+
+// stream-ordered scratch freed at scope exit
+struct Scratch {
+  gsmart_ctx* ctx;
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  Scratch(gsmart_ctx* c, cudaStream_t s) : ctx(c), st(s) {}
+  explicit Scratch(gsmart_ctx* c) : ctx(c), st(c->st) {}
+  ~Scratch() {
+    for (void* p : ptrs) dfree(st, p);
+  }
+  template <typename T>
+  gsmart_status get(T** p, uint64_t count) {
+    gsmart_status s = dalloc(ctx, p, count, st);
+    if (s == GSMART_OK) ptrs.push_back((void*)*p);
+    return s;
+  }
+};
+
+gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_pin, const unsigned long long* dev,
+                       int n, unsigned long long* host);
+
+void slots_free(gsmart_ctx* ctx);
+
+}  // namespace gsm

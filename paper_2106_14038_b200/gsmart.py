@@ -86,6 +86,7 @@ def _load():
         "gsmart_plan_describe": (st, [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "gsmart_plan_free": (None, [vp]),
         "gsmart_execute": (st, [vp, vp, u32, ctypes.POINTER(vp)]),
+        "gsmart_execute_batch": (st, [vp, ctypes.POINTER(vp), u32, u32, ctypes.POINTER(vp)]),
         "gsmart_result_shape": (st, [vp, ctypes.POINTER(u64), ctypes.POINTER(u32),
                                      ctypes.POINTER(ctypes.POINTER(u32))]),
         "gsmart_result_rows": (st, [vp, ctypes.POINTER(ctypes.POINTER(u32))]),
@@ -107,7 +108,8 @@ def _load():
 _lib = _load()
 EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gsmart_create", "gsmart_destroy",
             "gsmart_last_error", "gsmart_load_triples", "gsmart_build_lspm", "gsmart_lspm_get", "gsmart_plan",
-            "gsmart_plan_describe", "gsmart_plan_free", "gsmart_execute", "gsmart_result_shape",
+            "gsmart_plan_describe", "gsmart_plan_free", "gsmart_execute", "gsmart_execute_batch",
+            "gsmart_result_shape",
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
             "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host"]
 
@@ -248,6 +250,15 @@ def gsmart_execute(ctx, plan, flags=0):
     return h
 
 
+def gsmart_execute_batch(ctx, plans, flags=0):
+    """Run independent plans concurrently; returns one result handle per plan."""
+    n = len(plans)
+    arr = (ctypes.c_void_p * max(n, 1))(*[p.value if isinstance(p, ctypes.c_void_p) else p for p in plans])
+    out = (ctypes.c_void_p * max(n, 1))()
+    _check(_lib.gsmart_execute_batch(ctx, arr, n, flags, out), ctx)
+    return [ctypes.c_void_p(out[i]) for i in range(n)]
+
+
 def gsmart_result_shape(r):
     n = ctypes.c_uint64()
     c = ctypes.c_uint32()
@@ -330,6 +341,27 @@ class Engine:
 
     def plan(self, q):
         return Plan(self, q)
+
+    def query_batch(self, queries, flags=0):
+        """Execute several queries concurrently (gsmart_execute_batch); returns rows per query."""
+        plans = [Plan(self, q) for q in queries]
+        try:
+            res = gsmart_execute_batch(self.ctx, [p.h for p in plans], flags)
+            out = []
+            for r in res:
+                try:
+                    if flags & GSMART_COUNT_ONLY:
+                        out.append(gsmart_result_shape(r)[0])
+                    elif flags & GSMART_KEEP_ON_DEVICE:
+                        out.append(None)
+                    else:
+                        out.append(gsmart_result_rows(r))
+                finally:
+                    gsmart_result_free(r)
+            return out
+        finally:
+            for p in plans:
+                p.close()
 
     def query(self, q, flags=0, with_stats=False):
         with self.plan(q) as pl:

@@ -159,6 +159,20 @@ def test_lubm_queries_vs_oracle(G, eng, U):
     assert eng.query(L2, flags=G.GSMART_COUNT_ONLY) == d.n_courses
 
 
+def test_execute_batch_matches_single(G, eng):
+    """gsmart_execute_batch (concurrent slots, > 16 plans => several waves) gives
+    exactly the per-query results of the oracle."""
+    d = lubm.generate(4)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = lubm.queries(d) * 3
+    for q, got in zip(qs, eng.query_batch(qs)):
+        assert np.array_equal(got, ix.query(q)), q.name
+    counts = eng.query_batch(qs[:8], flags=G.GSMART_COUNT_ONLY)
+    assert counts == [len(ix.query(q)) for q in qs[:8]]
+
+
 def test_lubm_device_input_and_keep_set(G, eng):
     import torch
     d = lubm.generate(3)
