@@ -29,6 +29,7 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   CU(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
   TRY(dalloc(ctx, &s.lb_status, LB_CAP_TILES, s.st));
   TRY(dalloc(ctx, &s.lb_counters, LB_EPOCHS, s.st));
+  TRY(dalloc(ctx, &s.tile_start, LB_CAP_TILES, s.st));
   TRY(dalloc(ctx, &s.d_sz, 128, s.st));
   TRY(dalloc(ctx, &s.d_ovf, 1, s.st));
   TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
@@ -48,7 +49,7 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
     dfree(st, b.alive);
   }
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
-  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
+  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
   cudaStreamSynchronize(st);
   if (s.h_pin) cudaFreeHost(s.h_pin);
@@ -342,6 +343,7 @@ struct Exec {
       }
       a.seg_beg = sl.lv[k - 1].seg_beg;
       a.off = sl.lv[k - 1].off;
+      a.tile_start = sl.tile_start;
       a.d_T = dsz + 32 + k;
       a.out_parent = sl.lv[k].parent;
       a.out_bind = sl.lv[k].bind;

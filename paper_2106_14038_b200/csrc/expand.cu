@@ -91,6 +91,7 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
 
 // ------------------------------------------------------------------ level k: segments + scan
 constexpr int SS_T = 256, SS_I = 4, SS_TILE = SS_T * SS_I;
+constexpr int EX_T = 256, EX_I = 4, EX_TILE = EX_T * EX_I;  // expansion tile (entries)
 
 template <typename PT>
 __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
@@ -137,18 +138,24 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
       const uint64_t n = base + j;
       if (n < F) {
         a.off[n] = (uint32_t)run;
+        // the parent holding each expansion-tile boundary t records itself, so
+        // k_expand_lb finds a tile's parent range without a global search
+        for (uint64_t t = (run + EX_TILE - 1) / EX_TILE * EX_TILE; t < run + len[j]; t += EX_TILE)
+          if (t / EX_TILE < a.lb.cap_tiles) a.tile_start[t / EX_TILE] = (uint32_t)n;
         run += len[j];
       }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
-      a.off[F] = (uint32_t)(pref + tot);
-      *a.d_T = pref + tot;
+      const uint64_t T = pref + tot;
+      a.off[F] = (uint32_t)T;
+      *a.d_T = T;
+      const uint64_t nt = (T + EX_TILE - 1) / EX_TILE;
+      if (nt < a.lb.cap_tiles) a.tile_start[nt] = (uint32_t)F;  // sentinel
     }
   }
 }
 
 // ------------------------------------------------------------------ level k: expansion
-constexpr int EX_T = 256, EX_I = 4, EX_TILE = EX_T * EX_I;
 constexpr uint32_t OFFCAP = 2048, TGTP = 1024, TGTC = 4;
 
 template <typename PT>
@@ -180,8 +187,8 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
     const uint32_t base = tile * EX_TILE;
     const uint32_t last = (uint32_t)min((uint64_t)base + EX_TILE, T) - 1;
     if (threadIdx.x == 0) {
-      s_nlo = ub_global(a.off, F1, base) - 1;
-      s_nhi = ub_global(a.off, F1, last) - 1;
+      s_nlo = __ldg(a.tile_start + tile);
+      s_nhi = min(__ldg(a.tile_start + tile + 1), (uint32_t)F - 1);
     }
     __syncthreads();
     const uint32_t nlo = s_nlo, nr = s_nhi - s_nlo + 1;

@@ -265,16 +265,43 @@ __global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __re
   }
   __syncthreads();
   const uint32_t lo = s_lo, hi = s_hi;
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t base = lo + warp * 32; base < hi; base += nwarps * 32) {
-    uint32_t k = base + lane;
-    bool valid = k < hi;
-    uint32_t id = valid ? __ldg(f.col + k) : 0u;
-    uint32_t word = valid ? (id >> 5) : 0xffffffffu;
-    uint32_t peers = __match_any_sync(GSM_FULL, word);
-    uint32_t orv = __reduce_or_sync(peers, valid ? (1u << (id & 31)) : 0u);
-    if (valid && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
+  __shared__ uint32_t s_words[8][32];  // per-warp window of 32 bitmap words
+  // a warp takes 128 consecutive (sorted) entries: lane i reads entries 4i..4i+3.
+  // If they span < 32 words, bits are OR-ed into a shared window and written with
+  // one atomicOr per non-zero word; else per-entry warp-aggregated atomics.
+  for (uint32_t base = lo + warp * 128; base < hi; base += nwarps * 128) {
+    uint32_t id[4];
+    bool v[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t k = base + lane * 4 + j;
+      v[j] = k < hi;
+      id[j] = v[j] ? __ldg(f.col + k) : 0u;
+    }
+    const uint32_t w_first = __shfl_sync(GSM_FULL, id[0], 0) >> 5;
+    const uint32_t last_k = min(hi, base + 128) - 1 - base;
+    const uint32_t w_last = __shfl_sync(GSM_FULL, id[last_k & 3], last_k >> 2) >> 5;
+    if (w_last - w_first < 32) {
+      s_words[wib][lane] = 0;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (v[j]) atomicOr(&s_words[wib][(id[j] >> 5) - w_first], 1u << (id[j] & 31));
+      __syncwarp();
+      const uint32_t x = s_words[wib][lane];
+      if (x) atomicOr(bits + w_first + lane, x);
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint32_t word = v[j] ? (id[j] >> 5) : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(GSM_FULL, word);
+        const uint32_t orv = __reduce_or_sync(peers, v[j] ? (1u << (id[j] & 31)) : 0u);
+        if (v[j] && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
+      }
+    }
   }
 }
 
@@ -347,9 +374,20 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   unsigned long long n_rows = 0, n_scanned = 0;
   uint32_t n_matched = 0;
-  for (uint32_t w = warp; w < a.n_words; w += nwarps) {
-    const uint32_t m = a.cand[w];
-    if (m == 0) continue;
+  // a warp owns chunks of 32 consecutive bitmap words (1024 rows): one coalesced
+  // load of the chunk, then only its non-zero words are processed (sparse
+  // candidate sets cost one load per 1024 rows, not one dependent load per word)
+  const uint32_t n_chunks = (a.n_words + 31) >> 5;
+  for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
+    const uint32_t wl = (ch << 5) + lane;
+    const uint32_t mine = wl < a.n_words ? a.cand[wl] : 0u;
+    uint32_t mnew = mine;
+    uint32_t nz = __ballot_sync(GSM_FULL, mine != 0);
+   while (nz) {
+    const int jw = __ffs(nz) - 1;
+    nz &= nz - 1;
+    const uint32_t w = (ch << 5) + jw;
+    const uint32_t m = __shfl_sync(GSM_FULL, mine, jw);
     const uint32_t row = (w << 5) + lane;
     bool ok = (m >> lane) & 1u;
 #pragma unroll
@@ -411,7 +449,9 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
       ok = ok && (sat == need);
     }
     const uint32_t nw = __ballot_sync(GSM_FULL, ok);
-    if (lane == 0 && nw != m) a.cand[w] = nw;
+    if ((int)lane == jw) mnew = nw;
+   }
+    if (mnew != mine) a.cand[wl] = mnew;
   }
   // one atomic per warp per counter
 #pragma unroll
@@ -503,7 +543,7 @@ template <typename PT>
 static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_t st, int* launches) {
   FilterArgsT<PT> t = to_t<PT>(a);
   // 8 warps per CTA; enough CTAs for ~16 resident warps/SM-worth of words, grid-stride beyond
-  uint64_t want = ((uint64_t)a.n_words + 7) / 8;
+  uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;  // one 32-word chunk per warp
   unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
   k_group_filter<PT><<<g, 256, 0, st>>>(t);
   if (launches) *launches += 1;

@@ -115,6 +115,7 @@ struct ExpArgs2 {
   uint32_t ncl;
   uint32_t* seg_beg;                       // [cap_par]
   uint32_t* off;                           // [cap_par + 1]
+  uint32_t* tile_start;                    // [lb.cap_tiles]: parent holding each expansion-tile boundary
   unsigned long long* d_T;                 // total entries of level k
   uint32_t* out_parent;
   uint32_t* out_bind;
