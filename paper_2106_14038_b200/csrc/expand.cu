@@ -45,35 +45,50 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __re
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
   const uint32_t ntiles = (n_words + BC_TILE - 1) / BC_TILE;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // warp wib of a tile owns words [tile*2048 + wib*256, +256) in 8 coalesced rounds of
+  // 32 words; ids are emitted warp-cooperatively (lane b writes bit b of each word)
   while (true) {
     const uint32_t tile = lb_claim(lb.counter, &s_tile);
     if (tile >= ntiles) break;
-    const uint64_t base = (uint64_t)tile * BC_TILE + threadIdx.x * BC_W;
-    uint32_t w[BC_W];
-    if (base + BC_W <= n_words) {
-      uint4 x = *reinterpret_cast<const uint4*>(bm + base);
-      uint4 y = *reinterpret_cast<const uint4*>(bm + base + 4);
-      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w; w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
-    } else {
+    const uint64_t wbase = (uint64_t)tile * BC_TILE + wib * (BC_W * 32);
+    uint32_t w[BC_W], off[BC_W];
+    uint32_t run = 0;  // words of earlier rounds in this warp
 #pragma unroll
-      for (int i = 0; i < BC_W; i++) w[i] = base + i < n_words ? bm[base + i] : 0u;
+    for (int r = 0; r < BC_W; r++) {
+      const uint64_t wi = wbase + r * 32 + lane;
+      w[r] = wi < n_words ? __ldcg(bm + wi) : 0u;
     }
-    unsigned long long c = 0;
 #pragma unroll
-    for (int i = 0; i < BC_W; i++) c += __popc(w[i]);
+    for (int r = 0; r < BC_W; r++) {
+      const uint32_t c = __popc(w[r]);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(GSM_FULL, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      off[r] = run + incl - c;
+      run += __shfl_sync(GSM_FULL, incl, 31);
+    }
+    // block: exclusive scan of the 8 warp totals
     unsigned long long tot;
-    unsigned long long ex = block_exclusive_scan<unsigned long long>(c, s_red, &tot);
+    const unsigned long long wex =
+        block_exclusive_scan<unsigned long long>(lane == 0 ? (unsigned long long)run : 0ull, s_red, &tot);
     const uint64_t pref = lb_prefix(lb.status, lb.epoch, tile, tot, &s_pref);
-    uint64_t pos = pref + ex;
+    const uint64_t base_pos = pref + __shfl_sync(GSM_FULL, wex, 0);
 #pragma unroll
-    for (int i = 0; i < BC_W; i++) {
-      uint32_t x = w[i];
-      while (x) {
-        int b = __ffs(x) - 1;
-        x &= x - 1;
-        if (pos < cap) ids[pos] = (uint32_t)((base + i) * 32 + b);
-        else atomicOr(overflow, 1);
-        pos++;
+    for (int r = 0; r < BC_W; r++) {
+      uint32_t nz = __ballot_sync(GSM_FULL, w[r] != 0);
+      while (nz) {
+        const int j = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t wj = __shfl_sync(GSM_FULL, w[r], j), oj = __shfl_sync(GSM_FULL, off[r], j);
+        if ((wj >> lane) & 1u) {
+          const uint64_t pos = base_pos + oj + __popc(wj & lanemask_lt());
+          if (pos < cap) ids[pos] = (uint32_t)((wbase + r * 32 + j) * 32 + lane);
+          else atomicOr(overflow, 1);
+        }
       }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) *d_count = pref + tot;

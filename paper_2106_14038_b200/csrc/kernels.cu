@@ -368,90 +368,158 @@ __device__ __forceinline__ uint32_t match_entry(const FilterArgsT<PT>& a, int d,
   return s;
 }
 
+// Evaluate the group's edges of one direction set for 32 candidate rows, one per
+// lane (lanes with has == false idle).  Returns per-lane "all edges satisfied".
+template <typename PT>
+__device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32_t row, const bool has,
+                                          const uint32_t lane, unsigned long long& n_rows,
+                                          unsigned long long& n_scanned, uint32_t& n_matched) {
+  bool ok = has;
+#pragma unroll
+  for (int d = 0; d < 2; d++) {
+    if (a.ne[d] == 0) continue;
+    const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
+    uint32_t b = 0, e = 0, sat = 0;
+    bool medium = false;
+    if (ok) {
+      b = __ldg(a.f[d].rp + row);
+      e = __ldg(a.f[d].rp + row + 1);
+      n_rows++;
+      const uint32_t len = e - b;
+      if (len > HEAVY_ROW) {
+        // defer: provisional keep; chunks OR their satisfied edges into heavy_sat[slot]
+        const uint32_t slot = atomicAdd(a.heavy_count, 1u);
+        const uint32_t nch = (len + HEAVY_CHUNK - 1) / HEAVY_CHUNK;
+        const uint32_t c0 = atomicAdd(a.heavy_count + 1, nch);
+        a.heavy_rows[slot] = row | ((uint32_t)d << 31);
+        for (uint32_t c = 0; c < nch; c++) {
+          a.heavy_chunks[2 * (c0 + c)] = slot;
+          a.heavy_chunks[2 * (c0 + c) + 1] = c;
+        }
+        sat = need;
+      } else if (len > SHORT_ROW) {
+        medium = true;
+      } else {
+        // 4 entries per step: their pred loads, then col loads, then bitmap probes
+        // are issued together (3 dependent load levels per 4 entries, not 12)
+        for (uint32_t k = b; k < e && sat != need; k += 4) {
+          uint32_t l[4], c[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) l[j] = k + j < e ? (uint32_t)__ldg(a.f[d].pred + k + j) : 0xffffffffu;
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            c[j] = (l[j] >= a.minl[d] && l[j] <= a.maxl[d]) ? __ldg(a.f[d].col + k + j) : 0u;
+          bool past = false;
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            if (l[j] == 0xffffffffu) break;
+            n_scanned++;
+            if (l[j] > a.maxl[d]) { past = true; break; }
+            if (l[j] >= a.minl[d]) sat |= match_entry(a, d, l[j], c[j], row, sat, n_matched);
+          }
+          if (past) break;
+        }
+      }
+    }
+    // warp-cooperative scan of medium rows, one row at a time
+    uint32_t mm = __ballot_sync(GSM_FULL, medium);
+    while (mm) {
+      const int src = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const uint32_t rb = __shfl_sync(GSM_FULL, b, src), re = __shfl_sync(GSM_FULL, e, src);
+      const uint32_t rrow = __shfl_sync(GSM_FULL, row, src);
+      uint32_t wsat = 0;
+      for (uint32_t base = rb; base < re; base += 32) {
+        const uint32_t k = base + lane;
+        uint32_t s = 0;
+        if (k < re) {
+          const uint32_t l = __ldg(a.f[d].pred + k);
+          n_scanned++;
+          if (l >= a.minl[d] && l <= a.maxl[d]) s = match_entry(a, d, l, __ldg(a.f[d].col + k), rrow, wsat, n_matched);
+        }
+        wsat |= __reduce_or_sync(GSM_FULL, s);
+        if (wsat == need) break;
+      }
+      if ((int)lane == src) sat = wsat;
+    }
+    ok = ok && (sat == need);
+  }
+  return ok;
+}
+
+// clear the candidate bits of failed rows (one atomicAnd per distinct word per warp)
+__device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row, const bool fail, const uint32_t lane) {
+  const uint32_t word = fail ? (row >> 5) : 0xffffffffu;
+  const uint32_t peers = __match_any_sync(GSM_FULL, word);
+  const uint32_t bits = __reduce_or_sync(peers, fail ? (1u << (row & 31)) : 0u);
+  if (fail && (int)lane == __ffs(peers) - 1) atomicAnd(cand + word, ~bits);
+}
+
 template <typename PT>
 __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
-  const uint32_t lane = threadIdx.x & 31;
+  constexpr uint32_t QCAP = 1024 + 32;
+  __shared__ uint32_t s_q[8][QCAP];  // per-warp queue of candidate rows
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t* q = s_q[wib];
   unsigned long long n_rows = 0, n_scanned = 0;
   uint32_t n_matched = 0;
-  // a warp owns chunks of 32 consecutive bitmap words (1024 rows): one coalesced
-  // load of the chunk, then only its non-zero words are processed (sparse
-  // candidate sets cost one load per 1024 rows, not one dependent load per word)
+  // A warp streams chunks of 32 bitmap words (1024 rows; one coalesced load,
+  // next chunk prefetched), queues the candidate rows (set bits, ascending) and
+  // evaluates them 32 at a time, one row per lane: sparse candidate sets keep
+  // every lane busy and all rows of a batch have their loads in flight together.
   const uint32_t n_chunks = (a.n_words + 31) >> 5;
-  for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
+  uint32_t qn = 0;  // warp-uniform queue length
+  uint32_t ch = warp;
+  uint32_t nxt = 0;
+  if (ch < n_chunks) {
     const uint32_t wl = (ch << 5) + lane;
-    const uint32_t mine = wl < a.n_words ? a.cand[wl] : 0u;
-    uint32_t mnew = mine;
-    uint32_t nz = __ballot_sync(GSM_FULL, mine != 0);
-   while (nz) {
-    const int jw = __ffs(nz) - 1;
-    nz &= nz - 1;
-    const uint32_t w = (ch << 5) + jw;
-    const uint32_t m = __shfl_sync(GSM_FULL, mine, jw);
-    const uint32_t row = (w << 5) + lane;
-    bool ok = (m >> lane) & 1u;
-#pragma unroll
-    for (int d = 0; d < 2; d++) {
-      if (a.ne[d] == 0) continue;
-      const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
-      uint32_t b = 0, e = 0, sat = 0;
-      bool medium = false;
-      if (ok) {
-        b = __ldg(a.f[d].rp + row);
-        e = __ldg(a.f[d].rp + row + 1);
-        n_rows++;
-        uint32_t len = e - b;
-        if (len > HEAVY_ROW) {
-          // defer: provisional keep; chunks OR their satisfied edges into heavy_sat[slot]
-          uint32_t slot = atomicAdd(a.heavy_count, 1u);
-          uint32_t nch = (len + HEAVY_CHUNK - 1) / HEAVY_CHUNK;
-          uint32_t c0 = atomicAdd(a.heavy_count + 1, nch);
-          a.heavy_rows[slot] = row | ((uint32_t)d << 31);
-          for (uint32_t c = 0; c < nch; c++) {
-            a.heavy_chunks[2 * (c0 + c)] = slot;
-            a.heavy_chunks[2 * (c0 + c) + 1] = c;
-          }
-          sat = need;
-        } else if (len > SHORT_ROW) {
-          medium = true;
-        } else {
-          for (uint32_t k = b; k < e && sat != need; k++) {
-            uint32_t l = __ldg(a.f[d].pred + k);
-            n_scanned++;
-            if (l < a.minl[d]) continue;
-            if (l > a.maxl[d]) break;
-            sat |= match_entry(a, d, l, __ldg(a.f[d].col + k), row, sat, n_matched);
-          }
-        }
-      }
-      // warp-cooperative scan of medium rows, one row at a time
-      uint32_t mm = __ballot_sync(GSM_FULL, medium);
-      while (mm) {
-        const int src = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const uint32_t rb = __shfl_sync(GSM_FULL, b, src), re = __shfl_sync(GSM_FULL, e, src);
-        const uint32_t rrow = (w << 5) + src;
-        uint32_t wsat = 0;
-        for (uint32_t base = rb; base < re; base += 32) {
-          uint32_t k = base + lane;
-          uint32_t s = 0;
-          if (k < re) {
-            uint32_t l = __ldg(a.f[d].pred + k);
-            n_scanned++;
-            if (l >= a.minl[d] && l <= a.maxl[d])
-              s = match_entry(a, d, l, __ldg(a.f[d].col + k), rrow, wsat, n_matched);
-          }
-          wsat |= __reduce_or_sync(GSM_FULL, s);
-          if (wsat == need) break;
-        }
-        if ((int)lane == src) sat = wsat;
-      }
-      ok = ok && (sat == need);
+    nxt = wl < a.n_words ? __ldcg(a.cand + wl) : 0u;
+  }
+  for (; ch < n_chunks; ch += nwarps) {
+    const uint32_t mine = nxt;
+    const uint32_t wl = (ch << 5) + lane;
+    if (ch + nwarps < n_chunks) {
+      const uint32_t wn = ((ch + nwarps) << 5) + lane;
+      nxt = wn < a.n_words ? __ldcg(a.cand + wn) : 0u;
     }
-    const uint32_t nw = __ballot_sync(GSM_FULL, ok);
-    if ((int)lane == jw) mnew = nw;
-   }
-    if (mnew != mine) a.cand[wl] = mnew;
+    const uint32_t cnt = __popc(mine);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(GSM_FULL, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(GSM_FULL, incl, 31);
+    if (total == 0) continue;
+    uint32_t pos = qn + incl - cnt, bits = mine;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      q[pos++] = (wl << 5) + b;
+    }
+    __syncwarp();
+    qn += total;
+    uint32_t done = 0;
+    for (; qn - done >= 32; done += 32) {
+      const uint32_t row = q[done + lane];
+      const bool ok = eval_rows(a, row, true, lane, n_rows, n_scanned, n_matched);
+      clear_failed(a.cand, row, !ok, lane);
+    }
+    if (done) {  // move the (< 32) leftovers to the front
+      const uint32_t left = qn - done;
+      const uint32_t v = lane < left ? q[done + lane] : 0u;
+      __syncwarp();
+      if (lane < left) q[lane] = v;
+      __syncwarp();
+      qn = left;
+    }
+  }
+  if (qn) {
+    const bool has = lane < qn;
+    const uint32_t row = has ? q[lane] : 0u;
+    const bool ok = eval_rows(a, row, has, lane, n_rows, n_scanned, n_matched);
+    clear_failed(a.cand, row, has && !ok, lane);
   }
   // one atomic per warp per counter
 #pragma unroll
@@ -544,7 +612,7 @@ static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_
   FilterArgsT<PT> t = to_t<PT>(a);
   // 8 warps per CTA; enough CTAs for ~16 resident warps/SM-worth of words, grid-stride beyond
   uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;  // one 32-word chunk per warp
-  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 16);
+  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 6);  // one wave
   k_group_filter<PT><<<g, 256, 0, st>>>(t);
   if (launches) *launches += 1;
   if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
