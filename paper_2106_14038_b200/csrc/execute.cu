@@ -33,10 +33,10 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   TRY(dalloc(ctx, &s.d_sz, 128, s.st));
   TRY(dalloc(ctx, &s.d_ovf, 1, s.st));
   TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
-  TRY(dalloc(ctx, &s.heavy_cnt, 2, s.st));
+  TRY(dalloc(ctx, &s.heavy_cnt, 4, s.st));
   CU(cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st));
   CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
-  CU(cudaMemsetAsync(s.heavy_cnt, 0, 8, s.st));
+  CU(cudaMemsetAsync(s.heavy_cnt, 0, 16, s.st));
   CU(cudaMallocHost(&s.h_pin, 256 * sizeof(unsigned long long)));
   s.epoch = 0;
   return GSMART_OK;
@@ -288,6 +288,7 @@ struct Exec {
       a.heavy_sat = sl.heavy_sat;
       a.heavy_count = sl.heavy_cnt;
       a.ctr = sl.d_ctr;
+      a.variant = ctx->filter_variant;
       prof.begin(K_FILTER);
       CU(launch_group_filter(a, ctx->pred_bytes, ctx->sm_count, sl.st, &launches[K_FILTER]));
       prof.end();

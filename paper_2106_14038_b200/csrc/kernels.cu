@@ -349,6 +349,7 @@ struct FilterArgsT {
   uint32_t* heavy_sat;
   uint32_t* heavy_count;
   unsigned long long* ctr;
+  int variant;
 };
 
 template <typename PT>
@@ -366,6 +367,61 @@ __device__ __forceinline__ uint32_t match_entry(const FilterArgsT<PT>& a, int d,
     }
   }
   return s;
+}
+
+// Short row (<= SHORT_ROW entries) with uint8 labels: the row's labels are read
+// with <= 3 aligned 16-byte loads; each edge's label range [lo, hi) inside the
+// row follows from SIMD byte compares (__vcmpltu4 / __vcmpeq4 + popc), then only
+// the cols of that range are loaded and probed.  4 dependent load levels per row.
+template <typename PT>
+__device__ __forceinline__ uint32_t short_row_u8(const FilterArgsT<PT>& a, const int d, const uint32_t row,
+                                                 const uint32_t b, const uint32_t e, const uint32_t need,
+                                                 unsigned long long& n_scanned, uint32_t& n_matched) {
+  const uint8_t* P = reinterpret_cast<const uint8_t*>(a.f[d].pred);
+  const uint32_t a0 = b & ~15u;
+  uint32_t w[12];
+  const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(P + a0));
+  const uint4 v1 = a0 + 16 < e ? __ldg(reinterpret_cast<const uint4*>(P + a0 + 16)) : make_uint4(0, 0, 0, 0);
+  const uint4 v2 = a0 + 32 < e ? __ldg(reinterpret_cast<const uint4*>(P + a0 + 32)) : make_uint4(0, 0, 0, 0);
+  w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
+  w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+  w[8] = v2.x; w[9] = v2.y; w[10] = v2.z; w[11] = v2.w;
+  uint32_t vm[12];  // byte masks of positions inside [b, e)
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    const int p0 = (int)(a0 + 4 * i);
+    const int lo = min(max((int)b - p0, 0), 4), hi = min(max((int)e - p0, 0), 4);
+    const uint32_t mhi = hi >= 4 ? 0xffffffffu : ((1u << (8 * hi)) - 1u);
+    const uint32_t mlo = lo >= 4 ? 0xffffffffu : ((1u << (8 * lo)) - 1u);
+    vm[i] = mhi & ~mlo;
+  }
+  n_scanned += e - b;
+  uint32_t sat = 0;
+#pragma unroll
+  for (int j = 0; j < MAXG; j++) {
+    if (j >= (int)a.ne[d]) break;
+    const uint32_t L = a.e[d][j].label * 0x01010101u;
+    uint32_t lt = 0, eq = 0;
+#pragma unroll
+    for (int i = 0; i < 12; i++) {
+      lt += __popc(__vcmpltu4(w[i], L) & vm[i]);
+      eq += __popc(__vcmpeq4(w[i], L) & vm[i]);
+    }
+    uint32_t k = b + (lt >> 3);
+    const uint32_t kend = k + (eq >> 3);
+    const uint32_t mode = a.e[d][j].mode;
+    for (; k < kend; k++) {
+      const uint32_t c = __ldg(a.f[d].col + k);
+      n_matched++;
+      const bool ok = mode == GE_PROBE ? (bit_of(a.e[d][j].nbr, c) != 0) : (c == (mode == GE_SELF ? row : a.e[d][j].cval));
+      if (ok) {
+        sat |= 1u << j;
+        break;
+      }
+    }
+  }
+  (void)need;
+  return sat;
 }
 
 // Evaluate the group's edges of one direction set for 32 candidate rows, one per
@@ -399,6 +455,8 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
         sat = need;
       } else if (len > SHORT_ROW) {
         medium = true;
+      } else if (sizeof(PT) == 1 && (a.variant & 1)) {
+        sat = short_row_u8(a, d, row, b, e, need, n_scanned, n_matched);
       } else {
         // 4 entries per step: their pred loads, then col loads, then bitmap probes
         // are issued together (3 dependent load levels per 4 entries, not 12)
@@ -457,8 +515,8 @@ __device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row,
 
 template <typename PT>
 __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
-  constexpr uint32_t QCAP = 1024 + 32;
-  __shared__ uint32_t s_q[8][QCAP];  // per-warp queue of candidate rows
+  constexpr uint32_t QCAP = 64;
+  __shared__ uint32_t s_q[8][QCAP];  // per-warp queue of candidate rows (< 64)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   uint32_t* q = s_q[wib];
@@ -470,49 +528,50 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   // every lane busy and all rows of a batch have their loads in flight together.
   const uint32_t n_chunks = (a.n_words + 31) >> 5;
   uint32_t qn = 0;  // warp-uniform queue length
+  const bool dyn = (a.variant & 2) != 0;
   uint32_t ch = warp;
+  if (dyn) {
+    uint32_t c0 = 0;
+    if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
+    ch = __shfl_sync(GSM_FULL, c0, 0);
+  }
   uint32_t nxt = 0;
   if (ch < n_chunks) {
     const uint32_t wl = (ch << 5) + lane;
     nxt = wl < a.n_words ? __ldcg(a.cand + wl) : 0u;
   }
-  for (; ch < n_chunks; ch += nwarps) {
+  while (ch < n_chunks) {
     const uint32_t mine = nxt;
-    const uint32_t wl = (ch << 5) + lane;
-    if (ch + nwarps < n_chunks) {
-      const uint32_t wn = ((ch + nwarps) << 5) + lane;
+    uint32_t cn = ch + nwarps;
+    if (dyn) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
+      cn = __shfl_sync(GSM_FULL, c0, 0);
+    }
+    if (cn < n_chunks) {
+      const uint32_t wn = (cn << 5) + lane;
       nxt = wn < a.n_words ? __ldcg(a.cand + wn) : 0u;
     }
-    const uint32_t cnt = __popc(mine);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(GSM_FULL, incl, o);
-      if ((int)lane >= o) incl += y;
-    }
-    const uint32_t total = __shfl_sync(GSM_FULL, incl, 31);
-    if (total == 0) continue;
-    uint32_t pos = qn + incl - cnt, bits = mine;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      q[pos++] = (wl << 5) + b;
-    }
-    __syncwarp();
-    qn += total;
-    uint32_t done = 0;
-    for (; qn - done >= 32; done += 32) {
-      const uint32_t row = q[done + lane];
-      const bool ok = eval_rows(a, row, true, lane, n_rows, n_scanned, n_matched);
-      clear_failed(a.cand, row, !ok, lane);
-    }
-    if (done) {  // move the (< 32) leftovers to the front
-      const uint32_t left = qn - done;
-      const uint32_t v = lane < left ? q[done + lane] : 0u;
+    const uint32_t chc = ch;
+    ch = cn;
+    uint32_t nz = __ballot_sync(GSM_FULL, mine != 0);
+    while (nz) {  // enqueue word by word (queue holds < 64 rows), evaluate 32 at a time
+      const int j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t wj = __shfl_sync(GSM_FULL, mine, j);
+      if ((wj >> lane) & 1u) q[qn + __popc(wj & lanemask_lt())] = (((chc << 5) + j) << 5) + lane;
+      qn += __popc(wj);
       __syncwarp();
-      if (lane < left) q[lane] = v;
-      __syncwarp();
-      qn = left;
+      if (qn >= 32) {
+        const uint32_t row = q[lane];
+        const uint32_t extra = lane + 32 < qn ? q[lane + 32] : 0u;
+        __syncwarp();
+        if (lane + 32 < qn) q[lane] = extra;
+        qn -= 32;
+        __syncwarp();
+        const bool ok = eval_rows(a, row, true, lane, n_rows, n_scanned, n_matched);
+        clear_failed(a.cand, row, !ok, lane);
+      }
     }
   }
   if (qn) {
@@ -583,6 +642,7 @@ __global__ void k_filter_finalize(FilterArgsT<PT> a) {
   if (threadIdx.x == 0) {
     a.heavy_count[0] = 0;
     a.heavy_count[1] = 0;
+    a.heavy_count[2] = 0;  // dynamic chunk counter
   }
 }
 
@@ -603,7 +663,7 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
   }
   t.cand = a.cand; t.n_words = a.n_words;
   t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
-  t.heavy_count = a.heavy_count; t.ctr = a.ctr;
+  t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant;
   return t;
 }
 
@@ -617,8 +677,11 @@ static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_
   if (launches) *launches += 1;
   if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
     k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
+    if (launches) *launches += 1;
+  }
+  if (a.heavy || (a.variant & 2)) {  // clears failed heavy rows, resets counters
     k_filter_finalize<PT><<<1, 1024, 0, st>>>(t);
-    if (launches) *launches += 2;
+    if (launches) *launches += 1;
   }
   return cudaGetLastError();
 }

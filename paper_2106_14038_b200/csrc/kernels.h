@@ -84,6 +84,7 @@ struct FilterArgs {
   uint32_t* heavy_count;    // [0] rows, [1] chunks (zero between launches; finalize resets)
   unsigned long long* ctr;
   int heavy;                // launch the heavy-row kernels
+  int variant;              // bit0: SIMD label ranges (uint8 labels); bit1: dynamic chunk claiming
 };
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
                               uint32_t ones_mask, cudaStream_t st);

@@ -105,6 +105,7 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   auto ctx = std::make_unique<gsmart_ctx>();
   ctx->cfg = *cfg;
   ctx->sm_count = prop.multiProcessorCount;
+  if (const char* fv = getenv("GSMART_FILTER_VARIANT")) ctx->filter_variant = atoi(fv);
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     g_static_err = "cudaSetDevice failed";
     return GSMART_E_CUDA;
@@ -266,7 +267,7 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
   if (M >= 0xffffffffull) FAIL(GSMART_E_UNSUPPORTED, "more than 2^32-2 entries in one LSpM format");
   TRY(dalloc(ctx, &L.rp, (uint64_t)N + 1));
   TRY(dalloc(ctx, &L.col, M));
-  TRY(dalloc(ctx, (uint8_t**)&L.pred, M * ctx->pred_bytes));
+  TRY(dalloc(ctx, (uint8_t**)&L.pred, M * ctx->pred_bytes + 64));  // +64: 16-byte label loads may overrun
   CU(cudaMemsetAsync(L.rp, 0, ((uint64_t)N + 1) * 4, ctx->st));
   if (n) CU(launch_unpack(keys2, n, flags, drop_bit, sh_row, sh_pred, L.col, L.pred, ctx->pred_bytes, L.rp, ctx->st));
   {

@@ -81,6 +81,7 @@ struct gsmart_ctx {
   int pred_bytes = 1;
   gsm::Lspm f[2];
   uint64_t lspm_gen = 0;
+  int filter_variant = 2;               // see FilterArgs::variant (GSMART_FILTER_VARIANT)
   unsigned long long* d_ctr = nullptr;  // load/build scratch
   unsigned long long* h_pin = nullptr;
   ncclComm_t comm = nullptr;
