@@ -77,14 +77,29 @@ typedef enum {
 typedef struct gsmart_ctx gsmart_ctx;
 typedef struct gsmart_plan_s gsmart_plan_t;
 typedef struct gsmart_result gsmart_result;
+typedef struct gsmart_comm gsmart_comm;
 
 typedef struct {
   int device;                 /* CUDA device ordinal */
-  int rank, world;            /* world >= 1; world > 1 = 1-D row partition over ranks */
-  const void* nccl_unique_id; /* 128 bytes from gsmart_get_nccl_id on rank 0; NULL if world == 1 */
+  int rank, world;            /* world >= 1; world > 1 = 1-D vertex-range partition over ranks */
+  const void* nccl_unique_id; /* 128 bytes from gsmart_get_nccl_id on rank 0 (world > 1 over NCCL) */
   void* stream;               /* cudaStream_t to run on, or NULL: the library creates one */
   uint64_t max_result_rows;   /* capacity for rows and for each trie level; 0 = 2^31 - 1 */
+  gsmart_comm* local_comm;    /* world > 1 inside one process (one thread per rank) instead of NCCL; else NULL */
 } gsmart_config;
+
+/* In-process communicator for `world` ranks driven by `world` host threads of
+ * one process (ranks may share a GPU).  Pass it as cfg.local_comm to every
+ * rank's gsmart_create; destroy after every rank's context.  Collective calls
+ * (execute with world > 1) must be made by all ranks in the same order. */
+gsmart_status gsmart_comm_create_local(int world, gsmart_comm** out);
+void gsmart_comm_destroy(gsmart_comm* comm);
+
+/* The bitmap word range [word_lo, word_hi) (32 entities per word) that rank
+ * `rank` of `world` owns in the 1-D vertex-range partition: the ranks filter
+ * their own candidate rows and root bindings (host helper, no device). */
+gsmart_status gsmart_partition_words(uint32_t n_entities, int world, int rank, uint32_t* word_lo,
+                                     uint32_t* word_hi);
 
 /* ABI version and a build string (static storage). */
 int gsmart_abi_version(void);

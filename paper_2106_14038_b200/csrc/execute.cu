@@ -175,6 +175,8 @@ struct Exec {
   int launches[GSMART_NKERNELS] = {0};
   uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
   int attempts = 0;
+  uint32_t wlo = 0, whi = 0, slice = 0;  // this rank's bitmap words (1-D vertex-range partition)
+  bool identity = false;                 // trie order == column order: rows come out sorted
   std::vector<uint64_t> F;
   std::chrono::steady_clock::time_point t0;
 
@@ -282,7 +284,8 @@ struct Exec {
         if (a.ne[d] && ctx->f[d].heavy_rows) a.heavy = 1;
       }
       a.cand = cand(g.center);
-      a.n_words = W;
+      a.word_lo = wlo & ~31u;
+      a.n_words = whi > wlo ? whi : 0;  // this rank's rows only (world > 1)
       a.heavy_rows = sl.heavy_rows;
       a.heavy_chunks = sl.heavy_chunks;
       a.heavy_sat = sl.heavy_sat;
@@ -294,6 +297,13 @@ struct Exec {
       prof.end();
       filter_main++;
     }
+    if (ctx->world > 1) {  // every rank needs the whole candidate bitmap of the center
+      prof.begin(K_COLLECTIVE);
+      TRY(coll_allgather(ctx, sl.st, cand(g.center), (size_t)slice * 4));
+      prof.end();
+      launches[K_COLLECTIVE]++;
+      R->stats.allgather_bytes += (uint64_t)(ctx->world - 1) * slice * 4;
+    }
     return GSMART_OK;
   }
 
@@ -304,8 +314,9 @@ struct Exec {
     CU(cudaMemsetAsync(sl.d_ovf, 0, 4, sl.st));
     if (L > 1) CU(cudaMemsetAsync(sl.lv[0].alive, 0, sl.lv[0].cap, sl.st));
     prof.begin(K_COMPACT);
-    CU(launch_bitmap_compact_lb(cand(plan->levels[0].var), W, sl.lv[0].bind, sl.lv[0].cap, dsz + 0, sl.d_ovf,
-                                next_lb(sl), ctx->sm_count, sl.st));
+    // level 0 = this rank's root candidates (its word range; all of them when world == 1)
+    CU(launch_bitmap_compact_lb(cand(plan->levels[0].var) + wlo, whi - wlo, sl.lv[0].bind, sl.lv[0].cap, dsz + 0,
+                                sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
     launches[K_COMPACT]++;
     prof.end();
     for (uint32_t k = 1; k < L; k++) {
@@ -376,7 +387,18 @@ struct Exec {
     const uint32_t nvar = (uint32_t)plan->vars.size();
     W = (N + 31) / 32;
     Wpad = (W + 31) / 32 * 32;
+    wlo = 0;
+    whi = W;
+    if (ctx->world > 1) {
+      slice = partition_slice(W, ctx->world);
+      wlo = std::min<uint32_t>((uint32_t)ctx->rank * slice, W);
+      whi = std::min<uint32_t>(wlo + slice, W);
+      Wpad = std::max<uint32_t>(Wpad, slice * (uint32_t)ctx->world);  // all-gather needs world equal slices
+    }
     L = (uint32_t)plan->levels.size();
+    identity = true;
+    for (uint32_t k = 0; k < L; k++)
+      if ((uint32_t)plan->col_of[plan->levels[k].var] != k) identity = false;
     R->n_words = W;
     R->stride_words = Wpad;
     slot.assign(plan->n_vertices, -1);
@@ -497,11 +519,7 @@ struct Exec {
     if (!(flags & GSMART_COUNT_ONLY)) {
       const uint32_t nc = (uint32_t)plan->vars.size();
       std::vector<uint32_t> col_of_level(L);
-      bool identity = true;
-      for (uint32_t k = 0; k < L; k++) {
-        col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
-        if (col_of_level[k] != k) identity = false;
-      }
+      for (uint32_t k = 0; k < L; k++) col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
       uint32_t* rows = nullptr;
       TRY(identity ? alloc_result((void**)&rows, n_rows * nc * 4) : sc.get(&rows, n_rows * nc));
       prof.begin(K_ENUMERATE);
@@ -526,6 +544,40 @@ struct Exec {
   }
 
   // after the slot stream drained
+  // world > 1: every rank holds the rows of its own root bindings; rank 0
+  // gathers them (rank order = ascending root ranges) and sorts unless the trie
+  // order is already the column order.  All ranks report the global count.
+  gsmart_status gather_rows() {
+    std::vector<unsigned long long> cnt;
+    TRY(coll_allgather_host(ctx, sl.st, R->n_rows, &cnt));
+    uint64_t total = 0;
+    for (auto c : cnt) total += c;
+    const uint32_t nc = R->n_cols;
+    if (!(flags & GSMART_COUNT_ONLY) && total && nc) {
+      std::vector<unsigned long long> bytes(ctx->world);
+      for (int q = 0; q < ctx->world; q++) bytes[q] = cnt[q] * nc * 4;
+      uint32_t* all = nullptr;
+      if (ctx->rank == 0) TRY(alloc_result((void**)&all, total * nc * 4));
+      prof.begin(K_COLLECTIVE);
+      TRY(coll_gather_root(ctx, sl.st, R->d_rows, all, bytes));
+      prof.end();
+      launches[K_COLLECTIVE]++;
+      if (ctx->rank == 0 && !identity) {
+        uint32_t* sorted = nullptr;
+        TRY(alloc_result((void**)&sorted, total * nc * 4));
+        const size_t tb = sort_rows_tmp_bytes(total, nc);
+        void* tmp = nullptr;
+        TRY(sc.get((char**)&tmp, tb));
+        CU(sort_rows(all, sorted, total, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
+        all = sorted;
+      }
+      R->d_rows = ctx->rank == 0 ? all : nullptr;  // rows live on rank 0
+      CU(cudaStreamSynchronize(sl.st));
+    }
+    R->n_rows = total;
+    return GSMART_OK;
+  }
+
   gsmart_status finalize() {
     prof.flush();
     if (state == S_PHASE2 && R->n_rows) {
@@ -534,6 +586,7 @@ struct Exec {
         R->stats.level_alive[k] = sl.h_pin[128 + k];
       }
     }
+    if (ctx->world > 1 && state == S_PHASE2) TRY(gather_rows());
     unsigned long long c[C_NCTR];
     CU(cudaMemcpy(c, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost));
     auto& st = R->stats;
@@ -578,7 +631,9 @@ gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan) {
 gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint32_t n, uint32_t flags,
                         gsmart_result** out) {
   for (uint32_t i = 0; i < n; i++) TRY(check_plan(ctx, plans[i]));
-  const uint32_t ns = std::min<uint32_t>(std::max<uint32_t>(n, 1), MAX_SLOTS);
+  // world > 1: collectives of one plan complete before the next plan starts (same
+  // order on every rank), so a batch runs one plan at a time on slot 0
+  const uint32_t ns = ctx->world > 1 ? 1u : std::min<uint32_t>(std::max<uint32_t>(n, 1), MAX_SLOTS);
   TRY(ensure_slots(ctx, ns));
   // fork: every slot stream starts after the work already queued on ctx->st
   cudaEvent_t fork;
@@ -648,7 +703,6 @@ extern "C" gsmart_status gsmart_execute(gsmart_ctx* ctx, const gsmart_plan_t* pl
   *out = nullptr;
   if (ctx->poisoned) return GSMART_E_CUDA;
   if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
-  if (ctx->cfg.world > 1) FAIL(GSMART_E_UNSUPPORTED, "world > 1 execute is not available in this build");
   CU(cudaSetDevice(ctx->cfg.device));
   return run_batch(ctx, &plan, 1, flags, out);
 }
@@ -659,7 +713,6 @@ extern "C" gsmart_status gsmart_execute_batch(gsmart_ctx* ctx, const gsmart_plan
   for (uint32_t i = 0; i < n; i++) out[i] = nullptr;
   if (ctx->poisoned) return GSMART_E_CUDA;
   if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
-  if (ctx->cfg.world > 1) FAIL(GSMART_E_UNSUPPORTED, "world > 1 execute is not available in this build");
   CU(cudaSetDevice(ctx->cfg.device));
   gsmart_status s = run_batch(ctx, plans, n, flags, out);
   if (s != GSMART_OK)

@@ -40,7 +40,7 @@ constexpr int BC_T = 256, BC_W = 8, BC_TILE = BC_T * BC_W;  // words per tile
 __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __restrict__ bm, uint32_t n_words,
                                                            uint32_t* __restrict__ ids, uint64_t cap,
                                                            unsigned long long* d_count, int* overflow,
-                                                           LBArgs lb) {
+                                                           LBArgs lb, uint32_t id_base) {
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __re
         const uint32_t wj = __shfl_sync(GSM_FULL, w[r], j), oj = __shfl_sync(GSM_FULL, off[r], j);
         if ((wj >> lane) & 1u) {
           const uint64_t pos = base_pos + oj + __popc(wj & lanemask_lt());
-          if (pos < cap) ids[pos] = (uint32_t)((wbase + r * 32 + j) * 32 + lane);
+          if (pos < cap) ids[pos] = (uint32_t)((wbase + r * 32 + j) * 32 + lane) + id_base;
           else atomicOr(overflow, 1);
         }
       }
@@ -97,10 +97,10 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __re
 
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, uint32_t id_base) {
   uint32_t ntiles = (n_words + BC_TILE - 1) / BC_TILE;
   unsigned g = std::max(1u, std::min(ntiles, (uint32_t)sm_count * 8));
-  k_bitmap_compact_lb<<<g, BC_T, 0, st>>>(bm, n_words, ids, cap, d_count, overflow, lb);
+  k_bitmap_compact_lb<<<g, BC_T, 0, st>>>(bm, n_words, ids, cap, d_count, overflow, lb, id_base);
   return cudaGetLastError();
 }
 

@@ -350,6 +350,7 @@ struct FilterArgsT {
   uint32_t* heavy_count;
   unsigned long long* ctr;
   int variant;
+  uint32_t word_lo;
 };
 
 template <typename PT>
@@ -529,11 +530,12 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   const uint32_t n_chunks = (a.n_words + 31) >> 5;
   uint32_t qn = 0;  // warp-uniform queue length
   const bool dyn = (a.variant & 2) != 0;
-  uint32_t ch = warp;
+  const uint32_t c_begin = a.word_lo >> 5;  // partitioned: this rank's first chunk
+  uint32_t ch = c_begin + warp;
   if (dyn) {
     uint32_t c0 = 0;
     if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
-    ch = __shfl_sync(GSM_FULL, c0, 0);
+    ch = c_begin + __shfl_sync(GSM_FULL, c0, 0);
   }
   uint32_t nxt = 0;
   if (ch < n_chunks) {
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     if (dyn) {
       uint32_t c0 = 0;
       if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
-      cn = __shfl_sync(GSM_FULL, c0, 0);
+      cn = c_begin + __shfl_sync(GSM_FULL, c0, 0);
     }
     if (cn < n_chunks) {
       const uint32_t wn = (cn << 5) + lane;
@@ -663,7 +665,7 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
   }
   t.cand = a.cand; t.n_words = a.n_words;
   t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
-  t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant;
+  t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant; t.word_lo = a.word_lo;
   return t;
 }
 

@@ -85,6 +85,7 @@ struct FilterArgs {
   unsigned long long* ctr;
   int heavy;                // launch the heavy-row kernels
   int variant;              // bit0: SIMD label ranges (uint8 labels); bit1: dynamic chunk claiming
+  uint32_t word_lo;         // first bitmap word of this rank's range (multiple of 32); n_words = end
 };
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
                               uint32_t ones_mask, cudaStream_t st);
@@ -127,9 +128,10 @@ struct ExpArgs2 {
   unsigned long long* ctr;
   LBArgs lb;
 };
+// ids of set bits of bm[0, n_words) plus id_base
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
-                                     cudaStream_t st);
+                                     cudaStream_t st, uint32_t id_base = 0);
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,

@@ -130,10 +130,18 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
     g_static_err = "context allocation failed";
     return GSMART_E_OOM;
   }
-  if (cfg->world > 1) {
+  ctx->rank = cfg->rank;
+  ctx->world = cfg->world;
+  if (cfg->world > 1 && cfg->local_comm) {
+    if (cfg->local_comm->world != cfg->world) {
+      g_static_err = "local_comm world differs from cfg.world";
+      return GSMART_E_INVALID_ARG;
+    }
+    ctx->lcomm = cfg->local_comm;
+  } else if (cfg->world > 1) {
     const NcclApi* api = nccl_api();
     if (!api || !cfg->nccl_unique_id) {
-      g_static_err = "world > 1 needs NCCL and a unique id";
+      g_static_err = "world > 1 needs NCCL and a unique id (or a local_comm)";
       return GSMART_E_NCCL;
     }
     ncclUniqueId id;

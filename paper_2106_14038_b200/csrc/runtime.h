@@ -2,7 +2,9 @@
 // and execute.cu (slots, executor).  Product code.
 #pragma once
 #include <algorithm>
+#include <condition_variable>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -68,6 +70,32 @@ struct Slot {
 
 }  // namespace gsm
 
+// In-process communicator: `world` ranks, one host thread each (any devices).
+// Collectives rendezvous on a generation barrier and copy device buffers
+// directly (cudaMemcpyPeerAsync), standing in for NCCL when all ranks live in
+// one process (tests on one GPU, or one process driving several GPUs).
+struct gsmart_comm {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptr;
+  std::vector<int> dev;
+  std::vector<unsigned long long> val;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct gsmart_ctx {
   gsmart_config cfg{};
   cudaStream_t st = nullptr;
@@ -84,7 +112,9 @@ struct gsmart_ctx {
   int filter_variant = 2;               // see FilterArgs::variant (GSMART_FILTER_VARIANT)
   unsigned long long* d_ctr = nullptr;  // load/build scratch
   unsigned long long* h_pin = nullptr;
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;     // world > 1 with NCCL
+  gsmart_comm* lcomm = nullptr;  // world > 1 with an in-process communicator
+  int rank = 0, world = 1;
   std::vector<std::unique_ptr<gsm::Slot>> slots;
   uint64_t cap() const { return cfg.max_result_rows ? cfg.max_result_rows : 0x7fffffffull; }
 };
@@ -173,5 +203,22 @@ gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_p
                        int n, unsigned long long* host);
 
 void slots_free(gsmart_ctx* ctx);
+
+// ---- 1-D vertex-range partition of the bitmaps: rank r owns
+// words [r*slice, min((r+1)*slice, n_words)) with slice a multiple of 32 words.
+inline uint32_t partition_slice(uint32_t n_words, int world) {
+  const uint32_t chunks = (n_words + 31) / 32;
+  return ((chunks + world - 1) / world) * 32;
+}
+
+// ---- collectives for world > 1 (NCCL or the in-process communicator), comm.cu
+// In-place all-gather: rank r's bytes_per_rank bytes at buf + r*bytes_per_rank.
+gsmart_status coll_allgather(gsmart_ctx* ctx, cudaStream_t st, void* buf, size_t bytes_per_rank);
+// Host values of all ranks (blocking).
+gsmart_status coll_allgather_host(gsmart_ctx* ctx, cudaStream_t st, unsigned long long v,
+                                  std::vector<unsigned long long>* out);
+// Rank r's send_bytes[r] bytes land at recv + sum_{q<r} send_bytes[q] on rank 0 (blocking).
+gsmart_status coll_gather_root(gsmart_ctx* ctx, cudaStream_t st, const void* send, void* recv,
+                               const std::vector<unsigned long long>& send_bytes);
 
 }  // namespace gsm

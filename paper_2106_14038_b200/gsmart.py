@@ -33,7 +33,7 @@ class GsmartError(RuntimeError):
 class gsmart_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("max_result_rows", ctypes.c_uint64)]
+                ("max_result_rows", ctypes.c_uint64), ("local_comm", ctypes.c_void_p)]
 
 
 class gsmart_lspm_view(ctypes.Structure):
@@ -97,6 +97,9 @@ def _load():
         "gsmart_result_stats": (st, [vp, ctypes.POINTER(gsmart_stats)]),
         "gsmart_result_free": (None, [vp]),
         "gsmart_copy_to_host": (st, [vp, vp, vp, ctypes.c_size_t]),
+        "gsmart_comm_create_local": (st, [ctypes.c_int, ctypes.POINTER(vp)]),
+        "gsmart_comm_destroy": (None, [vp]),
+        "gsmart_partition_words": (st, [u32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(u32), ctypes.POINTER(u32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -111,7 +114,8 @@ EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gs
             "gsmart_plan_describe", "gsmart_plan_free", "gsmart_execute", "gsmart_execute_batch",
             "gsmart_result_shape",
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
-            "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host"]
+            "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host",
+            "gsmart_comm_create_local", "gsmart_comm_destroy", "gsmart_partition_words"]
 
 
 def lib():
@@ -139,8 +143,9 @@ def gsmart_get_nccl_id():
     return buf.raw
 
 
-def gsmart_create(device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0):
+def gsmart_create(device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None):
     cfg = gsmart_config()
+    cfg.local_comm = local_comm.value if isinstance(local_comm, ctypes.c_void_p) else local_comm
     cfg.device, cfg.rank, cfg.world = device, rank, world
     idbuf = None
     if nccl_id is not None:
@@ -151,6 +156,22 @@ def gsmart_create(device=0, rank=0, world=1, nccl_id=None, stream=None, max_resu
     h = ctypes.c_void_p()
     _check(_lib.gsmart_create(ctypes.byref(cfg), ctypes.byref(h)))
     return h
+
+
+def gsmart_comm_create_local(world):
+    h = ctypes.c_void_p()
+    _check(_lib.gsmart_comm_create_local(world, ctypes.byref(h)))
+    return h
+
+
+def gsmart_comm_destroy(comm):
+    _lib.gsmart_comm_destroy(comm)
+
+
+def gsmart_partition_words(n_entities, world, rank):
+    lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.gsmart_partition_words(n_entities, world, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
 
 
 def gsmart_destroy(ctx):
@@ -332,8 +353,8 @@ def gsmart_copy_to_host(ctx, dev_ptr, nbytes, dtype=np.uint32):
 class Engine:
     """One context: load -> build -> query.  Thin sugar over the functions above."""
 
-    def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0):
-        self.ctx = gsmart_create(device, rank, world, nccl_id, stream, max_result_rows)
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None):
+        self.ctx = gsmart_create(device, rank, world, nccl_id, stream, max_result_rows, local_comm)
 
     def load(self, s, p, o, n_entities, n_predicates, keep=None):
         gsmart_load_triples(self.ctx, s, p, o, n_entities, n_predicates)
