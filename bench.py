@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--universities", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"],
+                    help="N>1: replicas = every GPU serves its own copy of the batch (weak scaling); "
+                         "partitioned = one batch over a 1-D vertex-range partition with NCCL all-gathers")
     return ap.parse_args()
 
 
@@ -214,7 +217,14 @@ def main():
     s_h, p_h, o_h = s_d.cpu().numpy(), p_d.cpu().numpy(), o_d.cpu().numpy()
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
-    eng = G.Engine(local, stream=stream.cuda_stream)
+    partitioned = world > 1 and args.mode == "partitioned"
+    if partitioned:  # NCCL unique id from rank 0 over torch.distributed
+        obj = [G.gsmart_get_nccl_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        eng = G.Engine(local, rank=rank, world=world, nccl_id=obj[0], stream=stream.cuda_stream)
+    else:
+        eng = G.Engine(local, stream=stream.cuda_stream)
+    copies = 1 if partitioned else world  # batches processed per step across all ranks
     # ---- a1 build, timed separately (resident triples)
     G.gsmart_load_triples(eng.ctx, s_d, p_d, o_d, d.n_entities, d.n_predicates)
     bt = []
@@ -270,7 +280,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.barrier()
         ms = float(t.item())
-    value = world * sum(E) / (ms / 1000)
+    value = copies * sum(E) / (ms / 1000)
 
     # ---- profiled pass: the same queries one at a time (GSMART_PROFILE: per-kernel-class
     # CUDA events on the launching stream; sequential so no other stream shares the GPU)
@@ -320,15 +330,16 @@ def main():
         nbytes = 0
         for q in qs:
             rows = eng.query(q)
-            nbytes += rows.nbytes
-            if it == 0:
-                per_query[q.name]["rows"] = int(rows.shape[0])
+            if rows is not None:  # partitioned: rows on rank 0
+                nbytes += rows.nbytes
+                if it == 0:
+                    per_query[q.name]["rows"] = int(rows.shape[0])
         torch.cuda.synchronize()
         if it:
             e2e_times.append(time.perf_counter() - t0)
         d2h = nbytes
     e2e_s = statistics.mean(e2e_times)
-    e2e_value = world * sum(E) / e2e_s
+    e2e_value = copies * sum(E) / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.universities <= 200:
@@ -347,12 +358,13 @@ def main():
                "ms_per_batch": 1000 * cpu_s}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "universities": args.universities, "triples": int(len(s_h)),
                        "entities": d.n_entities, "queries": [q.name for q in qs],
                        "edges_per_step": int(sum(E)), "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": "replicas" if world > 1 else "single"},
+                       "parallelism": ("partitioned" if partitioned else "replicas") if world > 1 else "single"},
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(3 * 4 * len(s_h)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * e2e_s},

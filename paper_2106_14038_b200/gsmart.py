@@ -355,6 +355,7 @@ class Engine:
 
     def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None):
         self.ctx = gsmart_create(device, rank, world, nccl_id, stream, max_result_rows, local_comm)
+        self.rank, self.world = rank, world
 
     def load(self, s, p, o, n_entities, n_predicates, keep=None):
         gsmart_load_triples(self.ctx, s, p, o, n_entities, n_predicates)
@@ -419,8 +420,8 @@ class Plan:
         try:
             if flags & GSMART_COUNT_ONLY:
                 rows = gsmart_result_shape(r)[0]
-            elif flags & GSMART_KEEP_ON_DEVICE:
-                rows = None
+            elif flags & GSMART_KEEP_ON_DEVICE or self.eng.rank != 0:
+                rows = None  # with world > 1 the rows live on rank 0
             else:
                 rows = gsmart_result_rows(r)
             stats = gsmart_result_stats(r) if with_stats else None
