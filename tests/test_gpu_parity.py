@@ -159,6 +159,37 @@ def test_lubm_queries_vs_oracle(G, eng, U):
     assert eng.query(L2, flags=G.GSMART_COUNT_ONLY) == d.n_courses
 
 
+@pytest.mark.parametrize("scale", [0.01, 0.04])
+def test_watdiv_queries_vs_oracle(G, eng, scale):
+    """configs[2] shape (WatDiv-style L/S/F/C templates, 85 predicates) at
+    parity-test scale; batch execution."""
+    from synth import watdiv
+    d = watdiv.generate(scale)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = watdiv.queries(d)
+    exp = [ix.query(q) for q in qs]
+    for q, e, got in zip(qs, exp, eng.query_batch(qs)):
+        assert got.shape == e.shape and np.array_equal(got, e), q.name
+
+
+@pytest.mark.parametrize("n_pred", [200, 1000])
+def test_powerlaw_queries_vs_oracle(G, eng, n_pred):
+    """configs[4] shape (Zipf predicates, hub objects > HEAVY_ROW entries,
+    random-walk stars/chains/triangles); n_pred > 255 exercises uint16 labels."""
+    from synth import powerlaw
+    d = powerlaw.generate(400_000, 20_000, n_pred)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    assert G.gsmart_lspm_get(eng.ctx, G.GSMART_CSR)["pred_bytes"] == (1 if n_pred <= 255 else 2)
+    ix = OracleIndex(s, p, o)
+    for q in powerlaw.queries(d, 15, seed=n_pred):
+        e = ix.query(q)
+        got = eng.query(q)
+        assert got.shape == e.shape and np.array_equal(got, e), q
+
+
 def test_execute_batch_matches_single(G, eng):
     """gsmart_execute_batch (concurrent slots, > 16 plans => several waves) gives
     exactly the per-query results of the oracle."""
