@@ -460,3 +460,57 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
         for x, grp in list(reversed(plan["groups"]))[1:]:
             eval_group(x, grp)
     return cand, ok
+
+
+# --------------------------------------------------------------------------
+# Sampled parity at any size: all solutions whose binding of one variable lies
+# in a sample of values, computed on the triples within `hops` of the sample.
+# --------------------------------------------------------------------------
+
+
+def query_hops(q, var):
+    """Largest undirected distance (in pattern edges) from variable `var` to any
+    vertex of q: every triple of a solution touches a vertex within hops-1 of
+    var's binding, so the triples within `hops` of it contain the solution."""
+    adj = {i: set() for i in range(q.n_vertices)}
+    for a, _, b in q.edges:
+        adj[a].add(b)
+        adj[b].add(a)
+    dist, frontier = {var: 0}, [var]
+    while frontier:
+        nxt = []
+        for v in frontier:
+            if q.vertices[v] is not None and v != var:
+                continue  # constants do not extend a walk: their triples are reached from a variable
+            for w in adj[v]:
+                if w not in dist:
+                    dist[w] = dist[v] + 1
+                    nxt.append(w)
+        frontier = nxt
+    return max(dist.values())
+
+
+def local_triples(s, p, o, seeds, hops):
+    """Triples with an endpoint reachable from `seeds` in < hops steps (undirected)."""
+    s = np.asarray(s)
+    p = np.asarray(p)
+    o = np.asarray(o)
+    front = np.unique(np.asarray(seeds, dtype=s.dtype))
+    keep = np.zeros(len(s), dtype=bool)
+    for _ in range(hops):
+        m = np.isin(s, front) | np.isin(o, front)
+        new = m & ~keep
+        keep |= m
+        front = np.unique(np.concatenate([s[new], o[new]]))
+    return s[keep], p[keep], o[keep]
+
+
+def solutions_for_bindings(s, p, o, q, var, values):
+    """The exact solution rows of q whose binding of variable `var` is in
+    `values` (BGP definition restricted to those bindings), via the C oracle on
+    the local triple subset around `values`."""
+    from .coracle import oracle_bgp
+    ls, lp, lo = local_triples(s, p, o, values, query_hops(q, var))
+    rows = oracle_bgp(ls, lp, lo, q)
+    col = q.variables.index(var)
+    return rows[np.isin(rows[:, col], np.asarray(values))] if len(rows) else rows

@@ -190,6 +190,45 @@ def test_powerlaw_queries_vs_oracle(G, eng, n_pred):
         assert got.shape == e.shape and np.array_equal(got, e), q
 
 
+@pytest.mark.parametrize("U", [1000, 10000])
+def test_lubm_full_size_sampled_parity(G, U):
+    """BASELINE configs[3] at full size (LUBM-10k, ~1.3e9 triples, one B200) and
+    LUBM-1000, in bench.py's launch configuration (device-resident input,
+    gsmart_execute_batch): exact counts pinned by the generator's counters
+    (L2, L3, L4, L5, L6, Q14), and for every query the rows of sampled root
+    bindings equal the oracle's solutions for those bindings (computed on the
+    local triple subset around them)."""
+    import torch
+    from oracle import reference as R
+    d = lubm.generate(U, seed=lubm.SEED_LUBM10K, device="cuda")
+    qs = lubm.queries(d)
+    e = G.Engine(0)
+    try:
+        G.gsmart_load_triples(e.ctx, d.s, d.p, d.o, d.n_entities, d.n_predicates)
+        G.gsmart_build_lspm(e.ctx)
+        counts = e.query_batch(qs, flags=G.GSMART_COUNT_ONLY)
+        for q, c in zip(qs, counts):
+            if q.name in d.counts:
+                assert c == d.counts[q.name], (q.name, c, d.counts[q.name])
+        s, p, o = d.s.cpu().numpy(), d.p.cpu().numpy(), d.o.cpu().numpy()
+        del d
+        torch.cuda.empty_cache()
+        rng = np.random.default_rng(U)
+        for q, c in zip(qs, counts):
+            if c > 50_000_000:
+                continue
+            rows = e.query(q)
+            assert len(rows) == c
+            var = q.variables[0]
+            picked = rows[rng.integers(0, len(rows), 20), 0] if len(rows) else np.zeros(0, np.uint32)
+            vals = np.unique(np.concatenate([picked, rng.integers(0, len(s), 5).astype(np.uint32) % 1000003]))
+            exp = R.solutions_for_bindings(s, p, o, q, var, vals)
+            got = rows[np.isin(rows[:, 0], vals)]
+            assert got.shape == exp.shape and np.array_equal(got, exp), q.name
+    finally:
+        e.close()
+
+
 def test_execute_batch_matches_single(G, eng):
     """gsmart_execute_batch (concurrent slots, > 16 plans => several waves) gives
     exactly the per-query results of the oracle."""

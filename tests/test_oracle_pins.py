@@ -236,6 +236,30 @@ def test_star_and_acyclic_counts_lubm1():
     assert len(oracle_bgp(s, p, o, qs["L2"])) == d.n_courses
 
 
+def test_lubm_generator_counters_pin_counts():
+    """The LUBM generator's counters (used as expected counts at full size,
+    where enumeration by the oracle is too slow) equal the oracle's counts."""
+    d = lubm.generate(2)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    for q in lubm.queries(d):
+        if q.name in d.counts:
+            assert len(oracle_bgp(s, p, o, q)) == d.counts[q.name], q.name
+
+
+def test_sampled_bindings_equal_full_oracle():
+    """solutions_for_bindings (local triple subset around sampled bindings) is
+    exactly the full answer restricted to those bindings."""
+    d = lubm.generate(3)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    for q in lubm.queries(d):
+        full = oracle_bgp(s, p, o, q)
+        vals = np.unique(np.concatenate([full[:30, 0] if len(full) else np.zeros(0, np.uint32),
+                                         np.array([5, 17, 1234], np.uint32)]))
+        got = R.solutions_for_bindings(s, p, o, q, q.variables[0], vals)
+        exp = full[np.isin(full[:, 0], vals)] if len(full) else full
+        assert np.array_equal(got, exp), q.name
+
+
 def test_zero_edge_and_const_only_queries():
     s, p, o = fixtures.fig1_triples()
     assert R.brute_force(s, p, o, 8, Query((), ())) == [()]
