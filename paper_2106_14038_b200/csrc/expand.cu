@@ -246,7 +246,13 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
         const ClosingDev cl = a.cl[q];
         uint32_t tgt = c;
         if (!cl.self) tgt = stgt ? s_tgt[(n - nlo) * TGTC + q] : ancestor(a.tab, a.k - 1, n, cl.other_level);
-        keep = cl.dir ? has_entry(f1, c, cl.label, tgt) : has_entry(f0, c, cl.label, tgt);
+        // (c, l, tgt) in the child's row of format dir  <=>  (tgt, l, c) in tgt's row of the
+        // other format: binary-search the shorter row (a hub on one side costs log of the other)
+        const Fmt<PT>& fc = cl.dir ? f1 : f0;
+        const Fmt<PT>& fo = cl.dir ? f0 : f1;
+        const uint32_t lc = __ldg(fc.rp + c + 1) - __ldg(fc.rp + c);
+        const uint32_t lt = __ldg(fo.rp + tgt + 1) - __ldg(fo.rp + tgt);
+        keep = lc <= lt ? has_entry(fc, c, cl.label, tgt) : has_entry(fo, tgt, cl.label, c);
         n_close++;
       }
       node[j] = n;
