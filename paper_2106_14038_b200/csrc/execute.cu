@@ -51,6 +51,7 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
   dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
+  dfree(st, s.frows);
   cudaStreamSynchronize(st);
   if (s.h_pin) cudaFreeHost(s.h_pin);
   if (s.ev) cudaEventDestroy(s.ev);
@@ -261,6 +262,22 @@ struct Exec {
     std::vector<const GroupEdge*> by[2];
     for (auto& e : g.edges) by[e.dir == OUT ? 0 : 1].push_back(&e);
     size_t done[2] = {0, 0};
+    // row-list path: compact the center's candidate rows of this rank once per group
+    const bool rowlist = (ctx->filter_variant & 4) != 0;
+    unsigned long long* d_nrows = sl.d_ctr + 56;
+    if (rowlist) {
+      if (sl.frows_cap < (uint64_t)W * 32) {
+        dfree(sl.st, sl.frows);
+        TRY(dalloc(ctx, &sl.frows, (uint64_t)W * 32, sl.st));
+        sl.frows_cap = (uint64_t)W * 32;
+      }
+      prof.begin(K_COMPACT);
+      CU(cudaMemsetAsync(d_nrows, 0, 8, sl.st));
+      CU(launch_bitmap_compact_lb(cand(g.center) + wlo, whi > wlo ? whi - wlo : 0, sl.frows, sl.frows_cap, d_nrows,
+                                  sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
+      launches[K_COMPACT]++;
+      prof.end();
+    }
     while (done[0] < by[0].size() || done[1] < by[1].size()) {
       FilterArgs a;
       memset(&a, 0, sizeof a);
@@ -292,6 +309,11 @@ struct Exec {
       a.heavy_count = sl.heavy_cnt;
       a.ctr = sl.d_ctr;
       a.variant = ctx->filter_variant;
+      a.claim = next_lb(sl).counter;  // fresh zeroed counter, no reset launch
+      if (rowlist) {
+        a.rows = sl.frows;
+        a.d_nrows = d_nrows;
+      }
       prof.begin(K_FILTER);
       CU(launch_group_filter(a, ctx->pred_bytes, ctx->sm_count, sl.st, &launches[K_FILTER]));
       prof.end();

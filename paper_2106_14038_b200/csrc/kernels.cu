@@ -351,6 +351,7 @@ struct FilterArgsT {
   unsigned long long* ctr;
   int variant;
   uint32_t word_lo;
+  uint32_t* claim;
 };
 
 template <typename PT>
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   uint32_t ch = c_begin + warp;
   if (dyn) {
     uint32_t c0 = 0;
-    if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
+    if (lane == 0) c0 = atomicAdd(a.claim, 1u);
     ch = c_begin + __shfl_sync(GSM_FULL, c0, 0);
   }
   uint32_t nxt = 0;
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     uint32_t cn = ch + nwarps;
     if (dyn) {
       uint32_t c0 = 0;
-      if (lane == 0) c0 = atomicAdd(a.heavy_count + 2, 1u);
+      if (lane == 0) c0 = atomicAdd(a.claim, 1u);
       cn = c_begin + __shfl_sync(GSM_FULL, c0, 0);
     }
     if (cn < n_chunks) {
@@ -583,6 +584,37 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     clear_failed(a.cand, row, has && !ok, lane);
   }
   // one atomic per warp per counter
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
+    n_scanned += __shfl_down_sync(GSM_FULL, n_scanned, o);
+    n_matched += __shfl_down_sync(GSM_FULL, n_matched, o);
+  }
+  if (lane == 0) {
+    if (n_rows) atomicAdd(a.ctr + C_FILTER_ROWS, n_rows);
+    if (n_scanned) atomicAdd(a.ctr + C_FILTER_SCANNED, n_scanned);
+    if (n_matched) atomicAdd(a.ctr + C_FILTER_MATCHED, (unsigned long long)n_matched);
+  }
+}
+
+// Candidate rows given as a compacted id list (k_bitmap_compact_lb): every warp
+// takes batches of 32 consecutive ids, one row per lane, so dense and sparse
+// candidate sets alike spread over all warps of the GPU (no per-chunk serial
+// batches), then failed rows are cleared in the center's bitmap.
+template <typename PT>
+__global__ void __launch_bounds__(256) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
+                                                          const unsigned long long* __restrict__ d_nrows) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t n = *d_nrows;
+  unsigned long long n_rows = 0, n_scanned = 0;
+  uint32_t n_matched = 0;
+  for (uint64_t base = (uint64_t)warp * 32; base < n; base += (uint64_t)nwarps * 32) {
+    const bool has = base + lane < n;
+    const uint32_t row = has ? __ldg(rows + base + lane) : 0u;
+    const bool ok = eval_rows(a, row, has, lane, n_rows, n_scanned, n_matched);
+    clear_failed(a.cand, row, has && !ok, lane);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
@@ -644,7 +676,6 @@ __global__ void k_filter_finalize(FilterArgsT<PT> a) {
   if (threadIdx.x == 0) {
     a.heavy_count[0] = 0;
     a.heavy_count[1] = 0;
-    a.heavy_count[2] = 0;  // dynamic chunk counter
   }
 }
 
@@ -665,23 +696,27 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
   }
   t.cand = a.cand; t.n_words = a.n_words;
   t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
-  t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant; t.word_lo = a.word_lo;
+  t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant; t.word_lo = a.word_lo; t.claim = a.claim;
   return t;
 }
 
 template <typename PT>
 static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_t st, int* launches) {
   FilterArgsT<PT> t = to_t<PT>(a);
-  // 8 warps per CTA; enough CTAs for ~16 resident warps/SM-worth of words, grid-stride beyond
-  uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;  // one 32-word chunk per warp
-  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 6);  // one wave
-  k_group_filter<PT><<<g, 256, 0, st>>>(t);
+  if (a.rows) {  // candidate rows already compacted: perfectly balanced batches of 32 rows
+    k_group_filter_rows<PT><<<(unsigned)sm_count * 8, 256, 0, st>>>(t, a.rows, a.d_nrows);
+  } else {
+    // 8 warps per CTA; one 32-word chunk per warp, persistent (one wave)
+    uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;
+    unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 6);
+    k_group_filter<PT><<<g, 256, 0, st>>>(t);
+  }
   if (launches) *launches += 1;
   if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
     k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
     if (launches) *launches += 1;
   }
-  if (a.heavy || (a.variant & 2)) {  // clears failed heavy rows, resets counters
+  if (a.heavy) {  // clears failed heavy rows, resets the heavy counters
     k_filter_finalize<PT><<<1, 1024, 0, st>>>(t);
     if (launches) *launches += 1;
   }

@@ -86,6 +86,9 @@ struct FilterArgs {
   int heavy;                // launch the heavy-row kernels
   int variant;              // bit0: SIMD label ranges (uint8 labels); bit1: dynamic chunk claiming
   uint32_t word_lo;         // first bitmap word of this rank's range (multiple of 32); n_words = end
+  uint32_t* claim;          // zeroed chunk counter of this launch (dynamic claiming)
+  const uint32_t* rows;     // non-null: the center's candidate rows, compacted (row-list path)
+  const unsigned long long* d_nrows;  // their count (device)
 };
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
                               uint32_t ones_mask, cudaStream_t st);

@@ -66,6 +66,8 @@ struct Slot {
   unsigned long long* h_pin = nullptr; // 256 pinned slots
   uint32_t *heavy_rows = nullptr, *heavy_chunks = nullptr, *heavy_sat = nullptr, *heavy_cnt = nullptr;
   uint64_t heavy_gen = ~0ull;          // LSpM generation the heavy buffers were sized for
+  uint32_t* frows = nullptr;           // group filter: compacted candidate rows of the center
+  uint64_t frows_cap = 0;
 };
 
 }  // namespace gsm
@@ -109,7 +111,7 @@ struct gsmart_ctx {
   int pred_bytes = 1;
   gsm::Lspm f[2];
   uint64_t lspm_gen = 0;
-  int filter_variant = 2;               // see FilterArgs::variant (GSMART_FILTER_VARIANT)
+  int filter_variant = 6;               // FilterArgs::variant bits + 4: row-list path (GSMART_FILTER_VARIANT)
   unsigned long long* d_ctr = nullptr;  // load/build scratch
   unsigned long long* h_pin = nullptr;
   ncclComm_t comm = nullptr;     // world > 1 with NCCL
