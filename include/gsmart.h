@@ -72,7 +72,9 @@ typedef enum {
 #define GSMART_COUNT_ONLY 1u      /* stop after pruning: n_rows only, no row enumeration */
 #define GSMART_KEEP_ON_DEVICE 2u  /* do not copy rows to host (use gsmart_result_rows_device) */
 #define GSMART_NO_REFINE 4u       /* skip the backward group re-evaluation */
-#define GSMART_PROFILE 8u         /* per-kernel CUDA-event timing into gsmart_stats */
+#define GSMART_PROFILE 8u         /* per-kernel CUDA-event timing into gsmart_stats (no graph replay) */
+#define GSMART_KEEP_CANDIDATES 16u /* keep the candidate bitmaps for gsmart_result_candidates */
+#define GSMART_NO_GRAPH 32u       /* launch kernels one by one instead of replaying the plan's CUDA graph */
 
 typedef struct gsmart_ctx gsmart_ctx;
 typedef struct gsmart_plan_s gsmart_plan_t;
@@ -203,7 +205,8 @@ gsmart_status gsmart_result_rows(gsmart_result* r, const uint32_t** rows);
 gsmart_status gsmart_result_rows_device(const gsmart_result* r, const uint32_t** rows_dev);
 /* Candidate bitmap of query vertex `vertex` after the filter schedule:
  * device pointer to ceil(n_entities/32) uint32 words, bit (i & 31) of word
- * (i >> 5) set iff entity i is a candidate. */
+ * (i >> 5) set iff entity i is a candidate.  Only when the execute was given
+ * GSMART_KEEP_CANDIDATES (else GSMART_E_INVALID_ARG). */
 gsmart_status gsmart_result_candidates(const gsmart_result* r, uint32_t vertex,
                                        const uint32_t** bits_dev, uint32_t* n_words);
 /* Trie level k (0 = root level) after pruning: variable vertex, node count and

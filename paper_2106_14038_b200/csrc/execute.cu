@@ -34,11 +34,12 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   TRY(dalloc(ctx, &s.d_ovf, 1, s.st));
   TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
   TRY(dalloc(ctx, &s.heavy_cnt, 4, s.st));
+  TRY(dalloc(ctx, &s.d_epoch, 1, s.st));
   CU(cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st));
   CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
   CU(cudaMemsetAsync(s.heavy_cnt, 0, 16, s.st));
   CU(cudaMallocHost(&s.h_pin, 256 * sizeof(unsigned long long)));
-  s.epoch = 0;
+  s.epoch_next = 1;
   return GSMART_OK;
 }
 
@@ -51,7 +52,9 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
   dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
-  dfree(st, s.frows);
+  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch);
+  for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second.exec);
+  s.graphs.clear();
   cudaStreamSynchronize(st);
   if (s.h_pin) cudaFreeHost(s.h_pin);
   if (s.ev) cudaEventDestroy(s.ev);
@@ -85,20 +88,36 @@ static gsmart_status slot_heavy(gsmart_ctx* ctx, Slot& s) {
   CU(cudaMemsetAsync(s.heavy_sat, 0, rows * 4, s.st));
   CU(cudaMemsetAsync(s.heavy_cnt, 0, 8, s.st));
   s.heavy_gen = ctx->lspm_gen;
+  s.ws_gen++;
   return GSMART_OK;
 }
 
-// a fresh (epoch, zeroed counter) pair for one look-back launch
-static LBArgs next_lb(Slot& s) {
-  if (++s.epoch >= LB_EPOCHS) {
-    cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st);
-    cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st);
-    s.epoch = 1;
+// Look-back epochs.  An execute is one launch sequence: its look-back launches
+// take epochs base + 0, 1, 2, ... where base lives in device memory (set by a
+// one-thread kernel), so a captured phase-1 graph replays with fresh epochs.
+constexpr uint32_t SEQ_MAX = 8192;  // epochs one execute may use
+
+static gsmart_status begin_seq(gsmart_ctx* ctx, Slot& s) {
+  if (s.epoch_next + SEQ_MAX >= LB_EPOCHS) {  // wrap: every status word / counter back to "unused"
+    CU(cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st));
+    CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
+    s.epoch_next = 1;
   }
+  s.seq_base = s.epoch_next;
+  s.seq_off = 0;
+  CU(launch_set_u32(s.d_epoch, s.seq_base, s.st));
+  return GSMART_OK;
+}
+
+static void end_seq(Slot& s) { s.epoch_next = s.seq_base + std::min(s.seq_off, SEQ_MAX); }
+
+// the next look-back launch of the current sequence
+static LBArgs next_lb(Slot& s) {
   LBArgs a;
   a.status = s.lb_status;
-  a.counter = s.lb_counters + s.epoch;
-  a.epoch = s.epoch;
+  a.counters = s.lb_counters;
+  a.d_epoch = s.d_epoch;
+  a.off = s.seq_off < SEQ_MAX ? s.seq_off++ : SEQ_MAX - 1;
   a.cap_tiles = LB_CAP_TILES;
   return a;
 }
@@ -118,6 +137,19 @@ static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t n
   TRY(dalloc(ctx, &b.newidx, cap, s.st));
   TRY(dalloc(ctx, &b.alive, cap, s.st));
   b.cap = cap;
+  s.ws_gen++;
+  return GSMART_OK;
+}
+
+// grow a plain workspace buffer (moves it: cached graphs of this slot go stale)
+template <typename T>
+static gsmart_status slot_buf(gsmart_ctx* ctx, Slot& s, T** p, uint64_t* cap, uint64_t need) {
+  if (*p && *cap >= need) return GSMART_OK;
+  dfree(s.st, *p);
+  *p = nullptr;
+  TRY(dalloc(ctx, p, need, s.st));
+  *cap = need;
+  s.ws_gen++;
   return GSMART_OK;
 }
 
@@ -176,6 +208,8 @@ struct Exec {
   int launches[GSMART_NKERNELS] = {0};
   uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
   int attempts = 0;
+  bool seq_open = false;        // a look-back launch sequence was started (end it in finalize)
+  bool graph_replayed = false;  // phase 1 came from the plan's cached CUDA graph
   uint32_t wlo = 0, whi = 0, slice = 0;  // this rank's bitmap words (1-D vertex-range partition)
   bool identity = false;                 // trie order == column order: rows come out sorted
   std::vector<uint64_t> F;
@@ -186,7 +220,9 @@ struct Exec {
     t0 = std::chrono::steady_clock::now();
   }
 
-  uint32_t* cand(uint32_t vertex) { return R->d_cand + (uint64_t)slot[vertex] * Wpad; }
+  // candidate bitmaps live in the slot (stable addresses for graph replay);
+  // GSMART_KEEP_CANDIDATES copies them into the result at the end
+  uint32_t* cand(uint32_t vertex) { return sl.cand + (uint64_t)slot[vertex] * Wpad; }
 
   gsmart_status alloc_result(void** p, uint64_t bytes) {
     TRY(dalloc(ctx, (char**)p, bytes, sl.st));
@@ -205,7 +241,7 @@ struct Exec {
       if (g.s >= N || g.o >= N) *empty = true;
     if (*empty) {  // a constant outside the data: every candidate set is empty (R12)
       if (!plan->vars.empty())
-        CU(cudaMemsetAsync(R->d_cand, 0, (size_t)Wpad * plan->vars.size() * 4, sl.st));
+        CU(cudaMemsetAsync(sl.cand, 0, (size_t)Wpad * plan->vars.size() * 4, sl.st));
       return GSMART_OK;
     }
     std::vector<std::vector<const Seed*>> by_var(plan->n_vertices);
@@ -215,7 +251,7 @@ struct Exec {
       if (by_var[v].empty()) ones |= 1u << slot[v];
     if (!plan->vars.empty()) {
       prof.begin(K_BITMAP);
-      CU(launch_init_cands(R->d_cand, (uint32_t)plan->vars.size(), Wpad, N, ones, sl.st));
+      CU(launch_init_cands(sl.cand, (uint32_t)plan->vars.size(), Wpad, N, ones, sl.st));
       launches[K_BITMAP]++;
       prof.end();
     }
@@ -249,7 +285,7 @@ struct Exec {
     }
     if (!plan->guards.empty() && !plan->vars.empty()) {
       prof.begin(K_BITMAP);
-      CU(launch_zero_if_flag(R->d_cand, (uint64_t)Wpad * plan->vars.size(), flag, sl.st));
+      CU(launch_zero_if_flag(sl.cand, (uint64_t)Wpad * plan->vars.size(), flag, sl.st));
       launches[K_BITMAP]++;
       prof.end();
     }
@@ -265,12 +301,7 @@ struct Exec {
     // row-list path: compact the center's candidate rows of this rank once per group
     const bool rowlist = (ctx->filter_variant & 4) != 0;
     unsigned long long* d_nrows = sl.d_ctr + 56;
-    if (rowlist) {
-      if (sl.frows_cap < (uint64_t)W * 32) {
-        dfree(sl.st, sl.frows);
-        TRY(dalloc(ctx, &sl.frows, (uint64_t)W * 32, sl.st));
-        sl.frows_cap = (uint64_t)W * 32;
-      }
+    if (rowlist) {  // sl.frows sized in ensure_workspace()
       prof.begin(K_COMPACT);
       CU(cudaMemsetAsync(d_nrows, 0, 8, sl.st));
       CU(launch_bitmap_compact_lb(cand(g.center) + wlo, whi > wlo ? whi - wlo : 0, sl.frows, sl.frows_cap, d_nrows,
@@ -309,7 +340,7 @@ struct Exec {
       a.heavy_count = sl.heavy_cnt;
       a.ctr = sl.d_ctr;
       a.variant = ctx->filter_variant;
-      a.claim = next_lb(sl).counter;  // fresh zeroed counter, no reset launch
+      a.claim = next_lb(sl);  // its counter() is fresh and zeroed: no reset launch
       if (rowlist) {
         a.rows = sl.frows;
         a.d_nrows = d_nrows;
@@ -399,8 +430,91 @@ struct Exec {
     }
     CU(cudaMemcpyAsync(dsz + 127, sl.d_ovf, 4, cudaMemcpyDeviceToDevice, sl.st));
     CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
+    return GSMART_OK;
+  }
+
+  gsmart_status relaunch_expansion() {
+    TRY(launch_expansion());
     CU(cudaEventRecord(sl.ev, sl.st));
     state = S_EXPANDING;
+    return GSMART_OK;
+  }
+
+  // every workspace buffer phase 1 touches, sized before any launch (a graph
+  // replay must see the same addresses; growth bumps sl.ws_gen)
+  gsmart_status ensure_workspace() {
+    const uint64_t nvar = plan->vars.size();
+    TRY(slot_heavy(ctx, sl));
+    TRY(slot_buf(ctx, sl, &sl.cand, &sl.cand_words, std::max<uint64_t>((uint64_t)Wpad * nvar, 1)));
+    if (ctx->filter_variant & 4) TRY(slot_buf(ctx, sl, &sl.frows, &sl.frows_cap, (uint64_t)W * 32));
+    for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
+    for (uint32_t k = 1; k < L; k++)
+      if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
+    return GSMART_OK;
+  }
+
+  // phase 1 = seeds + grouped evaluation + expansion: pure device work on
+  // stable workspace addresses, launched directly or replayed from a graph
+  gsmart_status phase1_kernels() {
+    CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
+    bool empty = false;
+    TRY(seeds_and_guards(&empty));
+    for (auto& g : plan->groups) TRY(eval_group(g));
+    if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
+      for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i]));
+    return launch_expansion();
+  }
+
+  gsmart_status run_phase1() {
+    const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && ctx->world == 1;
+    if (!graphable) return phase1_kernels();
+    const uint32_t key_flags = flags & GSMART_NO_REFINE;
+    auto it = sl.graphs.find(plan->uid);
+    if (it != sl.graphs.end() && it->second.ws_gen == sl.ws_gen && it->second.lspm_gen == ctx->lspm_gen &&
+        it->second.flags == key_flags) {
+      CU(cudaGraphLaunch(it->second.exec, sl.st));
+      sl.seq_off = it->second.n_lb;
+      graph_replayed = true;
+      for (int i = 0; i < GSMART_NKERNELS; i++) launches[i] += it->second.launches[i];
+      filter_main += it->second.filter_main;
+      return GSMART_OK;
+    }
+    if (it != sl.graphs.end()) {
+      cudaGraphExecDestroy(it->second.exec);
+      sl.graphs.erase(it);
+    }
+    // capture this plan's phase 1 once, then replay it (launch offsets relative to the epoch base)
+    const uint32_t off0 = sl.seq_off;
+    const std::vector<int> l0(launches, launches + GSMART_NKERNELS);
+    const uint64_t fm0 = filter_main;
+    CU(cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal));
+    gsmart_status s = phase1_kernels();
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(sl.st, &graph);
+    if (s != GSMART_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture", __LINE__);
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate", __LINE__);
+    Slot::GraphEntry ge;
+    ge.exec = exec;
+    ge.ws_gen = sl.ws_gen;
+    ge.lspm_gen = ctx->lspm_gen;
+    ge.flags = key_flags;
+    ge.n_lb = sl.seq_off - off0;
+    ge.launches.resize(GSMART_NKERNELS);
+    for (int i = 0; i < GSMART_NKERNELS; i++) ge.launches[i] = launches[i] - l0[i];
+    ge.filter_main = filter_main - fm0;
+    if (sl.graphs.size() >= 256) {  // bounded cache
+      for (auto& kv : sl.graphs) cudaGraphExecDestroy(kv.second.exec);
+      sl.graphs.clear();
+    }
+    sl.graphs[plan->uid] = ge;
+    CU(cudaGraphLaunch(exec, sl.st));
     return GSMART_OK;
   }
 
@@ -431,11 +545,27 @@ struct Exec {
       fa[d].col = ctx->f[d].col;
       fa[d].pred = ctx->f[d].pred;
     }
-    TRY(slot_heavy(ctx, sl));
-    CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
-    if (nvar) TRY(alloc_result((void**)&R->d_cand, (uint64_t)Wpad * nvar * 4));
+    for (uint32_t k = 1; k < L; k++)
+      if (plan->levels[k].closing.size() > (size_t)MAXC)
+        FAIL(GSMART_E_UNSUPPORTED, "more than 16 closing edges on one level");
+    TRY(ensure_workspace());
+    TRY(begin_seq(ctx, sl));
+    seq_open = true;
+    F.assign(L, 0);
+    R->stats.n_levels = L;
 
     bool empty = false;
+    for (auto& sd : plan->seeds)
+      if (sd.cid >= N) empty = true;
+    for (auto& g : plan->guards)
+      if (g.s >= N || g.o >= N) empty = true;
+    if (nvar > 0 && !empty) {  // the common path: all device work of phase 1, then one event
+      TRY(run_phase1());
+      CU(cudaEventRecord(sl.ev, sl.st));
+      state = S_EXPANDING;
+      return GSMART_OK;
+    }
+    CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
     TRY(seeds_and_guards(&empty));
     if (nvar == 0) {  // only guards (or nothing): one empty row iff all hold
       uint64_t rows = 0;
@@ -452,32 +582,13 @@ struct Exec {
       state = S_DONE;
       return GSMART_OK;
     }
-    if (empty) {
-      R->n_rows = 0;
-      R->host_valid = true;
-      R->stats.n_levels = L;
-      for (auto& Lv : plan->levels) R->levels.push_back({Lv.var, 0, nullptr, nullptr});
-      state = S_DONE;
-      return GSMART_OK;
-    }
-    // forward groups, then backward re-evaluation (R-refine)
-    for (auto& g : plan->groups) TRY(eval_group(g));
-    if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
-      for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i]));
-    // expansion workspace
-    for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
-    for (uint32_t k = 1; k < L; k++) {
-      if (plan->levels[k].tree_edge < 0 && sl.list_cap[k] < (uint64_t)W * 32) {
-        dfree(sl.st, sl.list[k]);
-        TRY(dalloc(ctx, &sl.list[k], (uint64_t)W * 32, sl.st));
-        sl.list_cap[k] = (uint64_t)W * 32;
-      }
-      if (plan->levels[k].closing.size() > (size_t)MAXC)
-        FAIL(GSMART_E_UNSUPPORTED, "more than 16 closing edges on one level");
-    }
-    F.assign(L, 0);
-    R->stats.n_levels = L;
-    return launch_expansion();
+    // a constant outside the data: empty result, all candidate sets empty
+    R->n_rows = 0;
+    R->host_valid = true;
+    for (auto& Lv : plan->levels) R->levels.push_back({Lv.var, 0, nullptr, nullptr});
+    TRY(keep_candidates());
+    state = S_DONE;
+    return GSMART_OK;
   }
 
   // called once sl.ev completed
@@ -495,16 +606,26 @@ struct Exec {
       if (F[k] > sl.lv[k].cap) {  // later levels are invalid: grow and re-run the expansion
         TRY(slot_level(ctx, sl, k, F[k]));
         if (++attempts > 2 * (int)L + 2) FAIL(GSMART_E_CUDA, "expansion capacity did not converge");
-        return launch_expansion();
+        return relaunch_expansion();
       }
     }
     for (uint32_t k = 0; k < L; k++) R->stats.level_nodes[k] = F[k];
     return phase2();
   }
 
+  // GSMART_KEEP_CANDIDATES: the result gets its own copy of the slot's bitmaps
+  gsmart_status keep_candidates() {
+    if (!(flags & GSMART_KEEP_CANDIDATES) || plan->vars.empty()) return GSMART_OK;
+    const uint64_t bytes = (uint64_t)Wpad * plan->vars.size() * 4;
+    TRY(alloc_result((void**)&R->d_cand, bytes));
+    CU(cudaMemcpyAsync(R->d_cand, sl.cand, bytes, cudaMemcpyDeviceToDevice, sl.st));
+    return GSMART_OK;
+  }
+
   // ---- a8 prune + compaction, a9 rows + sort (async)
   gsmart_status phase2() {
     state = S_PHASE2;
+    TRY(keep_candidates());
     const uint64_t n_rows = F[L - 1];
     unsigned long long* dsz = sl.d_sz;
     R->levels.clear();
@@ -602,6 +723,10 @@ struct Exec {
 
   gsmart_status finalize() {
     prof.flush();
+    if (seq_open) {
+      end_seq(sl);
+      seq_open = false;
+    }
     if (state == S_PHASE2 && R->n_rows) {
       for (uint32_t k = 0; k < L && k < (uint32_t)R->levels.size(); k++) {
         R->levels[k].n = sl.h_pin[128 + k];
@@ -681,7 +806,11 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
       ex[i] = std::make_unique<Exec>(ctx, *ctx->slots[i], p, flags, R);
     }
     std::vector<gsmart_status> st(m, GSMART_OK);
+    static const bool trace = getenv("GSMART_TRACE") != nullptr;
+    const auto tb = std::chrono::steady_clock::now();
+    auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb).count(); };
     for (uint32_t i = 0; i < m; i++) st[i] = ex[i]->start();
+    if (trace) fprintf(stderr, "[gsmart] %u plans: phase-1 launched at %.1f us\n", m, us());
     // wait on each expansion readback; re-launch on overflow; then phase 2
     bool pending = true;
     while (pending) {
@@ -693,17 +822,22 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
           st[i] = cuda_fail(ctx, e, "expansion event", __LINE__);
           continue;
         }
+        if (trace) fprintf(stderr, "[gsmart]   plan %u expansion done at %.1f us\n", i, us());
         st[i] = ex[i]->after_expand();
+        if (trace) fprintf(stderr, "[gsmart]   plan %u phase-2 launched at %.1f us\n", i, us());
         if (st[i] == GSMART_OK && ex[i]->state == Exec::S_EXPANDING) pending = true;
       }
     }
     for (uint32_t i = 0; i < m; i++) {
       cudaError_t e = cudaStreamSynchronize(ex[i]->sl.st);
+      if (trace) fprintf(stderr, "[gsmart]   plan %u drained at %.1f us\n", i, us());
       if (e != cudaSuccess && st[i] == GSMART_OK) st[i] = cuda_fail(ctx, e, "execute sync", __LINE__);
       if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
       else ex[i]->prof.flush();
+      if (trace) fprintf(stderr, "[gsmart]   plan %u finalized at %.1f us\n", i, us());
     }
     for (uint32_t i = 0; i < m; i++) {
+      if (ex[i]->seq_open) end_seq(ex[i]->sl);  // epochs of a failed run are never reused
       ex[i].reset();  // frees stream-ordered scratch
       if (st[i] == GSMART_OK || (st[i] == GSMART_E_RESULT_OVERFLOW && n == 1)) {
         out[base + i] = res[i].release();

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __re
   // warp wib of a tile owns words [tile*2048 + wib*256, +256) in 8 coalesced rounds of
   // 32 words; ids are emitted warp-cooperatively (lane b writes bit b of each word)
   while (true) {
-    const uint32_t tile = lb_claim(lb.counter, &s_tile);
+    const uint32_t tile = lb_claim(lb.counter(), &s_tile);
     if (tile >= ntiles) break;
     const uint64_t wbase = (uint64_t)tile * BC_TILE + wib * (BC_W * 32);
     uint32_t w[BC_W], off[BC_W];
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __re
     unsigned long long tot;
     const unsigned long long wex =
         block_exclusive_scan<unsigned long long>(lane == 0 ? (unsigned long long)run : 0ull, s_red, &tot);
-    const uint64_t pref = lb_prefix(lb.status, lb.epoch, tile, tot, &s_pref);
+    const uint64_t pref = lb_prefix(lb.status, lb.epoch(), tile, tot, &s_pref);
     const uint64_t base_pos = pref + __shfl_sync(GSM_FULL, wex, 0);
 #pragma unroll
     for (int r = 0; r < BC_W; r++) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
   Fmt<PT> f = fmt_of<PT>(a.f[a.dir & 1]);
   const uint32_t list_len = a.tree ? 0u : (uint32_t)*a.d_list_len;
   while (true) {
-    const uint32_t tile = lb_claim(a.lb.counter, &s_tile);
+    const uint32_t tile = lb_claim(a.lb.counter(), &s_tile);
     if (tile >= ntiles) break;
     const uint64_t base = (uint64_t)tile * SS_TILE + threadIdx.x * SS_I;
     uint32_t len[SS_I];
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
     }
     unsigned long long tot;
     unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, s_red, &tot);
-    const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch, tile, tot, &s_pref);
+    const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch(), tile, tot, &s_pref);
     uint64_t run = pref + ex;
 #pragma unroll
     for (int j = 0; j < SS_I; j++) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
   const uint32_t F1 = (uint32_t)F + 1;
   unsigned long long n_exam = 0, n_close = 0;
   while (true) {
-    const uint32_t tile = lb_claim(a.lb.counter, &s_tile);
+    const uint32_t tile = lb_claim(a.lb.counter(), &s_tile);
     if (tile >= ntiles) break;
     const uint32_t base = tile * EX_TILE;
     const uint32_t last = (uint32_t)min((uint64_t)base + EX_TILE, T) - 1;
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
     }
     unsigned long long tot;
     unsigned long long ex = block_exclusive_scan<unsigned long long>((unsigned long long)__popc(keepm), s_red, &tot);
-    const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch, tile, tot, &s_pref);
+    const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch(), tile, tot, &s_pref);
     uint64_t pos = pref + ex;
 #pragma unroll
     for (int j = 0; j < EX_I; j++) {
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
   const uint64_t n = *d_n;
   const uint32_t ntiles = (uint32_t)((n + CA_TILE - 1) / CA_TILE);
   while (true) {
-    const uint32_t tile = lb_claim(lb.counter, &s_tile);
+    const uint32_t tile = lb_claim(lb.counter(), &s_tile);
     if (tile >= ntiles) break;
     const uint64_t base = (uint64_t)tile * CA_TILE + threadIdx.x * CA_I;
     uint32_t fl = 0;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
       if (base + j < n && (!alive || alive[base + j])) fl |= 1u << j;
     unsigned long long tot;
     unsigned long long ex = block_exclusive_scan<unsigned long long>((unsigned long long)__popc(fl), s_red, &tot);
-    const uint64_t pref = lb_prefix(lb.status, lb.epoch, tile, tot, &s_pref);
+    const uint64_t pref = lb_prefix(lb.status, lb.epoch(), tile, tot, &s_pref);
     uint64_t q = pref + ex;
 #pragma unroll
     for (int j = 0; j < CA_I; j++) {

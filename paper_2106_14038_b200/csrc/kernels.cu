@@ -190,6 +190,13 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // =====================================================================================
 // bitmaps
 // =====================================================================================
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
+  k_set_u32<<<1, 1, 0, st>>>(p, v);
+  return cudaGetLastError();
+}
+
 // all-ones over bits [0, n_bits), zero beyond (padding words included)
 __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
@@ -256,15 +263,10 @@ cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag,
 template <typename PT>
 __global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __restrict__ bits,
                                unsigned long long* ctr) {
-  __shared__ uint32_t s_lo, s_hi;
-  if (threadIdx.x == 0) {
-    uint32_t lo, hi;
-    label_range(f, c, l, lo, hi);
-    s_lo = lo; s_hi = hi;
-    if (blockIdx.x == 0) atomicAdd(ctr + C_SEED, (unsigned long long)(hi - lo));
-  }
-  __syncthreads();
-  const uint32_t lo = s_lo, hi = s_hi;
+  // every warp finds the label range itself (warp-cooperative search, no CTA barrier)
+  uint32_t lo, hi;
+  warp_label_range(f, c, l, lo, hi);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ctr + C_SEED, (unsigned long long)(hi - lo));
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   __shared__ uint32_t s_words[8][32];  // per-warp window of 32 bitmap words
@@ -351,7 +353,7 @@ struct FilterArgsT {
   unsigned long long* ctr;
   int variant;
   uint32_t word_lo;
-  uint32_t* claim;
+  LBArgs claim;
 };
 
 template <typename PT>
@@ -486,8 +488,11 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
     while (mm) {
       const int src = __ffs(mm) - 1;
       mm &= mm - 1;
-      const uint32_t rb = __shfl_sync(GSM_FULL, b, src), re = __shfl_sync(GSM_FULL, e, src);
+      const uint32_t rb0 = __shfl_sync(GSM_FULL, b, src), re0 = __shfl_sync(GSM_FULL, e, src);
       const uint32_t rrow = __shfl_sync(GSM_FULL, row, src);
+      // only the entries whose labels lie in [minl, maxl] (rows are sorted by label)
+      const uint32_t rb = warp_lower_bound(a.f[d].pred, rb0, re0, a.minl[d]);
+      const uint32_t re = warp_lower_bound(a.f[d].pred, rb, re0, a.maxl[d] + 1);
       uint32_t wsat = 0;
       for (uint32_t base = rb; base < re; base += 32) {
         const uint32_t k = base + lane;
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   uint32_t ch = c_begin + warp;
   if (dyn) {
     uint32_t c0 = 0;
-    if (lane == 0) c0 = atomicAdd(a.claim, 1u);
+    if (lane == 0) c0 = atomicAdd(a.claim.counter(), 1u);
     ch = c_begin + __shfl_sync(GSM_FULL, c0, 0);
   }
   uint32_t nxt = 0;
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     uint32_t cn = ch + nwarps;
     if (dyn) {
       uint32_t c0 = 0;
-      if (lane == 0) c0 = atomicAdd(a.claim, 1u);
+      if (lane == 0) c0 = atomicAdd(a.claim.counter(), 1u);
       cn = c_begin + __shfl_sync(GSM_FULL, c0, 0);
     }
     if (cn < n_chunks) {

@@ -32,6 +32,7 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
                                cudaStream_t st);
 
 // ----------------------------------------------------------------- bitmaps
+cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // one device word
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st);
 cudaError_t launch_and_inplace(uint32_t* dst, const uint32_t* src, uint32_t n_words, cudaStream_t st);
 cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag, cudaStream_t st);
@@ -51,12 +52,20 @@ __host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
   return f;
 }
 
-// decoupled look-back state of one launch (lookback.cuh)
+// decoupled look-back state of one launch (lookback.cuh).  The epoch is
+// device-resident (base of the current launch sequence + this launch's offset)
+// so a captured CUDA graph replays with fresh epochs: status words of an
+// earlier replay never look valid, and each epoch owns a zeroed tile counter.
 struct LBArgs {
   unsigned long long* status;  // epoch-stamped tile status words [cap_tiles]
-  uint32_t* counter;           // zeroed tile counter of this launch
-  uint32_t epoch;              // 1..65535, distinct per launch
+  uint32_t* counters;          // [LB_EPOCHS] zero until their epoch is used
+  const uint32_t* d_epoch;     // base epoch of the launch sequence (device)
+  uint32_t off;                // this launch's epoch offset from the base
   uint32_t cap_tiles;
+#ifdef __CUDACC__
+  __device__ __forceinline__ uint32_t epoch() const { return *(volatile const uint32_t*)d_epoch + off; }
+  __device__ __forceinline__ uint32_t* counter() const { return counters + epoch(); }
+#endif
 };
 cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
                                 unsigned long long* ctr, int sm_count, cudaStream_t st);
@@ -86,7 +95,7 @@ struct FilterArgs {
   int heavy;                // launch the heavy-row kernels
   int variant;              // bit0: SIMD label ranges (uint8 labels); bit1: dynamic chunk claiming
   uint32_t word_lo;         // first bitmap word of this rank's range (multiple of 32); n_words = end
-  uint32_t* claim;          // zeroed chunk counter of this launch (dynamic claiming)
+  LBArgs claim;             // its counter() is this launch's zeroed chunk counter (dynamic claiming)
   const uint32_t* rows;     // non-null: the center's candidate rows, compacted (row-list path)
   const unsigned long long* d_nrows;  // their count (device)
 };

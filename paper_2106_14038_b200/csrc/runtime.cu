@@ -2,6 +2,7 @@
 // build orchestration (a1, §6.2), planning entry points and result
 // accessors.  Host code only sequences kernels; every data-path step runs on
 // the GPU.  The executor (a3-a9) is in execute.cu.
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -337,7 +338,9 @@ extern "C" gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uin
                                      gsmart_plan_t** out) {
   if (!out) return GSMART_E_INVALID_ARG;
   *out = nullptr;
+  static std::atomic<uint64_t> next_uid{1};
   auto p = std::make_unique<gsmart_plan_t>();
+  p->uid = next_uid++;
   std::string err;
   gsmart_status s = build_plan(q, traversal, p.get(), &err);
   if (s != GSMART_OK) {

@@ -6,6 +6,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -68,6 +69,19 @@ struct Slot {
   uint64_t heavy_gen = ~0ull;          // LSpM generation the heavy buffers were sized for
   uint32_t* frows = nullptr;           // group filter: compacted candidate rows of the center
   uint64_t frows_cap = 0;
+  uint32_t* cand = nullptr;            // candidate bitmaps of the running plan (stable for graph replay)
+  uint64_t cand_words = 0;
+  uint32_t* d_epoch = nullptr;         // device base epoch of the current launch sequence
+  uint32_t epoch_next = 1, seq_base = 1, seq_off = 0;
+  uint64_t ws_gen = 0;                 // bumped whenever a workspace buffer moves
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t ws_gen = 0, lspm_gen = 0;
+    uint32_t flags = 0, n_lb = 0;
+    std::vector<int> launches;  // kernel launches inside the graph, per kernel class
+    uint64_t filter_main = 0;
+  };
+  std::unordered_map<uint64_t, GraphEntry> graphs;  // plan uid -> captured phase 1
 };
 
 }  // namespace gsm

@@ -41,7 +41,7 @@ def _bits_to_set(words, n):
 def _cands(G, eng, q, flags):
     """rows + candidate sets per variable from one execute."""
     pl = G.gsmart_plan(eng.ctx, q)
-    r = G.gsmart_execute(eng.ctx, pl, flags)
+    r = G.gsmart_execute(eng.ctx, pl, flags | G.GSMART_KEEP_CANDIDATES)
     try:
         rows = G.gsmart_result_rows(r)
         cs = {}
@@ -227,6 +227,33 @@ def test_lubm_full_size_sampled_parity(G, U):
             assert got.shape == exp.shape and np.array_equal(got, exp), q.name
     finally:
         e.close()
+
+
+def test_graph_replay_matches(G, eng):
+    """Plans executed repeatedly replay their captured phase-1 CUDA graph (fresh
+    look-back epochs each time); interleaved plans, batches and NO_GRAPH give
+    identical rows, equal to the oracle."""
+    d = lubm.generate(5)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = lubm.queries(d)
+    exp = [ix.query(q) for q in qs]
+    plans = [G.gsmart_plan(eng.ctx, q) for q in qs]
+    try:
+        for rep in range(3):
+            for flags in (0, G.GSMART_NO_GRAPH):
+                for q, pl, e in zip(qs, plans, exp):
+                    r = G.gsmart_execute(eng.ctx, pl, flags)
+                    got = G.gsmart_result_rows(r)
+                    G.gsmart_result_free(r)
+                    assert np.array_equal(got, e), (q.name, rep, flags)
+            for q, r, e in zip(qs, G.gsmart_execute_batch(eng.ctx, plans, 0), exp):
+                assert np.array_equal(G.gsmart_result_rows(r), e), (q.name, rep, "batch")
+                G.gsmart_result_free(r)
+    finally:
+        for pl in plans:
+            G.gsmart_plan_free(pl)
 
 
 def test_execute_batch_matches_single(G, eng):
