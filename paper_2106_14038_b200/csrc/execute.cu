@@ -31,7 +31,7 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   TRY(dalloc(ctx, &s.lb_counters, LB_EPOCHS, s.st));
   TRY(dalloc(ctx, &s.tile_start, LB_CAP_TILES, s.st));
   TRY(dalloc(ctx, &s.d_sz, 128, s.st));
-  TRY(dalloc(ctx, &s.d_ovf, 1, s.st));
+  s.d_ovf = reinterpret_cast<int*>(s.d_sz + 127);  // overflow flags travel with the sizes
   TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
   TRY(dalloc(ctx, &s.heavy_cnt, 4, s.st));
   TRY(dalloc(ctx, &s.d_epoch, 1, s.st));
@@ -50,9 +50,9 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
     dfree(st, b.alive);
   }
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
-  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ovf); dfree(st, s.d_ctr);
+  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
-  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch);
+  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2);
   for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second.exec);
   s.graphs.clear();
   cudaStreamSynchronize(st);
@@ -105,7 +105,9 @@ static gsmart_status begin_seq(gsmart_ctx* ctx, Slot& s) {
   }
   s.seq_base = s.epoch_next;
   s.seq_off = 0;
-  CU(launch_set_u32(s.d_epoch, s.seq_base, s.st));
+  // the sequence's first kernel (k_init_cands) copies it to s.d_epoch; the slot is
+  // idle here (every execute drains its stream before the next one begins)
+  reinterpret_cast<volatile uint32_t*>(s.h_pin + H_EPOCH)[0] = s.seq_base;
   return GSMART_OK;
 }
 
@@ -210,6 +212,7 @@ struct Exec {
   int attempts = 0;
   bool seq_open = false;        // a look-back launch sequence was started (end it in finalize)
   bool graph_replayed = false;  // phase 1 came from the plan's cached CUDA graph
+  bool ctr_pinned = false;      // counters already copied to sl.h_pin[192..) on the stream
   uint32_t wlo = 0, whi = 0, slice = 0;  // this rank's bitmap words (1-D vertex-range partition)
   bool identity = false;                 // trie order == column order: rows come out sorted
   std::vector<uint64_t> F;
@@ -250,8 +253,16 @@ struct Exec {
     for (uint32_t v : plan->vars)
       if (by_var[v].empty()) ones |= 1u << slot[v];
     if (!plan->vars.empty()) {
+      InitExtra x;
+      x.h_epoch = reinterpret_cast<const volatile uint32_t*>(sl.h_pin + H_EPOCH);
+      x.d_epoch = sl.d_epoch;
+      x.zero = sl.d_ctr;  // counters
+      x.n_zero = C_NCTR;
+      x.zero2 = sl.d_sz;  // expansion sizes
+      x.n_zero2 = 128;
+      x.ovf = sl.d_ovf;
       prof.begin(K_BITMAP);
-      CU(launch_init_cands(sl.cand, (uint32_t)plan->vars.size(), Wpad, N, ones, sl.st));
+      CU(launch_init_cands(sl.cand, (uint32_t)plan->vars.size(), Wpad, N, ones, x, sl.st));
       launches[K_BITMAP]++;
       prof.end();
     }
@@ -265,14 +276,28 @@ struct Exec {
       }
       prof.end();
     }
+    SeedBatch sb;
+    memset(&sb, 0, sizeof sb);
+    sb.f[0] = fa[0];
+    sb.f[1] = fa[1];
     for (uint32_t v : plan->vars) {
       const auto& ss = by_var[v];
       if (ss.empty()) continue;
+      if (sb.n == MAX_SEEDS) FAIL(GSMART_E_UNSUPPORTED, "more than 16 seeded variables");
+      sb.dir[sb.n] = ss[0]->dir == OUT ? 0 : 1;
+      sb.c[sb.n] = ss[0]->cid;
+      sb.label[sb.n] = ss[0]->label;
+      sb.bits[sb.n] = cand(v);
+      sb.n++;
+    }
+    if (sb.n) {
       prof.begin(K_SEED);
-      CU(launch_seed_scatter(fa[ss[0]->dir == OUT ? 0 : 1], ctx->pred_bytes, ss[0]->cid, ss[0]->label, cand(v),
-                             sl.d_ctr, ctx->sm_count, sl.st));
+      CU(launch_seed_scatter(sb, ctx->pred_bytes, sl.d_ctr, ctx->sm_count, sl.st));
       launches[K_SEED]++;
       prof.end();
+    }
+    for (uint32_t v : plan->vars) {
+      const auto& ss = by_var[v];
       if (ss.size() > 1) {
         // (c -l-> v): v's CSC row must hold (l, c); (v -l-> c): v's CSR row must hold (l, c)
         Group g;
@@ -306,7 +331,7 @@ struct Exec {
       CU(cudaMemsetAsync(d_nrows, 0, 8, sl.st));
       CU(launch_bitmap_compact_lb(cand(g.center) + wlo, whi > wlo ? whi - wlo : 0, sl.frows, sl.frows_cap, d_nrows,
                                   sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
-      launches[K_COMPACT]++;
+      launches[K_COMPACT] += compact_launches(whi > wlo ? whi - wlo : 0);
       prof.end();
     }
     while (done[0] < by[0].size() || done[1] < by[1].size()) {
@@ -361,16 +386,16 @@ struct Exec {
   }
 
   // ---- a5/a6/a7: one expansion attempt over all levels (async), sizes -> pinned
-  gsmart_status launch_expansion() {
+  // fresh: sizes and overflow flags were zeroed by this execute's k_init_cands
+  gsmart_status launch_expansion(bool fresh) {
     unsigned long long* dsz = sl.d_sz;
-    CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
-    CU(cudaMemsetAsync(sl.d_ovf, 0, 4, sl.st));
+    if (!fresh) CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
     if (L > 1) CU(cudaMemsetAsync(sl.lv[0].alive, 0, sl.lv[0].cap, sl.st));
     prof.begin(K_COMPACT);
     // level 0 = this rank's root candidates (its word range; all of them when world == 1)
     CU(launch_bitmap_compact_lb(cand(plan->levels[0].var) + wlo, whi - wlo, sl.lv[0].bind, sl.lv[0].cap, dsz + 0,
                                 sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
-    launches[K_COMPACT]++;
+    launches[K_COMPACT] += compact_launches(whi - wlo);
     prof.end();
     for (uint32_t k = 1; k < L; k++) {
       const Level& Lv = plan->levels[k];
@@ -401,7 +426,7 @@ struct Exec {
         prof.begin(K_COMPACT);
         CU(launch_bitmap_compact_lb(cand(Lv.var), W, sl.list[k], sl.list_cap[k], dsz + 64 + k, sl.d_ovf,
                                     next_lb(sl), ctx->sm_count, sl.st));
-        launches[K_COMPACT]++;
+        launches[K_COMPACT] += compact_launches(W);
         prof.end();
         a.list = sl.list[k];
         a.d_list_len = dsz + 64 + k;
@@ -428,13 +453,12 @@ struct Exec {
       launches[K_EXPAND_EMIT]++;
       prof.end();
     }
-    CU(cudaMemcpyAsync(dsz + 127, sl.d_ovf, 4, cudaMemcpyDeviceToDevice, sl.st));
     CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
     return GSMART_OK;
   }
 
   gsmart_status relaunch_expansion() {
-    TRY(launch_expansion());
+    TRY(launch_expansion(false));
     CU(cudaEventRecord(sl.ev, sl.st));
     state = S_EXPANDING;
     return GSMART_OK;
@@ -455,14 +479,13 @@ struct Exec {
 
   // phase 1 = seeds + grouped evaluation + expansion: pure device work on
   // stable workspace addresses, launched directly or replayed from a graph
-  gsmart_status phase1_kernels() {
-    CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
+  gsmart_status phase1_kernels() {  // counters/sizes are zeroed by k_init_cands
     bool empty = false;
     TRY(seeds_and_guards(&empty));
     for (auto& g : plan->groups) TRY(eval_group(g));
     if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
       for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i]));
-    return launch_expansion();
+    return launch_expansion(true);
   }
 
   gsmart_status run_phase1() {
@@ -625,6 +648,10 @@ struct Exec {
   // ---- a8 prune + compaction, a9 rows + sort (async)
   gsmart_status phase2() {
     state = S_PHASE2;
+    // phase 1 wrote every counter: read them back with the rest of the stream
+    static_assert(C_NCTR <= 64, "counter readback slots");
+    CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
+    ctr_pinned = true;
     TRY(keep_candidates());
     const uint64_t n_rows = F[L - 1];
     unsigned long long* dsz = sl.d_sz;
@@ -638,6 +665,20 @@ struct Exec {
       R->count_only = (flags & GSMART_COUNT_ONLY) != 0;
       return GSMART_OK;
     }
+    // one allocation owns the result's levels and rows (each part 256-B aligned)
+    const uint32_t nc = (uint32_t)plan->vars.size();
+    const bool want_rows = !(flags & GSMART_COUNT_ONLY);
+    auto al = [](uint64_t b) { return (b + 255) / 256 * 256; };
+    uint64_t arena_bytes = 0;
+    for (uint32_t k = 0; k < L; k++) arena_bytes += al(F[k] * 4) * (k > 0 ? 2 : 1);
+    if (want_rows) arena_bytes += al(n_rows * nc * 4);
+    char* arena = nullptr;
+    TRY(alloc_result((void**)&arena, arena_bytes));
+    auto take = [&](uint64_t b) {
+      char* p = arena;
+      arena += al(b);
+      return p;
+    };
     prof.begin(K_PRUNE);
     for (uint32_t k = L - 1; k >= 1; k--) {
       CU(launch_prune_mark_d(sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
@@ -646,8 +687,8 @@ struct Exec {
     }
     for (uint32_t k = 0; k < L; k++) {
       gsmart_result::Lv lv{plan->levels[k].var, 0, nullptr, nullptr};
-      TRY(alloc_result((void**)&lv.bind, F[k] * 4));
-      if (k > 0) TRY(alloc_result((void**)&lv.parent, F[k] * 4));
+      lv.bind = (uint32_t*)take(F[k] * 4);
+      if (k > 0) lv.parent = (uint32_t*)take(F[k] * 4);
       CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind, k + 1 < L ? sl.lv[k].alive : nullptr,
                                  dsz + k, k > 0 ? sl.lv[k - 1].newidx : nullptr, lv.parent, lv.bind,
                                  k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), ctx->sm_count,
@@ -659,23 +700,31 @@ struct Exec {
     }
     prof.end();
     CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
-    if (!(flags & GSMART_COUNT_ONLY)) {
-      const uint32_t nc = (uint32_t)plan->vars.size();
+    if (want_rows) {
       std::vector<uint32_t> col_of_level(L);
       for (uint32_t k = 0; k < L; k++) col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
-      uint32_t* rows = nullptr;
-      TRY(identity ? alloc_result((void**)&rows, n_rows * nc * 4) : sc.get(&rows, n_rows * nc));
+      uint32_t* out = (uint32_t*)take(n_rows * nc * 4);
+      uint32_t* rows = out;
+      size_t tb = 0;
+      if (!identity) {  // enumerate into slot scratch, then sort into the result
+        tb = sort_rows_tmp_bytes(n_rows, nc);
+        const uint64_t need = al(n_rows * nc * 4) + al(tb);
+        if (need > sl.p2_cap) {
+          dfree(sl.st, sl.p2);
+          sl.p2 = nullptr;
+          sl.p2_cap = 0;
+          TRY(dalloc(ctx, &sl.p2, need + need / 4, sl.st));
+          sl.p2_cap = need + need / 4;
+        }
+        rows = (uint32_t*)sl.p2;
+      }
       prof.begin(K_ENUMERATE);
       CU(launch_enumerate(pt, L, col_of_level.data(), (uint32_t)n_rows, nc, rows, sl.st));
       launches[K_ENUMERATE]++;
       prof.end();
-      if (identity) {
-        R->d_rows = rows;  // trie order == lexicographic order in variable-index order
-      } else {
-        TRY(alloc_result((void**)&R->d_rows, n_rows * nc * 4));
-        size_t tb = sort_rows_tmp_bytes(n_rows, nc);
-        void* tmp = nullptr;
-        TRY(sc.get((char**)&tmp, tb));
+      R->d_rows = out;
+      if (!identity) {  // otherwise trie order == lexicographic order in variable-index order
+        void* tmp = sl.p2 + al(n_rows * nc * 4);
         prof.begin(K_SORT_ROWS);
         CU(sort_rows(rows, R->d_rows, n_rows, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
         prof.end();
@@ -735,7 +784,8 @@ struct Exec {
     }
     if (ctx->world > 1 && state == S_PHASE2) TRY(gather_rows());
     unsigned long long c[C_NCTR];
-    CU(cudaMemcpy(c, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost));
+    if (ctr_pinned) memcpy(c, sl.h_pin + 192, C_NCTR * 8);
+    else CU(cudaMemcpy(c, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost));
     auto& st = R->stats;
     st.filter_rows = c[C_FILTER_ROWS];
     st.filter_entries = c[C_FILTER_SCANNED];
@@ -753,6 +803,21 @@ struct Exec {
     for (uint32_t k = 1; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) children += st.level_nodes[k];
     st.bytes[K_EXPAND_SEG] = 12 * parents;
     st.bytes[K_EXPAND_EMIT] = 4 * c[C_EXPAND] + 9 * children + 8 * parents;
+    // a5: every compaction reads this rank's bitmap range once and writes 4 B per id
+    // (row lists of the groups + level 0); initialisation writes the bitmaps once
+    const uint64_t range_bytes = 4ull * (whi - wlo);
+    st.bytes[K_COMPACT] = range_bytes * (uint64_t)launches[K_COMPACT] + 4 * (c[C_FILTER_ROWS] + st.level_nodes[0]);
+    st.bytes[K_BITMAP] = 4ull * Wpad * plan->vars.size();
+    // a8: mark reads parent (4) + alive (1) per child; compaction reads bind/parent/alive
+    // (9) and writes newidx (4) per node, plus 8 B per surviving node
+    // a9: 4 B per output cell + 8 B per surviving trie node read while walking parents
+    uint64_t prune = 0, alive = 0;
+    for (uint32_t k = 0; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) {
+      prune += (k ? 5 : 0) * st.level_nodes[k] + 13 * st.level_nodes[k] + 8 * st.level_alive[k];
+      alive += st.level_alive[k];
+    }
+    st.bytes[K_PRUNE] = state == S_PHASE2 ? prune : 0;
+    st.bytes[K_ENUMERATE] = launches[K_ENUMERATE] ? 4ull * R->n_rows * R->n_cols + 8 * alive : 0;
     for (int i = 0; i < GSMART_NKERNELS; i++) st.launches[i] = (uint64_t)launches[i];
     for (int i = 0; i < GSMART_NKERNELS; i++) st.kernel_names[i] = kKernelNames[i];
     if (!(flags & (GSMART_KEEP_ON_DEVICE | GSMART_COUNT_ONLY)) && R->d_rows && R->n_rows) {

@@ -35,72 +35,169 @@ __device__ __forceinline__ uint32_t ancestor(const LevelTab& t, uint32_t k, uint
 }
 
 // ------------------------------------------------------------------ bitmap -> ids
-constexpr int BC_T = 256, BC_W = 8, BC_TILE = BC_T * BC_W;  // words per tile
+// One launch, no inter-CTA chain.  The range is cut into <= ~4 chunks per SM of
+// whole 2048-word sub-tiles; a CTA takes a ticket (chunks in ticket order, so it
+// only ever waits on CTAs that are already running), and
+//   1. streams its chunk once (each lane 32 contiguous bytes per 256-word slice)
+//      into per-slice popcounts kept in shared memory, publishes the chunk total;
+//   2. sums the totals of all earlier chunks - every one is published directly,
+//      so this is one parallel read, not a walk back to an inclusive prefix;
+//   3. emits its ids sub-tile by sub-tile: a warp's offset comes from the slice
+//      counts (no block barrier), empty slices are skipped, and the re-read of a
+//      non-empty slice hits L2.
+// (A decoupled look-back over thousands of small tiles spent most of its time
+// walking back to the last inclusive prefix.)
+constexpr int BC_T = 256, BC_W = 8, BC_SLICE = BC_W * 32, BC_SUB = BC_SLICE * (BC_T / 32);
+constexpr uint32_t BC_MAX_SLICES = 2048;  // slices per chunk (their counts live in smem)
+constexpr uint32_t BC_MAX_CHUNKS = 8192;
 
-__global__ void __launch_bounds__(BC_T) k_bitmap_compact_lb(const uint32_t* __restrict__ bm, uint32_t n_words,
-                                                           uint32_t* __restrict__ ids, uint64_t cap,
-                                                           unsigned long long* d_count, int* overflow,
-                                                           LBArgs lb, uint32_t id_base) {
-  __shared__ uint32_t s_tile;
+static uint32_t bc_chunk_words(uint32_t n_words, int sm_count) {
+  const uint64_t want = (uint64_t)sm_count * 4;
+  const uint64_t per = std::max<uint64_t>(((uint64_t)n_words + want - 1) / want,
+                                          ((uint64_t)n_words + BC_MAX_CHUNKS - 1) / BC_MAX_CHUNKS);
+  const uint64_t c = std::max<uint64_t>(BC_SUB, (per + BC_SUB - 1) / BC_SUB * BC_SUB);
+  return (uint32_t)std::min<uint64_t>(c, (uint64_t)BC_MAX_SLICES * BC_SLICE);
+}
+
+__global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restrict__ bm, uint32_t n_words,
+                                                        uint32_t chunk, uint32_t* __restrict__ ids, uint64_t cap,
+                                                        unsigned long long* d_count, int* overflow, LBArgs lb,
+                                                        uint32_t id_base) {
   __shared__ unsigned long long s_red[32];
-  __shared__ unsigned long long s_pref;
-  const uint32_t ntiles = (n_words + BC_TILE - 1) / BC_TILE;
+  __shared__ unsigned long long s_p;
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_cnt[BC_MAX_SLICES];
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // warp wib of a tile owns words [tile*2048 + wib*256, +256) in 8 coalesced rounds of
-  // 32 words; ids are emitted warp-cooperatively (lane b writes bit b of each word)
-  while (true) {
-    const uint32_t tile = lb_claim(lb.counter(), &s_tile);
-    if (tile >= ntiles) break;
-    const uint64_t wbase = (uint64_t)tile * BC_TILE + wib * (BC_W * 32);
-    uint32_t w[BC_W], off[BC_W];
-    uint32_t run = 0;  // words of earlier rounds in this warp
-#pragma unroll
-    for (int r = 0; r < BC_W; r++) {
-      const uint64_t wi = wbase + r * 32 + lane;
-      w[r] = wi < n_words ? __ldcg(bm + wi) : 0u;
+  const uint32_t nch = (n_words + chunk - 1) / chunk;
+  const uint32_t epoch = lb.epoch();
+  const uint32_t tk = lb_claim(lb.counter(), &s_tile);
+  if (tk >= nch) return;
+  const uint64_t w0 = (uint64_t)tk * chunk, w1 = std::min<uint64_t>(n_words, w0 + chunk);
+  const uint32_t nsl = (uint32_t)((w1 - w0 + BC_SLICE - 1) / BC_SLICE);
+  // 1. slice counts
+  const bool vec = (reinterpret_cast<uintptr_t>(bm) & 15) == 0;
+  uint32_t wtot = 0;
+#pragma unroll 4
+  for (uint32_t si = wib; si < nsl; si += BC_T / 32) {
+    const uint64_t lw = w0 + (uint64_t)si * BC_SLICE + lane * 8;  // this lane's 8 words
+    uint32_t c = 0;
+    if (vec && lw + 8 <= w1) {
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(bm + lw));
+      const uint4 y = __ldcg(reinterpret_cast<const uint4*>(bm + lw + 4));
+      c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w) + __popc(y.x) + __popc(y.y) + __popc(y.z) +
+          __popc(y.w);
+    } else {
+      for (uint64_t i = lw; i < std::min<uint64_t>(lw + 8, w1); i++) c += __popc(__ldcg(bm + i));
     }
 #pragma unroll
-    for (int r = 0; r < BC_W; r++) {
-      const uint32_t c = __popc(w[r]);
-      uint32_t incl = c;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(GSM_FULL, c, o);
+    if (lane == 0) s_cnt[si] = c;
+    wtot += c;
+  }
+  const unsigned long long tot =
+      block_reduce_sum<unsigned long long>(lane == 0 ? (unsigned long long)wtot : 0ull, s_red);
+  if (threadIdx.x == 0) atomicExch(lb.status + tk, lb_pack(epoch, 1, tot));
+  // 2. prefix = sum of the earlier chunks' totals (each published on its own)
+  unsigned long long p = 0;
+  for (uint32_t i = threadIdx.x; i < tk; i += BC_T) {
+    unsigned long long v;
+    do {
+      v = *((volatile unsigned long long*)(lb.status + i));
+    } while ((uint32_t)(v >> 48) != epoch);
+    p += v & LB_VMASK;
+  }
+  p = block_reduce_sum<unsigned long long>(p, s_red);
+  if (threadIdx.x == 0) s_p = p;
+  __syncthreads();
+  // 3. emission
+  uint64_t run_base = s_p;  // ids before the current sub-tile (identical in all warps)
+  for (uint64_t t = w0; t < w1; t += BC_SUB) {
+    const uint32_t s0 = (uint32_t)((t - w0) / BC_SLICE);
+    const uint32_t c = (lane < BC_T / 32 && s0 + lane < nsl) ? s_cnt[s0 + lane] : 0u;
+    uint32_t tot8 = c, before = lane < wib ? c : 0u;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(GSM_FULL, incl, o);
-        if ((int)lane >= o) incl += y;
+    for (int o = 16; o > 0; o >>= 1) {
+      tot8 += __shfl_xor_sync(GSM_FULL, tot8, o);
+      before += __shfl_xor_sync(GSM_FULL, before, o);
+    }
+    const uint32_t mine = __shfl_sync(GSM_FULL, c, wib);
+    if (run_base + tot8 > cap) {  // capacity: flag once, the host grows and re-runs
+      if (threadIdx.x == 0 && tot8) atomicOr(overflow, 1);
+    } else if (mine) {
+      const uint64_t wbase = t + (uint64_t)wib * BC_SLICE;
+      uint32_t w[BC_W], incl[BC_W], rbase[BC_W];
+#pragma unroll
+      for (int r = 0; r < BC_W; r++) {
+        const uint64_t wi = wbase + r * 32 + lane;
+        w[r] = wi < w1 ? __ldcs(bm + wi) : 0u;
       }
-      off[r] = run + incl - c;
-      run += __shfl_sync(GSM_FULL, incl, 31);
-    }
-    // block: exclusive scan of the 8 warp totals
-    unsigned long long tot;
-    const unsigned long long wex =
-        block_exclusive_scan<unsigned long long>(lane == 0 ? (unsigned long long)run : 0ull, s_red, &tot);
-    const uint64_t pref = lb_prefix(lb.status, lb.epoch(), tile, tot, &s_pref);
-    const uint64_t base_pos = pref + __shfl_sync(GSM_FULL, wex, 0);
+      uint32_t run = 0;
 #pragma unroll
-    for (int r = 0; r < BC_W; r++) {
-      uint32_t nz = __ballot_sync(GSM_FULL, w[r] != 0);
-      while (nz) {
-        const int j = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t wj = __shfl_sync(GSM_FULL, w[r], j), oj = __shfl_sync(GSM_FULL, off[r], j);
-        if ((wj >> lane) & 1u) {
-          const uint64_t pos = base_pos + oj + __popc(wj & lanemask_lt());
-          if (pos < cap) ids[pos] = (uint32_t)((wbase + r * 32 + j) * 32 + lane) + id_base;
-          else atomicOr(overflow, 1);
+      for (int r = 0; r < BC_W; r++) {
+        incl[r] = __popc(w[r]);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(GSM_FULL, incl[r], o);
+          if ((int)lane >= o) incl[r] += y;
+        }
+        rbase[r] = run;
+        run += __shfl_sync(GSM_FULL, incl[r], 31);
+      }
+      const uint64_t base_pos = run_base + before;
+#pragma unroll
+      for (int r = 0; r < BC_W; r++) {
+        const uint32_t total = __shfl_sync(GSM_FULL, incl[r], 31);
+        uint32_t nz = __ballot_sync(GSM_FULL, w[r] != 0);
+        const uint32_t id0 = (uint32_t)((wbase + r * 32) * 32) + id_base;
+        uint32_t* out = ids + base_pos + rbase[r];
+        if ((total + 31) / 32 * 3 <= (uint32_t)__popc(nz)) {
+          // sparse words: id j of the round goes to lane j % 32 (coalesced stores);
+          // its word = #lanes with incl <= j, its bit = the (j - excl)-th set bit
+          for (uint32_t j0 = 0; j0 < total; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint32_t q = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1)
+              if (__shfl_sync(GSM_FULL, incl[r], q + s - 1) <= j) q += s;
+            uint32_t wq = __shfl_sync(GSM_FULL, w[r], q);
+            uint32_t k = j - (__shfl_sync(GSM_FULL, incl[r], q) - __popc(wq));
+            uint32_t bit = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+              const uint32_t lowc = __popc(wq & ((1u << s) - 1u));
+              if (k >= lowc) {
+                k -= lowc;
+                wq >>= s;
+                bit += s;
+              }
+            }
+            if (j < total) out[j] = id0 + q * 32 + bit;
+          }
+        } else {
+          // dense words: the warp walks the non-zero words, lane b emits bit b
+          const uint32_t excl = incl[r] - __popc(w[r]);
+          while (nz) {
+            const int j = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t wj = __shfl_sync(GSM_FULL, w[r], j), oj = __shfl_sync(GSM_FULL, excl, j);
+            if ((wj >> lane) & 1u) out[oj + __popc(wj & lanemask_lt())] = id0 + j * 32 + lane;
+          }
         }
       }
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) *d_count = pref + tot;
+    run_base += tot8;
   }
+  if (tk == nch - 1 && threadIdx.x == 0) *d_count = run_base;
 }
 
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
                                      cudaStream_t st, uint32_t id_base) {
-  uint32_t ntiles = (n_words + BC_TILE - 1) / BC_TILE;
-  unsigned g = std::max(1u, std::min(ntiles, (uint32_t)sm_count * 8));
-  k_bitmap_compact_lb<<<g, BC_T, 0, st>>>(bm, n_words, ids, cap, d_count, overflow, lb, id_base);
+  if (n_words == 0) return cudaMemsetAsync(d_count, 0, 8, st);
+  const uint32_t chunk = bc_chunk_words(n_words, sm_count);
+  const uint32_t nch = (n_words + chunk - 1) / chunk;
+  if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
+  k_bitmap_compact<<<nch, BC_T, 0, st>>>(bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base);
   return cudaGetLastError();
 }
 
@@ -263,16 +360,16 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
     unsigned long long ex = block_exclusive_scan<unsigned long long>((unsigned long long)__popc(keepm), s_red, &tot);
     const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch(), tile, tot, &s_pref);
     uint64_t pos = pref + ex;
+    if (pref + tot > a.cap_out) {  // capacity: flag once per tile, the host grows and re-runs
+      if (threadIdx.x == 0 && tot) atomicOr(a.overflow, 1);
+      keepm = 0;
+    }
 #pragma unroll
     for (int j = 0; j < EX_I; j++) {
       if (!((keepm >> j) & 1u)) continue;
-      if (pos < a.cap_out) {
-        a.out_parent[pos] = node[j];
-        a.out_bind[pos] = child[j];
-        if (a.out_alive) a.out_alive[pos] = 0;
-      } else {
-        atomicOr(a.overflow, 1);
-      }
+      a.out_parent[pos] = node[j];
+      a.out_bind[pos] = child[j];
+      if (a.out_alive) a.out_alive[pos] = 0;
       pos++;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) *a.d_nout = pref + tot;

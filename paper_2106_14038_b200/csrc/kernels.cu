@@ -190,13 +190,6 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // =====================================================================================
 // bitmaps
 // =====================================================================================
-__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
-
-cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
-  k_set_u32<<<1, 1, 0, st>>>(p, v);
-  return cudaGetLastError();
-}
-
 // all-ones over bits [0, n_bits), zero beyond (padding words included)
 __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
@@ -211,7 +204,17 @@ __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
 
 // every variable's candidate bitmap in one launch: slot s is all-ones over
 // [0, n_bits) if bit s of ones_mask is set (no seed), else zero (seeded)
-__global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, uint32_t n_bits, uint32_t ones_mask) {
+__global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, uint32_t n_bits, uint32_t ones_mask,
+                             InitExtra x) {
+  // first kernel of an execute: publish the look-back epoch base the host wrote to
+  // pinned memory (a replayed graph thus needs no extra launch to set it) and zero
+  // the execute's counters and size words (no memset nodes)
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0 && x.d_epoch) *x.d_epoch = *x.h_epoch;
+    if (threadIdx.x == 0 && x.ovf) *x.ovf = 0;
+    for (uint32_t i = threadIdx.x; i < x.n_zero; i += blockDim.x) x.zero[i] = 0;
+    for (uint32_t i = threadIdx.x; i < x.n_zero2; i += blockDim.x) x.zero2[i] = 0;
+  }
   const uint64_t total = (uint64_t)n_slots * stride;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = (uint32_t)(i / stride), w = (uint32_t)(i - (uint64_t)s * stride);
@@ -225,9 +228,9 @@ __global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, 
 }
 
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
-                              uint32_t ones_mask, cudaStream_t st) {
-  k_init_cands<<<grid_for((uint64_t)n_slots * stride_words, 256, 148 * 16), 256, 0, st>>>(cand, n_slots, stride_words,
-                                                                                        n_bits, ones_mask);
+                              uint32_t ones_mask, const InitExtra& x, cudaStream_t st) {
+  k_init_cands<<<grid_for((uint64_t)n_slots * stride_words, 256, 148 * 16), 256, 0, st>>>(
+      cand, n_slots, stride_words, n_bits, ones_mask, x);
   return cudaGetLastError();
 }
 
@@ -261,9 +264,13 @@ cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag,
 // a3 — constant seeding ("light" edges): bits |= {col : (c, l, col)}
 // =====================================================================================
 template <typename PT>
-__global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __restrict__ bits,
-                               unsigned long long* ctr) {
-  // every warp finds the label range itself (warp-cooperative search, no CTA barrier)
+__global__ void k_seed_scatter(SeedBatch sb, unsigned long long* ctr) {
+  // blockIdx.y = seed; every warp finds the label range itself (warp-cooperative
+  // search, no CTA barrier)
+  const uint32_t si = blockIdx.y;
+  const Fmt<PT> f = fmt_of<PT>(sb.f[sb.dir[si]]);
+  const uint32_t c = sb.c[si], l = sb.label[si];
+  uint32_t* __restrict__ bits = sb.bits[si];
   uint32_t lo, hi;
   warp_label_range(f, c, l, lo, hi);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ctr + C_SEED, (unsigned long long)(hi - lo));
@@ -307,11 +314,12 @@ __global__ void k_seed_scatter(Fmt<PT> f, uint32_t c, uint32_t l, uint32_t* __re
   }
 }
 
-cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
-                                unsigned long long* ctr, int sm_count, cudaStream_t st) {
-  unsigned g = (unsigned)sm_count * 4;
-  if (pred_bytes == 1) k_seed_scatter<uint8_t><<<g, 256, 0, st>>>(fmt_of<uint8_t>(f), c, label, bits, ctr);
-  else k_seed_scatter<uint16_t><<<g, 256, 0, st>>>(fmt_of<uint16_t>(f), c, label, bits, ctr);
+cudaError_t launch_seed_scatter(const SeedBatch& sb, int pred_bytes, unsigned long long* ctr, int sm_count,
+                                cudaStream_t st) {
+  if (sb.n == 0) return cudaSuccess;
+  const dim3 g(std::max<unsigned>((unsigned)sm_count * 4 / sb.n, (unsigned)sm_count), sb.n);
+  if (pred_bytes == 1) k_seed_scatter<uint8_t><<<g, 256, 0, st>>>(sb, ctr);
+  else k_seed_scatter<uint16_t><<<g, 256, 0, st>>>(sb, ctr);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,6 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
                                cudaStream_t st);
 
 // ----------------------------------------------------------------- bitmaps
-cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // one device word
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st);
 cudaError_t launch_and_inplace(uint32_t* dst, const uint32_t* src, uint32_t n_words, cudaStream_t st);
 cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag, cudaStream_t st);
@@ -67,8 +66,16 @@ struct LBArgs {
   __device__ __forceinline__ uint32_t* counter() const { return counters + epoch(); }
 #endif
 };
-cudaError_t launch_seed_scatter(FmtAny f, int pred_bytes, uint32_t c, uint32_t label, uint32_t* bits,
-                                unsigned long long* ctr, int sm_count, cudaStream_t st);
+// a3: the first seed of every seeded variable in one launch (blockIdx.y = seed)
+constexpr uint32_t MAX_SEEDS = 16;
+struct SeedBatch {
+  FmtAny f[2];
+  uint32_t n;
+  uint32_t dir[MAX_SEEDS], c[MAX_SEEDS], label[MAX_SEEDS];
+  uint32_t* bits[MAX_SEEDS];
+};
+cudaError_t launch_seed_scatter(const SeedBatch& sb, int pred_bytes, unsigned long long* ctr, int sm_count,
+                                cudaStream_t st);
 cudaError_t launch_guard(FmtAny f, int pred_bytes, uint32_t s, uint32_t label, uint32_t o, int* flag,
                          cudaStream_t st);
 
@@ -99,8 +106,18 @@ struct FilterArgs {
   const uint32_t* rows;     // non-null: the center's candidate rows, compacted (row-list path)
   const unsigned long long* d_nrows;  // their count (device)
 };
+// extra work of the first kernel of an execute (all optional)
+struct InitExtra {
+  const volatile uint32_t* h_epoch = nullptr;  // pinned host word: the look-back epoch base
+  uint32_t* d_epoch = nullptr;
+  unsigned long long* zero = nullptr;
+  uint32_t n_zero = 0;
+  unsigned long long* zero2 = nullptr;
+  uint32_t n_zero2 = 0;
+  int* ovf = nullptr;
+};
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
-                              uint32_t ones_mask, cudaStream_t st);
+                              uint32_t ones_mask, const InitExtra& x, cudaStream_t st);
 cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_count, cudaStream_t st,
                                 int* launches);
 
@@ -141,6 +158,8 @@ struct ExpArgs2 {
   LBArgs lb;
 };
 // ids of set bits of bm[0, n_words) plus id_base
+// kernels one launch_bitmap_compact_lb issues (none for an empty range)
+inline int compact_launches(uint32_t n_words) { return n_words ? 1 : 0; }
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
                                      cudaStream_t st, uint32_t id_base = 0);

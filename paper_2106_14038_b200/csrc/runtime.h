@@ -42,6 +42,7 @@ inline int bits_for(uint64_t v) {  // bits to represent values in [0, v]
 constexpr uint32_t LB_CAP_TILES = 1u << 22;  // 4M tiles x 1024 entries = the 2^32-entry limit
 constexpr uint32_t LB_EPOCHS = 65536;
 constexpr uint32_t MAX_SLOTS = 16;
+constexpr uint32_t H_EPOCH = 255;  // h_pin slot: look-back epoch base of the running execute
 
 // One concurrent execution lane: a stream plus everything an in-flight
 // execute writes (workspace, look-back state, counters, pinned readback).
@@ -64,13 +65,15 @@ struct Slot {
   unsigned long long* d_sz = nullptr;  // [0,32) F_k, [32,64) T_k, [64,96) list len, [96,128) alive, 127 overflow
   int* d_ovf = nullptr;
   unsigned long long* d_ctr = nullptr; // C_NCTR counters, then scratch (flag at 48)
-  unsigned long long* h_pin = nullptr; // 256 pinned slots
+  unsigned long long* h_pin = nullptr; // 256 pinned slots: [0,128) sizes, [128,160) alive, [192,..) counters, H_EPOCH
   uint32_t *heavy_rows = nullptr, *heavy_chunks = nullptr, *heavy_sat = nullptr, *heavy_cnt = nullptr;
   uint64_t heavy_gen = ~0ull;          // LSpM generation the heavy buffers were sized for
   uint32_t* frows = nullptr;           // group filter: compacted candidate rows of the center
   uint64_t frows_cap = 0;
   uint32_t* cand = nullptr;            // candidate bitmaps of the running plan (stable for graph replay)
   uint64_t cand_words = 0;
+  char* p2 = nullptr;                  // phase-2 scratch (unsorted rows + sort temp), grow-only
+  uint64_t p2_cap = 0;
   uint32_t* d_epoch = nullptr;         // device base epoch of the current launch sequence
   uint32_t epoch_next = 1, seq_base = 1, seq_off = 0;
   uint64_t ws_gen = 0;                 // bumped whenever a workspace buffer moves

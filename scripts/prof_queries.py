@@ -42,3 +42,4 @@ for rep in range(args.reps):
             print(f"{q.name:4s} rows={n:9d} wall_ms={dt:7.3f} launches={sum(st['launches'].values()):3d} "
                   f"levels={st['level_nodes']} filter_rows={st['filter_rows']} scanned={st['filter_entries']} "
                   f"expand={st['expand_entries']}", flush=True)
+            print("     ", {k: v for k, v in st['launches'].items() if v}, "cols", G.gsmart_result_shape(r0)[1] if False else "", flush=True)
