@@ -97,6 +97,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Programmatic dependent launch (sm_90+): every query-path kernel is launched
+// with programmatic stream serialization (pdl_launch), so the next kernel's CTAs
+// are scheduled while this one drains.  Each kernel first waits for its
+// predecessor grid to complete and flush (griddepcontrol.wait) - before ANY load
+// or store, so no read-after-write or write-after-read hazard can cross it - then
+// at once lets its own dependents launch (griddepcontrol.launch_dependents); they
+// in turn wait for this grid's completion before touching memory.
+#define GSM_PDL_ENTRY()                                        \
+  do {                                                         \
+    asm volatile("griddepcontrol.wait;" ::: "memory");         \
+    asm volatile("griddepcontrol.launch_dependents;" :::);     \
+  } while (0)
+
 // Block-wide exclusive scan of one value per thread (blockDim.x <= 1024, multiple of 32).
 template <typename T>
 __device__ __forceinline__ T block_exclusive_scan(T v, T* smem /* >= 32 */, T* total) {

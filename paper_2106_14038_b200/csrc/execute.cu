@@ -12,6 +12,7 @@
 //   finalize()     after the stream drained: alive counts, counters, stats.
 #include <chrono>
 #include <cstring>
+#include <thread>
 
 #include "runtime.h"
 
@@ -39,6 +40,8 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
   CU(cudaMemsetAsync(s.heavy_cnt, 0, 16, s.st));
   CU(cudaMallocHost(&s.h_pin, 256 * sizeof(unsigned long long)));
+  CU(cudaMallocHost(&s.h_tab, sizeof(OutTab)));
+  TRY(dalloc(ctx, &s.d_tab, 1, s.st));
   s.epoch_next = 1;
   return GSMART_OK;
 }
@@ -52,11 +55,12 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
   dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
-  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2);
+  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2); dfree(st, s.d_tab);
   for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second.exec);
   s.graphs.clear();
   cudaStreamSynchronize(st);
   if (s.h_pin) cudaFreeHost(s.h_pin);
+  if (s.h_tab) cudaFreeHost(s.h_tab);
   if (s.ev) cudaEventDestroy(s.ev);
   if (s.own_stream) cudaStreamDestroy(s.st);
   (void)ctx;
@@ -488,15 +492,20 @@ struct Exec {
     return launch_expansion(true);
   }
 
-  gsmart_status run_phase1() {
+  // Run `body` (stream work on stable workspace addresses only) directly, or
+  // replay it from this slot's graph cache under `key` (captured on first use).
+  // Look-back epochs inside are offsets from the execute's base, so a replay is
+  // valid only if the body starts at the same offset as when it was captured.
+  template <typename Body>
+  gsmart_status run_cached(uint64_t key, uint32_t key_flags, Body&& body) {
     const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && ctx->world == 1;
-    if (!graphable) return phase1_kernels();
-    const uint32_t key_flags = flags & GSMART_NO_REFINE;
-    auto it = sl.graphs.find(plan->uid);
+    if (!graphable) return body();
+    auto it = sl.graphs.find(key);
     if (it != sl.graphs.end() && it->second.ws_gen == sl.ws_gen && it->second.lspm_gen == ctx->lspm_gen &&
         it->second.flags == key_flags) {
+      if (it->second.off0 != sl.seq_off) return body();  // e.g. after an expansion re-run
       CU(cudaGraphLaunch(it->second.exec, sl.st));
-      sl.seq_off = it->second.n_lb;
+      sl.seq_off += it->second.n_lb;
       graph_replayed = true;
       for (int i = 0; i < GSMART_NKERNELS; i++) launches[i] += it->second.launches[i];
       filter_main += it->second.filter_main;
@@ -506,12 +515,11 @@ struct Exec {
       cudaGraphExecDestroy(it->second.exec);
       sl.graphs.erase(it);
     }
-    // capture this plan's phase 1 once, then replay it (launch offsets relative to the epoch base)
     const uint32_t off0 = sl.seq_off;
     const std::vector<int> l0(launches, launches + GSMART_NKERNELS);
     const uint64_t fm0 = filter_main;
     CU(cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal));
-    gsmart_status s = phase1_kernels();
+    gsmart_status s = body();
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(sl.st, &graph);
     if (s != GSMART_OK) {
@@ -528,17 +536,23 @@ struct Exec {
     ge.ws_gen = sl.ws_gen;
     ge.lspm_gen = ctx->lspm_gen;
     ge.flags = key_flags;
+    ge.off0 = off0;
     ge.n_lb = sl.seq_off - off0;
     ge.launches.resize(GSMART_NKERNELS);
     for (int i = 0; i < GSMART_NKERNELS; i++) ge.launches[i] = launches[i] - l0[i];
     ge.filter_main = filter_main - fm0;
-    if (sl.graphs.size() >= 256) {  // bounded cache
+    if (sl.graphs.size() >= 512) {  // bounded cache
       for (auto& kv : sl.graphs) cudaGraphExecDestroy(kv.second.exec);
       sl.graphs.clear();
     }
-    sl.graphs[plan->uid] = ge;
+    sl.graphs[key] = ge;
     CU(cudaGraphLaunch(exec, sl.st));
     return GSMART_OK;
+  }
+
+  // phase 1 = seeds + grouped evaluation + expansion (graph key: uid, tag 0)
+  gsmart_status run_phase1() {
+    return run_cached(plan->uid << 3, flags & GSMART_NO_REFINE, [&] { return phase1_kernels(); });
   }
 
   gsmart_status start() {
@@ -645,21 +659,20 @@ struct Exec {
     return GSMART_OK;
   }
 
-  // ---- a8 prune + compaction, a9 rows + sort (async)
+  // ---- a8 prune + compaction, a9 rows + sort (async).  The device work reads its
+  // output pointers from the slot's OutTab (filled here per execute, copied to the
+  // device inside the work), so it replays from a per-plan graph like phase 1.
   gsmart_status phase2() {
     state = S_PHASE2;
-    // phase 1 wrote every counter: read them back with the rest of the stream
     static_assert(C_NCTR <= 64, "counter readback slots");
-    CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
-    ctr_pinned = true;
     TRY(keep_candidates());
     const uint64_t n_rows = F[L - 1];
     unsigned long long* dsz = sl.d_sz;
     R->levels.clear();
-    LevelTab pt;
-    memset(&pt, 0, sizeof pt);
     R->n_rows = n_rows;
     if (!n_rows) {
+      CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
+      ctr_pinned = true;
       for (uint32_t k = 0; k < L; k++) R->levels.push_back({plan->levels[k].var, 0, nullptr, nullptr});
       R->host_valid = (flags & GSMART_COUNT_ONLY) == 0;
       R->count_only = (flags & GSMART_COUNT_ONLY) != 0;
@@ -668,6 +681,10 @@ struct Exec {
     // one allocation owns the result's levels and rows (each part 256-B aligned)
     const uint32_t nc = (uint32_t)plan->vars.size();
     const bool want_rows = !(flags & GSMART_COUNT_ONLY);
+    enum { M_COUNT = 0, M_IDENTITY, M_SORT_SMALL, M_SORT_BIG };
+    const int mode = !want_rows ? M_COUNT
+                     : identity ? M_IDENTITY
+                                : (sort_small_ok(n_rows, nc) ? M_SORT_SMALL : M_SORT_BIG);
     auto al = [](uint64_t b) { return (b + 255) / 256 * 256; };
     uint64_t arena_bytes = 0;
     for (uint32_t k = 0; k < L; k++) arena_bytes += al(F[k] * 4) * (k > 0 ? 2 : 1);
@@ -679,35 +696,20 @@ struct Exec {
       arena += al(b);
       return p;
     };
-    prof.begin(K_PRUNE);
-    for (uint32_t k = L - 1; k >= 1; k--) {
-      CU(launch_prune_mark_d(sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
-                             ctx->sm_count, sl.st));
-      launches[K_PRUNE]++;
-    }
+    OutTab& ot = *sl.h_tab;
+    memset(&ot, 0, sizeof ot);
     for (uint32_t k = 0; k < L; k++) {
       gsmart_result::Lv lv{plan->levels[k].var, 0, nullptr, nullptr};
-      lv.bind = (uint32_t*)take(F[k] * 4);
-      if (k > 0) lv.parent = (uint32_t*)take(F[k] * 4);
-      CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind, k + 1 < L ? sl.lv[k].alive : nullptr,
-                                 dsz + k, k > 0 ? sl.lv[k - 1].newidx : nullptr, lv.parent, lv.bind,
-                                 k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), ctx->sm_count,
-                                 sl.st));
-      launches[K_PRUNE]++;
-      pt.parent[k] = lv.parent;
-      pt.bind[k] = lv.bind;
+      lv.bind = ot.bind[k] = (uint32_t*)take(F[k] * 4);
+      if (k > 0) lv.parent = ot.parent[k] = (uint32_t*)take(F[k] * 4);
       R->levels.push_back(lv);
     }
-    prof.end();
-    CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
+    size_t tb = 0;
     if (want_rows) {
-      std::vector<uint32_t> col_of_level(L);
-      for (uint32_t k = 0; k < L; k++) col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
-      uint32_t* out = (uint32_t*)take(n_rows * nc * 4);
-      uint32_t* rows = out;
-      size_t tb = 0;
-      if (!identity) {  // enumerate into slot scratch, then sort into the result
-        tb = sort_rows_tmp_bytes(n_rows, nc);
+      R->d_rows = (uint32_t*)take(n_rows * nc * 4);
+      ot.rows = ot.sorted = R->d_rows;
+      if (mode != M_IDENTITY) {  // enumerate into slot scratch, then sort into the result
+        tb = mode == M_SORT_SMALL ? SORT_SMALL_MAXN * 4 : sort_rows_tmp_bytes(n_rows, nc);
         const uint64_t need = al(n_rows * nc * 4) + al(tb);
         if (need > sl.p2_cap) {
           dfree(sl.st, sl.p2);
@@ -716,21 +718,61 @@ struct Exec {
           TRY(dalloc(ctx, &sl.p2, need + need / 4, sl.st));
           sl.p2_cap = need + need / 4;
         }
-        rows = (uint32_t*)sl.p2;
-      }
-      prof.begin(K_ENUMERATE);
-      CU(launch_enumerate(pt, L, col_of_level.data(), (uint32_t)n_rows, nc, rows, sl.st));
-      launches[K_ENUMERATE]++;
-      prof.end();
-      R->d_rows = out;
-      if (!identity) {  // otherwise trie order == lexicographic order in variable-index order
-        void* tmp = sl.p2 + al(n_rows * nc * 4);
-        prof.begin(K_SORT_ROWS);
-        CU(sort_rows(rows, R->d_rows, n_rows, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
-        prof.end();
+        ot.rows = (uint32_t*)sl.p2;
+        if (mode == M_SORT_SMALL) ot.rank = (uint32_t*)(sl.p2 + al(n_rows * nc * 4));
       }
     } else {
       R->count_only = true;
+    }
+    std::vector<uint32_t> col_of_level(L);
+    for (uint32_t k = 0; k < L; k++) col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
+    auto body = [&]() -> gsmart_status {
+      CU(cudaMemcpyAsync(sl.d_tab, sl.h_tab, sizeof(OutTab), cudaMemcpyHostToDevice, sl.st));
+      // phase 1 wrote every counter: read them back with the rest of the stream
+      CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
+      prof.begin(K_PRUNE);
+      for (uint32_t k = L - 1; k >= 1; k--) {
+        CU(launch_prune_mark_d(sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
+                               ctx->sm_count, sl.st));
+        launches[K_PRUNE]++;
+      }
+      for (uint32_t k = 0; k < L; k++) {
+        CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind,
+                                   k + 1 < L ? sl.lv[k].alive : nullptr, dsz + k,
+                                   k > 0 ? sl.lv[k - 1].newidx : nullptr, sl.d_tab, k,
+                                   k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), ctx->sm_count,
+                                   sl.st));
+        launches[K_PRUNE]++;
+      }
+      prof.end();
+      CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
+      if (mode != M_COUNT) {
+        prof.begin(K_ENUMERATE);
+        CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), dsz + 96 + (L - 1), nc, ctx->sm_count, sl.st));
+        launches[K_ENUMERATE]++;
+        prof.end();
+      }
+      if (mode == M_SORT_SMALL) {
+        prof.begin(K_SORT_ROWS);
+        CU(sort_rows_small(sl.d_tab, dsz + 96 + (L - 1), nc, sl.st, &launches[K_SORT_ROWS]));
+        prof.end();
+      }
+      return GSMART_OK;
+    };
+    TRY(run_cached((plan->uid << 3) | (uint64_t)(1 + mode), flags & GSMART_COUNT_ONLY, body));
+    ctr_pinned = true;
+    if (mode == M_SORT_BIG) {
+      // rows arrive in trie (pi-lexicographic) order: the longest tail of columns whose
+      // levels already increase needs no sort pass
+      std::vector<uint32_t> col_level(nc);
+      for (uint32_t k = 0; k < L; k++) col_level[col_of_level[k]] = k;
+      uint32_t n_key = nc - 1;  // columns [n_key, nc) have increasing levels
+      while (n_key > 0 && col_level[n_key - 1] < col_level[n_key]) n_key--;
+      void* tmp = sl.p2 + al(n_rows * nc * 4);
+      prof.begin(K_SORT_ROWS);
+      CU(sort_rows(ot.rows, R->d_rows, n_rows, nc, n_key, bits_for(ctx->N - 1), tmp, tb, sl.st,
+                   &launches[K_SORT_ROWS]));
+      prof.end();
     }
     return GSMART_OK;
   }
@@ -760,7 +802,7 @@ struct Exec {
         const size_t tb = sort_rows_tmp_bytes(total, nc);
         void* tmp = nullptr;
         TRY(sc.get((char**)&tmp, tb));
-        CU(sort_rows(all, sorted, total, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
+        CU(sort_rows(all, sorted, total, nc, nc, bits_for(ctx->N - 1), tmp, tb, sl.st, &launches[K_SORT_ROWS]));
         all = sorted;
       }
       R->d_rows = ctx->rank == 0 ? all : nullptr;  // rows live on rank 0
@@ -876,30 +918,40 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
     auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb).count(); };
     for (uint32_t i = 0; i < m; i++) st[i] = ex[i]->start();
     if (trace) fprintf(stderr, "[gsmart] %u plans: phase-1 launched at %.1f us\n", m, us());
-    // wait on each expansion readback; re-launch on overflow; then phase 2
-    bool pending = true;
-    while (pending) {
-      pending = false;
+    // serve the plans in completion order (a slow plan never holds back the
+    // host work of the others): expansion readback -> re-launch on overflow or
+    // phase 2; then, per drained stream, finalize
+    auto expanding = [&](uint32_t i) { return st[i] == GSMART_OK && ex[i]->state == Exec::S_EXPANDING; };
+    std::vector<uint8_t> done(m, 0);
+    for (uint32_t left = m; left;) {
+      bool progressed = false;
       for (uint32_t i = 0; i < m; i++) {
-        if (st[i] != GSMART_OK || ex[i]->state != Exec::S_EXPANDING) continue;
-        cudaError_t e = cudaEventSynchronize(ex[i]->sl.ev);
-        if (e != cudaSuccess) {
-          st[i] = cuda_fail(ctx, e, "expansion event", __LINE__);
-          continue;
+        if (done[i]) continue;
+        if (expanding(i)) {
+          const cudaError_t e = cudaEventQuery(ex[i]->sl.ev);
+          if (e == cudaErrorNotReady) continue;
+          progressed = true;
+          if (e != cudaSuccess) {
+            st[i] = cuda_fail(ctx, e, "expansion event", __LINE__);
+          } else {
+            if (trace) fprintf(stderr, "[gsmart]   plan %u expansion done at %.1f us\n", i, us());
+            st[i] = ex[i]->after_expand();
+            if (trace) fprintf(stderr, "[gsmart]   plan %u phase-2 launched at %.1f us\n", i, us());
+          }
+          continue;  // relaunched (still expanding) or phase 2 queued: drain later
         }
-        if (trace) fprintf(stderr, "[gsmart]   plan %u expansion done at %.1f us\n", i, us());
-        st[i] = ex[i]->after_expand();
-        if (trace) fprintf(stderr, "[gsmart]   plan %u phase-2 launched at %.1f us\n", i, us());
-        if (st[i] == GSMART_OK && ex[i]->state == Exec::S_EXPANDING) pending = true;
+        const cudaError_t e = cudaStreamQuery(ex[i]->sl.st);
+        if (e == cudaErrorNotReady) continue;
+        progressed = true;
+        if (trace) fprintf(stderr, "[gsmart]   plan %u drained at %.1f us\n", i, us());
+        if (e != cudaSuccess && st[i] == GSMART_OK) st[i] = cuda_fail(ctx, e, "execute sync", __LINE__);
+        if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
+        else ex[i]->prof.flush();
+        if (trace) fprintf(stderr, "[gsmart]   plan %u finalized at %.1f us\n", i, us());
+        done[i] = 1;
+        left--;
       }
-    }
-    for (uint32_t i = 0; i < m; i++) {
-      cudaError_t e = cudaStreamSynchronize(ex[i]->sl.st);
-      if (trace) fprintf(stderr, "[gsmart]   plan %u drained at %.1f us\n", i, us());
-      if (e != cudaSuccess && st[i] == GSMART_OK) st[i] = cuda_fail(ctx, e, "execute sync", __LINE__);
-      if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
-      else ex[i]->prof.flush();
-      if (trace) fprintf(stderr, "[gsmart]   plan %u finalized at %.1f us\n", i, us());
+      if (!progressed) std::this_thread::yield();
     }
     for (uint32_t i = 0; i < m; i++) {
       if (ex[i]->seq_open) end_seq(ex[i]->sl);  // epochs of a failed run are never reused

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restr
                                                         uint32_t chunk, uint32_t* __restrict__ ids, uint64_t cap,
                                                         unsigned long long* d_count, int* overflow, LBArgs lb,
                                                         uint32_t id_base) {
+  GSM_PDL_ENTRY();
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_p;
   __shared__ uint32_t s_tile;
@@ -197,7 +198,7 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
   const uint32_t chunk = bc_chunk_words(n_words, sm_count);
   const uint32_t nch = (n_words + chunk - 1) / chunk;
   if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
-  k_bitmap_compact<<<nch, BC_T, 0, st>>>(bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base);
+  pdl_launch(k_bitmap_compact, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base);
   return cudaGetLastError();
 }
 
@@ -207,6 +208,7 @@ constexpr int EX_T = 256, EX_I = 4, EX_TILE = EX_T * EX_I;  // expansion tile (e
 
 template <typename PT>
 __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
+  GSM_PDL_ENTRY();
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
@@ -272,6 +274,7 @@ constexpr uint32_t OFFCAP = 2048, TGTP = 1024, TGTC = 4;
 
 template <typename PT>
 __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
+  GSM_PDL_ENTRY();
   __shared__ uint32_t s_off[OFFCAP];
   __shared__ uint32_t s_tgt[TGTP * TGTC];
   __shared__ uint32_t s_tile, s_nlo, s_nhi;
@@ -387,21 +390,22 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
 
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 8;
-  if (pred_bytes == 1) k_seg_scan<uint8_t><<<g, SS_T, 0, st>>>(a);
-  else k_seg_scan<uint16_t><<<g, SS_T, 0, st>>>(a);
+  if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t>, g, SS_T, st, a);
+  else pdl_launch(k_seg_scan<uint16_t>, g, SS_T, st, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 6;
-  if (pred_bytes == 1) k_expand_lb<uint8_t><<<g, EX_T, 0, st>>>(a);
-  else k_expand_lb<uint16_t><<<g, EX_T, 0, st>>>(a);
+  if (pred_bytes == 1) pdl_launch(k_expand_lb<uint8_t>, g, EX_T, st, a);
+  else pdl_launch(k_expand_lb<uint16_t>, g, EX_T, st, a);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ a8 prune + compaction
 __global__ void k_prune_mark_d(const uint32_t* __restrict__ parent, const uint8_t* __restrict__ alive,
                                const unsigned long long* d_n, uint8_t* __restrict__ alive_prev) {
+  GSM_PDL_ENTRY();
   const uint64_t n = *d_n;
   for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < n; m += (uint64_t)gridDim.x * blockDim.x)
     if (!alive || alive[m]) alive_prev[__ldg(parent + m)] = 1;
@@ -409,7 +413,7 @@ __global__ void k_prune_mark_d(const uint32_t* __restrict__ parent, const uint8_
 
 cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
                                 uint8_t* alive_prev, int sm_count, cudaStream_t st) {
-  k_prune_mark_d<<<(unsigned)sm_count * 8, 256, 0, st>>>(parent, alive, d_n, alive_prev);
+  pdl_launch(k_prune_mark_d, (unsigned)sm_count * 8, 256, st, parent, alive, d_n, alive_prev);
   return cudaGetLastError();
 }
 
@@ -420,10 +424,12 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
                                                           const uint8_t* __restrict__ alive,
                                                           const unsigned long long* d_n,
                                                           const uint32_t* __restrict__ newidx_prev,
-                                                          uint32_t* __restrict__ out_parent,
-                                                          uint32_t* __restrict__ out_bind,
+                                                          const OutTab* __restrict__ ot, uint32_t k,
                                                           uint32_t* __restrict__ newidx,
                                                           unsigned long long* d_count, LBArgs lb) {
+  GSM_PDL_ENTRY();
+  uint32_t* __restrict__ out_parent = k ? ot->parent[k] : nullptr;
+  uint32_t* __restrict__ out_bind = ot->bind[k];
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
@@ -455,11 +461,11 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
 }
 
 cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
-                                    const unsigned long long* d_n, const uint32_t* newidx_prev, uint32_t* out_parent,
-                                    uint32_t* out_bind, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
+                                    const unsigned long long* d_n, const uint32_t* newidx_prev, const OutTab* ot,
+                                    uint32_t k, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
                                     int sm_count, cudaStream_t st) {
-  k_compact_alive_lb<<<(unsigned)sm_count * 8, CA_T, 0, st>>>(parent, bind, alive, d_n, newidx_prev, out_parent,
-                                                              out_bind, newidx, d_count, lb);
+  pdl_launch(k_compact_alive_lb, (unsigned)sm_count * 8, CA_T, st, parent, bind, alive, d_n, newidx_prev, ot, k,
+             newidx, d_count, lb);
   return cudaGetLastError();
 }
 

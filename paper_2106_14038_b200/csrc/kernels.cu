@@ -192,6 +192,7 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // =====================================================================================
 // all-ones over bits [0, n_bits), zero beyond (padding words included)
 __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
+  GSM_PDL_ENTRY();
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
     uint64_t lo = (uint64_t)w * 32;
     uint32_t v;
@@ -206,6 +207,7 @@ __global__ void k_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits) {
 // [0, n_bits) if bit s of ones_mask is set (no seed), else zero (seeded)
 __global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, uint32_t n_bits, uint32_t ones_mask,
                              InitExtra x) {
+  GSM_PDL_ENTRY();
   // first kernel of an execute: publish the look-back epoch base the host wrote to
   // pinned memory (a replayed graph thus needs no extra launch to set it) and zero
   // the execute's counters and size words (no memset nodes)
@@ -229,34 +231,36 @@ __global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, 
 
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,
                               uint32_t ones_mask, const InitExtra& x, cudaStream_t st) {
-  k_init_cands<<<grid_for((uint64_t)n_slots * stride_words, 256, 148 * 16), 256, 0, st>>>(
+  pdl_launch(k_init_cands, grid_for((uint64_t)n_slots * stride_words, 256, 148 * 16), 256, st,
       cand, n_slots, stride_words, n_bits, ones_mask, x);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st) {
-  k_fill_ones<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(bm, n_words, n_bits);
+  pdl_launch(k_fill_ones, grid_for(n_words, 256, 148 * 16), 256, st, bm, n_words, n_bits);
   return cudaGetLastError();
 }
 
 __global__ void k_and_inplace(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n_words) {
+  GSM_PDL_ENTRY();
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x)
     dst[w] &= __ldg(src + w);
 }
 
 cudaError_t launch_and_inplace(uint32_t* dst, const uint32_t* src, uint32_t n_words, cudaStream_t st) {
-  k_and_inplace<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(dst, src, n_words);
+  pdl_launch(k_and_inplace, grid_for(n_words, 256, 148 * 16), 256, st, dst, src, n_words);
   return cudaGetLastError();
 }
 
 __global__ void k_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag) {
+  GSM_PDL_ENTRY();
   if (*flag) return;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < n_words; w += (uint64_t)gridDim.x * blockDim.x)
     bm[w] = 0;
 }
 
 cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag, cudaStream_t st) {
-  k_zero_if_flag<<<grid_for(n_words, 256, 148 * 16), 256, 0, st>>>(bm, n_words, flag);
+  pdl_launch(k_zero_if_flag, grid_for(n_words, 256, 148 * 16), 256, st, bm, n_words, flag);
   return cudaGetLastError();
 }
 
@@ -265,6 +269,7 @@ cudaError_t launch_zero_if_flag(uint32_t* bm, uint64_t n_words, const int* flag,
 // =====================================================================================
 template <typename PT>
 __global__ void k_seed_scatter(SeedBatch sb, unsigned long long* ctr) {
+  GSM_PDL_ENTRY();
   // blockIdx.y = seed; every warp finds the label range itself (warp-cooperative
   // search, no CTA barrier)
   const uint32_t si = blockIdx.y;
@@ -318,20 +323,21 @@ cudaError_t launch_seed_scatter(const SeedBatch& sb, int pred_bytes, unsigned lo
                                 cudaStream_t st) {
   if (sb.n == 0) return cudaSuccess;
   const dim3 g(std::max<unsigned>((unsigned)sm_count * 4 / sb.n, (unsigned)sm_count), sb.n);
-  if (pred_bytes == 1) k_seed_scatter<uint8_t><<<g, 256, 0, st>>>(sb, ctr);
-  else k_seed_scatter<uint16_t><<<g, 256, 0, st>>>(sb, ctr);
+  if (pred_bytes == 1) pdl_launch(k_seed_scatter<uint8_t>, g, 256, st, sb, ctr);
+  else pdl_launch(k_seed_scatter<uint16_t>, g, 256, st, sb, ctr);
   return cudaGetLastError();
 }
 
 template <typename PT>
 __global__ void k_guard(Fmt<PT> f, uint32_t s, uint32_t l, uint32_t o, int* flag) {
+  GSM_PDL_ENTRY();
   if (!has_entry(f, s, l, o)) *flag = 0;
 }
 
 cudaError_t launch_guard(FmtAny f, int pred_bytes, uint32_t s, uint32_t label, uint32_t o, int* flag,
                          cudaStream_t st) {
-  if (pred_bytes == 1) k_guard<uint8_t><<<1, 1, 0, st>>>(fmt_of<uint8_t>(f), s, label, o, flag);
-  else k_guard<uint16_t><<<1, 1, 0, st>>>(fmt_of<uint16_t>(f), s, label, o, flag);
+  if (pred_bytes == 1) pdl_launch(k_guard<uint8_t>, 1, 1, st, fmt_of<uint8_t>(f), s, label, o, flag);
+  else pdl_launch(k_guard<uint16_t>, 1, 1, st, fmt_of<uint16_t>(f), s, label, o, flag);
   return cudaGetLastError();
 }
 
@@ -530,6 +536,7 @@ __device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row,
 
 template <typename PT>
 __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
+  GSM_PDL_ENTRY();
   constexpr uint32_t QCAP = 64;
   __shared__ uint32_t s_q[8][QCAP];  // per-warp queue of candidate rows (< 64)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -617,6 +624,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
 template <typename PT>
 __global__ void __launch_bounds__(256) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
                                                           const unsigned long long* __restrict__ d_nrows) {
+  GSM_PDL_ENTRY();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n = *d_nrows;
@@ -644,6 +652,7 @@ __global__ void __launch_bounds__(256) k_group_filter_rows(FilterArgsT<PT> a, co
 // heavy-row chunks: CTA per chunk, OR of satisfied edge bits into heavy_sat[slot]
 template <typename PT>
 __global__ void __launch_bounds__(256) k_filter_heavy(FilterArgsT<PT> a) {
+  GSM_PDL_ENTRY();
   __shared__ uint32_t s_sat;
   const uint32_t nch = a.heavy_count[1];
   for (uint32_t it = blockIdx.x; it < nch; it += gridDim.x) {
@@ -676,6 +685,7 @@ __global__ void __launch_bounds__(256) k_filter_heavy(FilterArgsT<PT> a) {
 // heavy-row state for the next launch (no host memsets between launches)
 template <typename PT>
 __global__ void k_filter_finalize(FilterArgsT<PT> a) {
+  GSM_PDL_ENTRY();
   const uint32_t nr = a.heavy_count[0];
   for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) {
     const uint32_t rec = a.heavy_rows[i];
@@ -717,20 +727,20 @@ template <typename PT>
 static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_t st, int* launches) {
   FilterArgsT<PT> t = to_t<PT>(a);
   if (a.rows) {  // candidate rows already compacted: perfectly balanced batches of 32 rows
-    k_group_filter_rows<PT><<<(unsigned)sm_count * 8, 256, 0, st>>>(t, a.rows, a.d_nrows);
+    pdl_launch(k_group_filter_rows<PT>, (unsigned)sm_count * 8, 256, st, t, a.rows, a.d_nrows);
   } else {
     // 8 warps per CTA; one 32-word chunk per warp, persistent (one wave)
     uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;
     unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 6);
-    k_group_filter<PT><<<g, 256, 0, st>>>(t);
+    pdl_launch(k_group_filter<PT>, g, 256, st, t);
   }
   if (launches) *launches += 1;
   if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
-    k_filter_heavy<PT><<<(unsigned)sm_count * 2, 256, 0, st>>>(t);
+    pdl_launch(k_filter_heavy<PT>, (unsigned)sm_count * 2, 256, st, t);
     if (launches) *launches += 1;
   }
   if (a.heavy) {  // clears failed heavy rows, resets the heavy counters
-    k_filter_finalize<PT><<<1, 1024, 0, st>>>(t);
+    pdl_launch(k_filter_finalize<PT>, 1, 1024, st, t);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
@@ -749,39 +759,53 @@ struct ColMap {
   uint32_t c[MAXL];
 };
 
-__global__ void k_enumerate(LevelTab t, uint32_t L, ColMap cm, uint32_t n_last, uint32_t n_cols,
-                            uint32_t* __restrict__ rows) {
+__global__ void k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
+                            const unsigned long long* __restrict__ d_n_last, uint32_t n_cols) {
+  GSM_PDL_ENTRY();
+  const uint32_t n_last = (uint32_t)*d_n_last;
+  uint32_t* __restrict__ rows = ot->rows;
+  uint32_t* __restrict__ rank = ot->rank;
   for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n_last; m += gridDim.x * blockDim.x) {
     uint32_t idx = m;
     uint32_t* r = rows + (uint64_t)m * n_cols;
     for (int k = (int)L - 1; k >= 0; k--) {
-      r[cm.c[k]] = __ldg(t.bind[k] + idx);
-      if (k > 0) idx = __ldg(t.parent[k] + idx);
+      r[cm.c[k]] = __ldg(ot->bind[k] + idx);
+      if (k > 0) idx = __ldg(ot->parent[k] + idx);
     }
+    if (rank && m < SORT_SMALL_MAXN) rank[m] = 0;  // the rank sort adds into it
   }
 }
 
-cudaError_t launch_enumerate(const LevelTab& tab, uint32_t n_levels, const uint32_t* col_of_level, uint32_t n_last,
-                             uint32_t n_cols, uint32_t* rows, cudaStream_t st) {
+cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
+                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st) {
   ColMap cm;
   for (uint32_t k = 0; k < MAXL; k++) cm.c[k] = k < n_levels ? col_of_level[k] : 0;
-  k_enumerate<<<grid_for(n_last, 256, 148 * 32), 256, 0, st>>>(tab, n_levels, cm, n_last, n_cols, rows);
+  pdl_launch(k_enumerate, (unsigned)sm_count * 16, 256, st, ot, n_levels, cm, d_n_last, n_cols);
   return cudaGetLastError();
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t n) {
+  GSM_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     v[i] = (uint32_t)i;
 }
 
-__global__ void k_gather_col(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
-                             uint32_t n_cols, uint32_t c, uint32_t* __restrict__ keys) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    keys[i] = rows[(uint64_t)perm[i] * n_cols + c];
+// key of up to 64 bits: columns [c0, c1) concatenated, most significant first
+__global__ void k_gather_key(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
+                             uint32_t n_cols, uint32_t c0, uint32_t c1, int key_bits,
+                             unsigned long long* __restrict__ keys) {
+  GSM_PDL_ENTRY();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* r = rows + (uint64_t)perm[i] * n_cols;
+    unsigned long long k = 0;
+    for (uint32_t c = c0; c < c1; c++) k = (k << key_bits) | r[c];
+    keys[i] = k;
+  }
 }
 
 __global__ void k_gather_rows(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
                               uint32_t n_cols, uint32_t* __restrict__ out) {
+  GSM_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * n_cols;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t r = i / n_cols, c = i - r * n_cols;
@@ -789,36 +813,105 @@ __global__ void k_gather_rows(const uint32_t* __restrict__ rows, const uint32_t*
   }
 }
 
-size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0, 32);
-  (void)n_cols;
-  return 4 * ((n * 4 + 255) / 256) * 256 + cub_bytes + 256;
+// Small results: rank sort.  rank(i) = #{j : row_j < row_i} is a permutation
+// (rows are distinct); the j range is split over gridDim.y CTAs whose partial
+// counts are added atomically (ot->rank was zeroed by the enumeration), then rows
+// are scattered to their ranks.  n is read from device memory, so the fixed grid
+// below is valid for any n <= SORT_SMALL_MAXN (CTAs past n exit at once).
+constexpr uint32_t SR_T = 256, SR_SMEM_W = 8192, SR_SPLIT = 32;
+static_assert((SORT_SMALL_MAXN / SR_SPLIT + 1) * SORT_SMALL_MAXC <= SR_SMEM_W, "rank-sort split fits smem");
+
+__global__ void __launch_bounds__(SR_T) k_rank_rows(const OutTab* __restrict__ ot,
+                                                   const unsigned long long* __restrict__ d_n, uint32_t nc) {
+  GSM_PDL_ENTRY();
+  __shared__ uint32_t s_rows[SR_SMEM_W];
+  const uint32_t n = (uint32_t)*d_n;
+  if (blockIdx.x * SR_T >= n) return;
+  const uint32_t* __restrict__ rows = ot->rows;
+  const uint32_t per = (n + gridDim.y - 1) / gridDim.y;
+  const uint32_t j0 = min(n, blockIdx.y * per), j1 = min(n, j0 + per);
+  for (uint32_t k = threadIdx.x; k < (j1 - j0) * nc; k += SR_T) s_rows[k] = rows[(uint64_t)j0 * nc + k];
+  __syncthreads();
+  const uint32_t i = blockIdx.x * SR_T + threadIdx.x;
+  if (i >= n || j1 == j0) return;
+  uint32_t me[SORT_SMALL_MAXC];
+#pragma unroll
+  for (uint32_t c = 0; c < SORT_SMALL_MAXC; c++) me[c] = c < nc ? rows[(uint64_t)i * nc + c] : 0u;
+  uint32_t cnt = 0;
+  for (uint32_t j = 0; j < j1 - j0; j++) {
+    const uint32_t* r = s_rows + j * nc;
+    int cmp = 0;  // sign of row_j - row_i
+#pragma unroll
+    for (uint32_t c = 0; c < SORT_SMALL_MAXC; c++) {
+      if (c >= nc || cmp) break;
+      const uint32_t x = r[c];
+      cmp = x < me[c] ? -1 : (x > me[c] ? 1 : 0);
+    }
+    cnt += cmp < 0;
+  }
+  if (cnt) atomicAdd(ot->rank + i, cnt);
 }
 
-// LSD radix over columns (stable), last column first.
-cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, int key_bits,
-                      void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches) {
-  size_t seg = ((n * 4 + 255) / 256) * 256;
+__global__ void k_scatter_rows(const OutTab* __restrict__ ot, const unsigned long long* __restrict__ d_n,
+                               uint32_t nc) {
+  GSM_PDL_ENTRY();
+  const uint32_t n = (uint32_t)*d_n;
+  const uint32_t* __restrict__ rows = ot->rows;
+  const uint32_t* __restrict__ rank = ot->rank;
+  uint32_t* __restrict__ out = ot->sorted;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < (uint64_t)n * nc;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(k / nc), c = (uint32_t)(k - (uint64_t)i * nc);
+    out[(uint64_t)rank[i] * nc + c] = rows[k];
+  }
+}
+
+cudaError_t sort_rows_small(const OutTab* ot, const unsigned long long* d_n, uint32_t n_cols, cudaStream_t st,
+                            int* launches) {
+  pdl_launch(k_rank_rows, dim3(SORT_SMALL_MAXN / SR_T, SR_SPLIT), SR_T, st, ot, d_n, n_cols);
+  pdl_launch(k_scatter_rows, 148 * 8, 256, st, ot, d_n, n_cols);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+// columns [0, n_key) in chunks of <= 64 key bits, least significant chunk first
+static int sort_chunk_cols(int key_bits) { return std::max(1, 64 / std::max(key_bits, 1)); }
+
+size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int64_t)n, 0, 64);
+  const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
+  return 2 * s4 + 2 * s8 + cub_bytes + 256;
+}
+
+// Lexicographic sort of distinct rows.  Only columns [0, n_key) need sorting: the
+// input order already sorts rows that agree on them (the caller derives n_key from
+// the trie order).  LSD over <= 64-bit keys of packed columns, stable.
+cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
+                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches) {
+  const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
   uint32_t* perm = (uint32_t*)tmp;
-  uint32_t* perm2 = (uint32_t*)((char*)tmp + seg);
-  uint32_t* keys = (uint32_t*)((char*)tmp + 2 * seg);
-  uint32_t* keys2 = (uint32_t*)((char*)tmp + 3 * seg);
-  void* ctmp = (char*)tmp + 4 * seg;
-  size_t cbytes = tmp_bytes - 4 * seg;
+  uint32_t* perm2 = (uint32_t*)((char*)tmp + s4);
+  unsigned long long* keys = (unsigned long long*)((char*)tmp + 2 * s4);
+  unsigned long long* keys2 = (unsigned long long*)((char*)tmp + 2 * s4 + s8);
+  void* ctmp = (char*)tmp + 2 * s4 + 2 * s8;
+  size_t cbytes = tmp_bytes - 2 * s4 - 2 * s8;
   unsigned g = grid_for(n, 256, 148 * 32);
-  k_iota<<<g, 256, 0, st>>>(perm, n);
+  pdl_launch(k_iota, g, 256, st, perm, n);
   int nl = 1;
-  for (int c = (int)n_cols - 1; c >= 0; c--) {
-    k_gather_col<<<g, 256, 0, st>>>(rows, perm, n, n_cols, (uint32_t)c, keys);
+  const int per = sort_chunk_cols(key_bits);
+  for (int c1 = (int)std::min(n_key, n_cols); c1 > 0; c1 -= per) {
+    const int c0 = std::max(0, c1 - per);
+    pdl_launch(k_gather_key, g, 256, st, rows, perm, n, n_cols, (uint32_t)c0, (uint32_t)c1, key_bits, keys);
     cudaError_t e = cub::DeviceRadixSort::SortPairs(ctmp, cbytes, keys, keys2, perm, perm2, (int64_t)n, 0,
-                                                    key_bits, st);
+                                                    (c1 - c0) * key_bits, st);
     if (e != cudaSuccess) return e;
     std::swap(perm, perm2);
     nl += 2;
   }
-  k_gather_rows<<<grid_for(n * n_cols, 256, 148 * 32), 256, 0, st>>>(rows, perm, n, n_cols, rows_out);
+  pdl_launch(k_gather_rows, grid_for(n * n_cols, 256, 148 * 32), 256, st, rows, perm, n, n_cols, rows_out);
   if (launches) *launches += nl + 1;
   return cudaGetLastError();
 }

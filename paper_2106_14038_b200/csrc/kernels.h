@@ -2,11 +2,30 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "device.cuh"
 
 namespace gsm {
+
+// Launch with programmatic stream serialization (see GSM_PDL_ENTRY): the kernel
+// must begin with GSM_PDL_ENTRY().  Inside a stream capture this becomes a
+// programmatic graph edge.
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ----------------------------------------------------------------- scans
 // Exclusive scan of n uint32 values (in may alias out).  Writes the 64-bit
@@ -167,17 +186,37 @@ cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cud
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
                                 uint8_t* alive_prev, int sm_count, cudaStream_t st);
+// Where phase 2 writes one execute's output.  Phase-2 kernels read these pointers
+// from a device copy of a table the host fills per execute, so a captured phase-2
+// graph writes into each result's own memory on every replay.
+struct OutTab {
+  uint32_t* parent[MAXL];  // compacted level k (parent index into level k-1), k >= 1
+  uint32_t* bind[MAXL];    // compacted level k bindings
+  uint32_t* rows;          // enumeration output [n_rows x n_cols]
+  uint32_t* sorted;        // rank-sort output (rows sorted lexicographically)
+  uint32_t* rank;          // rank-sort scratch [SORT_SMALL_MAXN], zeroed by the enumeration
+};
+constexpr uint32_t SORT_SMALL_MAXN = 8192, SORT_SMALL_MAXC = 16;
+
 cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,
-                                    const unsigned long long* d_n, const uint32_t* newidx_prev, uint32_t* out_parent,
-                                    uint32_t* out_bind, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
+                                    const unsigned long long* d_n, const uint32_t* newidx_prev, const OutTab* ot,
+                                    uint32_t k, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
                                     int sm_count, cudaStream_t st);
 
 // ----------------------------------------------------------------- a8 prune, a9 rows
-cudaError_t launch_enumerate(const LevelTab& tab, uint32_t n_levels, const uint32_t* col_of_level,
-                             uint32_t n_last, uint32_t n_cols, uint32_t* rows, cudaStream_t st);
+// one row per leaf; n_last read from device memory (grid-stride)
+cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
+                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st);
+// rank sort of ot->rows into ot->sorted for n (device) <= SORT_SMALL_MAXN, n_cols <= SORT_SMALL_MAXC
+inline bool sort_small_ok(uint64_t n, uint32_t n_cols) { return n <= SORT_SMALL_MAXN && n_cols <= SORT_SMALL_MAXC; }
+cudaError_t sort_rows_small(const OutTab* ot, const unsigned long long* d_n, uint32_t n_cols, cudaStream_t st,
+                            int* launches);
 size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols);
-// rows: [n x n_cols] uint32, sorted lexicographically into rows_out
-cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, int key_bits,
-                      void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches);
+// rows: [n x n_cols] uint32, distinct, sorted lexicographically into rows_out
+// (packed-key LSD radix passes).
+// The input must already be ordered on columns [n_key, n_cols) among rows that
+// agree on [0, n_key) (n_key = n_cols: no assumption).
+cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
+                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches);
 
 }  // namespace gsm

@@ -72,6 +72,8 @@ struct Slot {
   uint64_t frows_cap = 0;
   uint32_t* cand = nullptr;            // candidate bitmaps of the running plan (stable for graph replay)
   uint64_t cand_words = 0;
+  OutTab* h_tab = nullptr;             // pinned: this execute's phase-2 output pointers
+  OutTab* d_tab = nullptr;             // device copy (copied inside the phase-2 work)
   char* p2 = nullptr;                  // phase-2 scratch (unsorted rows + sort temp), grow-only
   uint64_t p2_cap = 0;
   uint32_t* d_epoch = nullptr;         // device base epoch of the current launch sequence
@@ -80,11 +82,11 @@ struct Slot {
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     uint64_t ws_gen = 0, lspm_gen = 0;
-    uint32_t flags = 0, n_lb = 0;
+    uint32_t flags = 0, n_lb = 0, off0 = 0;
     std::vector<int> launches;  // kernel launches inside the graph, per kernel class
     uint64_t filter_main = 0;
   };
-  std::unordered_map<uint64_t, GraphEntry> graphs;  // plan uid -> captured phase 1
+  std::unordered_map<uint64_t, GraphEntry> graphs;  // (plan uid << 3 | phase tag) -> captured work
 };
 
 }  // namespace gsm

@@ -21,3 +21,14 @@ for rep in range(4):
         G.gsmart_result_free(r)
         if rep == 3:
             print(f"    python wall {1e6*(t1-t0):.1f} us", file=sys.stderr, flush=True)
+# the bench step: all queries in one gsmart_execute_batch
+for rep in range(4):
+    if rep == 3:
+        print("--- batch", file=sys.stderr, flush=True)
+    t0 = time.perf_counter()
+    rs = G.gsmart_execute_batch(e.ctx, plans, G.GSMART_KEEP_ON_DEVICE)
+    t1 = time.perf_counter()
+    for r in rs:
+        G.gsmart_result_free(r)
+    if rep == 3:
+        print(f"    python wall {1e6*(t1-t0):.1f} us", file=sys.stderr, flush=True)

@@ -144,6 +144,34 @@ def test_skewed_graphs_vs_oracle(G, eng, seed, N, P, M, skew):
 
 
 # ------------------------------------------------------------------ LUBM-shaped
+def _relabel(q, perm):
+    """The same query with vertex i renamed perm[i] (changes the output column order)."""
+    inv = {old: new for new, old in enumerate(perm)}
+    verts = [q.vertices[perm[i]] for i in range(q.n_vertices)]
+    edges = [(inv[s], pr, inv[o]) for s, pr, o in q.edges]
+    return Query(verts, edges, name=q.name + "_perm")
+
+
+@pytest.mark.parametrize("U", [10])
+def test_permuted_column_order_sorts(G, eng, U):
+    """Relabelled variables make the trie order differ from the column order, so
+    rows go through the sort: the one-CTA path for small results and the packed-key
+    LSD path (with the already-ordered tail columns skipped) for large ones."""
+    d = lubm.generate(U)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    sizes = []
+    for q in lubm.queries(d):
+        for perm in (list(range(q.n_vertices))[::-1], list(range(1, q.n_vertices)) + [0]):
+            qp = _relabel(q, perm)
+            exp = ix.query(qp)
+            got = eng.query(qp)
+            assert got.shape == exp.shape and np.array_equal(got, exp), (qp.name, perm)
+            sizes.append(len(exp))
+    assert max(sizes) > 4096 and any(0 < n <= 4096 for n in sizes)  # both sort paths ran
+
+
 @pytest.mark.parametrize("U", [1, 10, 100])
 def test_lubm_queries_vs_oracle(G, eng, U):
     d = lubm.generate(U)
