@@ -273,47 +273,73 @@ __global__ void k_seed_scatter(SeedBatch sb, unsigned long long* ctr) {
   // blockIdx.y = seed; every warp finds the label range itself (warp-cooperative
   // search, no CTA barrier)
   const uint32_t si = blockIdx.y;
-  const Fmt<PT> f = fmt_of<PT>(sb.f[sb.dir[si]]);
-  const uint32_t c = sb.c[si], l = sb.label[si];
-  uint32_t* __restrict__ bits = sb.bits[si];
+  uint32_t dir = 0, c = 0, l = 0;
+  uint32_t* bits = nullptr;
+#pragma unroll
+  for (uint32_t i = 0; i < MAX_SEEDS; i++)  // constant offsets into the parameter block
+    if (i == si) {
+      dir = sb.dir[i];
+      c = sb.c[i];
+      l = sb.label[i];
+      bits = sb.bits[i];
+    }
+  const Fmt<PT> f = fmt_of<PT>(dir ? sb.f[1] : sb.f[0]);
   uint32_t lo, hi;
   warp_label_range(f, c, l, lo, hi);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ctr + C_SEED, (unsigned long long)(hi - lo));
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   __shared__ uint32_t s_words[8][32];  // per-warp window of 32 bitmap words
-  // a warp takes 128 consecutive (sorted) entries: lane i reads entries 4i..4i+3.
-  // If they span < 32 words, bits are OR-ed into a shared window and written with
-  // one atomicOr per non-zero word; else per-entry warp-aggregated atomics.
-  for (uint32_t base = lo + warp * 128; base < hi; base += nwarps * 128) {
-    uint32_t id[4];
-    bool v[4];
+  // A warp takes SEED_R rounds of 128 consecutive (sorted) entries, rounds strided by
+  // the grid (small ranges still spread over all warps), all loads issued before
+  // any is used (SEED_R x 512 B in flight per warp); in a round lane i holds
+  // entries 4i..4i+3.  If a round spans < 32 words, its bits are OR-ed into a shared
+  // window and written with one atomicOr per non-zero word; else per-entry
+  // warp-aggregated atomics.
+  constexpr int SEED_R = 4;
+  const uint64_t stride = (uint64_t)nwarps * 128;
+  for (uint64_t base0 = lo + (uint64_t)warp * 128; base0 < hi; base0 += stride * SEED_R) {
+    uint32_t id[SEED_R][4];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint32_t k = base + lane * 4 + j;
-      v[j] = k < hi;
-      id[j] = v[j] ? __ldg(f.col + k) : 0u;
-    }
-    const uint32_t w_first = __shfl_sync(GSM_FULL, id[0], 0) >> 5;
-    const uint32_t last_k = min(hi, base + 128) - 1 - base;
-    const uint32_t w_last = __shfl_sync(GSM_FULL, id[last_k & 3], last_k >> 2) >> 5;
-    if (w_last - w_first < 32) {
-      s_words[wib][lane] = 0;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (v[j]) atomicOr(&s_words[wib][(id[j] >> 5) - w_first], 1u << (id[j] & 31));
-      __syncwarp();
-      const uint32_t x = s_words[wib][lane];
-      if (x) atomicOr(bits + w_first + lane, x);
-      __syncwarp();
-    } else {
+    for (int r = 0; r < SEED_R; r++)
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const uint32_t word = v[j] ? (id[j] >> 5) : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(GSM_FULL, word);
-        const uint32_t orv = __reduce_or_sync(peers, v[j] ? (1u << (id[j] & 31)) : 0u);
-        if (v[j] && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
+        const uint64_t k = base0 + r * stride + lane * 4 + j;
+        id[r][j] = k < hi ? __ldg(f.col + k) : 0u;
+      }
+#pragma unroll
+    for (int r = 0; r < SEED_R; r++) {
+      const uint64_t base64 = base0 + r * stride;
+      if (base64 >= hi) break;
+      const uint32_t base = (uint32_t)base64;
+      bool v[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = base + lane * 4 + j < hi;
+      const uint32_t w_first = __shfl_sync(GSM_FULL, id[r][0], 0) >> 5;
+      const uint32_t last_k = min(hi, base + 128) - 1 - base;
+      uint32_t idl = id[r][0];
+#pragma unroll
+      for (int j = 1; j < 4; j++)
+        if ((last_k & 3) == (uint32_t)j) idl = id[r][j];
+      const uint32_t w_last = __shfl_sync(GSM_FULL, idl, last_k >> 2) >> 5;
+      if (w_last - w_first < 32) {
+        s_words[wib][lane] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (v[j]) atomicOr(&s_words[wib][(id[r][j] >> 5) - w_first], 1u << (id[r][j] & 31));
+        __syncwarp();
+        const uint32_t x = s_words[wib][lane];
+        if (x) atomicOr(bits + w_first + lane, x);
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t word = v[j] ? (id[r][j] >> 5) : 0xffffffffu;
+          const uint32_t peers = __match_any_sync(GSM_FULL, word);
+          const uint32_t orv = __reduce_or_sync(peers, v[j] ? (1u << (id[r][j] & 31)) : 0u);
+          if (v[j] && (int)lane == __ffs(peers) - 1) atomicOr(bits + word, orv);
+        }
       }
     }
   }
@@ -322,7 +348,7 @@ __global__ void k_seed_scatter(SeedBatch sb, unsigned long long* ctr) {
 cudaError_t launch_seed_scatter(const SeedBatch& sb, int pred_bytes, unsigned long long* ctr, int sm_count,
                                 cudaStream_t st) {
   if (sb.n == 0) return cudaSuccess;
-  const dim3 g(std::max<unsigned>((unsigned)sm_count * 4 / sb.n, (unsigned)sm_count), sb.n);
+  const dim3 g((unsigned)sm_count * 4, sb.n);
   if (pred_bytes == 1) pdl_launch(k_seed_scatter<uint8_t>, g, 256, st, sb, ctr);
   else pdl_launch(k_seed_scatter<uint16_t>, g, 256, st, sb, ctr);
   return cudaGetLastError();
@@ -444,7 +470,7 @@ __device__ __forceinline__ uint32_t short_row_u8(const FilterArgsT<PT>& a, const
 
 // Evaluate the group's edges of one direction set for 32 candidate rows, one per
 // lane (lanes with has == false idle).  Returns per-lane "all edges satisfied".
-template <typename PT>
+template <typename PT, bool SIMD>
 __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32_t row, const bool has,
                                           const uint32_t lane, unsigned long long& n_rows,
                                           unsigned long long& n_scanned, uint32_t& n_matched) {
@@ -473,7 +499,7 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
         sat = need;
       } else if (len > SHORT_ROW) {
         medium = true;
-      } else if (sizeof(PT) == 1 && (a.variant & 1)) {
+      } else if constexpr (SIMD) {
         sat = short_row_u8(a, d, row, b, e, need, n_scanned, n_matched);
       } else {
         // 4 entries per step: their pred loads, then col loads, then bitmap probes
@@ -534,7 +560,7 @@ __device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row,
   if (fail && (int)lane == __ffs(peers) - 1) atomicAnd(cand + word, ~bits);
 }
 
-template <typename PT>
+template <typename PT, bool SIMD>
 __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   GSM_PDL_ENTRY();
   constexpr uint32_t QCAP = 64;
@@ -592,7 +618,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
         if (lane + 32 < qn) q[lane] = extra;
         qn -= 32;
         __syncwarp();
-        const bool ok = eval_rows(a, row, true, lane, n_rows, n_scanned, n_matched);
+        const bool ok = eval_rows<PT, SIMD>(a, row, true, lane, n_rows, n_scanned, n_matched);
         clear_failed(a.cand, row, !ok, lane);
       }
     }
@@ -600,7 +626,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   if (qn) {
     const bool has = lane < qn;
     const uint32_t row = has ? q[lane] : 0u;
-    const bool ok = eval_rows(a, row, has, lane, n_rows, n_scanned, n_matched);
+    const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched);
     clear_failed(a.cand, row, has && !ok, lane);
   }
   // one atomic per warp per counter
@@ -621,8 +647,8 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
 // takes batches of 32 consecutive ids, one row per lane, so dense and sparse
 // candidate sets alike spread over all warps of the GPU (no per-chunk serial
 // batches), then failed rows are cleared in the center's bitmap.
-template <typename PT>
-__global__ void __launch_bounds__(256) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
+template <typename PT, bool SIMD>
+__global__ void __launch_bounds__(256, 6) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
                                                           const unsigned long long* __restrict__ d_nrows) {
   GSM_PDL_ENTRY();
   const uint32_t lane = threadIdx.x & 31;
@@ -633,7 +659,7 @@ __global__ void __launch_bounds__(256) k_group_filter_rows(FilterArgsT<PT> a, co
   for (uint64_t base = (uint64_t)warp * 32; base < n; base += (uint64_t)nwarps * 32) {
     const bool has = base + lane < n;
     const uint32_t row = has ? __ldg(rows + base + lane) : 0u;
-    const bool ok = eval_rows(a, row, has, lane, n_rows, n_scanned, n_matched);
+    const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched);
     clear_failed(a.cand, row, has && !ok, lane);
   }
 #pragma unroll
@@ -726,13 +752,17 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
 template <typename PT>
 static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_t st, int* launches) {
   FilterArgsT<PT> t = to_t<PT>(a);
+  const bool simd = sizeof(PT) == 1 && (a.variant & 1);  // byte-SIMD short rows (opt-in)
   if (a.rows) {  // candidate rows already compacted: perfectly balanced batches of 32 rows
-    pdl_launch(k_group_filter_rows<PT>, (unsigned)sm_count * 8, 256, st, t, a.rows, a.d_nrows);
+    const unsigned g = (unsigned)sm_count * 6;  // one resident wave (<= 40 registers)
+    if (simd) pdl_launch(k_group_filter_rows<PT, true>, g, 256, st, t, a.rows, a.d_nrows);
+    else pdl_launch(k_group_filter_rows<PT, false>, g, 256, st, t, a.rows, a.d_nrows);
   } else {
     // 8 warps per CTA; one 32-word chunk per warp, persistent (one wave)
     uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;
     unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)sm_count * 6);
-    pdl_launch(k_group_filter<PT>, g, 256, st, t);
+    if (simd) pdl_launch(k_group_filter<PT, true>, g, 256, st, t);
+    else pdl_launch(k_group_filter<PT, false>, g, 256, st, t);
   }
   if (launches) *launches += 1;
   if (a.heavy) {  // only when a scanned format has rows > HEAVY_ROW entries
