@@ -417,7 +417,7 @@ cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, co
   return cudaGetLastError();
 }
 
-constexpr int CA_T = 256, CA_I = 4, CA_TILE = CA_T * CA_I;
+constexpr int CA_T = 256, CA_I = 8, CA_TILE = CA_T * CA_I;
 
 __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __restrict__ parent,
                                                           const uint32_t* __restrict__ bind,
