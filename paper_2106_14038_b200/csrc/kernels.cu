@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
 // candidate sets alike spread over all warps of the GPU (no per-chunk serial
 // batches), then failed rows are cleared in the center's bitmap.
 template <typename PT, bool SIMD>
-__global__ void __launch_bounds__(256, 6) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
                                                           const unsigned long long* __restrict__ d_nrows) {
   GSM_PDL_ENTRY();
   const uint32_t lane = threadIdx.x & 31;
@@ -754,9 +754,9 @@ static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_
   FilterArgsT<PT> t = to_t<PT>(a);
   const bool simd = sizeof(PT) == 1 && (a.variant & 1);  // byte-SIMD short rows (opt-in)
   if (a.rows) {  // candidate rows already compacted: perfectly balanced batches of 32 rows
-    const unsigned g = (unsigned)sm_count * 6;  // one resident wave (<= 40 registers)
-    if (simd) pdl_launch(k_group_filter_rows<PT, true>, g, 256, st, t, a.rows, a.d_nrows);
-    else pdl_launch(k_group_filter_rows<PT, false>, g, 256, st, t, a.rows, a.d_nrows);
+    // one resident wave: 6 CTAs/SM at <= 40 registers (4 for the SIMD variant)
+    if (simd) pdl_launch(k_group_filter_rows<PT, true>, (unsigned)sm_count * 4, 256, st, t, a.rows, a.d_nrows);
+    else pdl_launch(k_group_filter_rows<PT, false>, (unsigned)sm_count * 6, 256, st, t, a.rows, a.d_nrows);
   } else {
     // 8 warps per CTA; one 32-word chunk per warp, persistent (one wave)
     uint64_t want = (((uint64_t)a.n_words + 31) / 32 + 7) / 8;
