@@ -39,6 +39,13 @@ UNIT = "edges/s"
 WORKLOAD = "LUBM-100 (configs[1]): L1-L7 + Q14 batch, 1 B200"
 
 
+def workload_name(U):
+    if U == 100:
+        return WORKLOAD
+    tag = "configs[3]" if U == 10000 else "LUBM-shaped"
+    return f"LUBM-{U} ({tag}): L1-L7 + Q14 batch, 1 B200"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -143,8 +150,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_class):
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def ncu_traffic(kernel_class, U=100):
+    """DRAM bytes per launch of a kernel class from the committed ncu capture of
+    the same workload (profiles/ncu_traffic.json is LUBM-100; other sizes use
+    profiles/ncu_traffic_u<U>.json when one was captured, else null)."""
+    name = "ncu_traffic.json" if U == 100 else f"ncu_traffic_u{U}.json"
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -186,7 +197,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "queries": [q.name for q in qs], "triples": int(len(s)),
+            "config": {"workload": workload_name(args.universities), "queries": [q.name for q in qs], "triples": int(len(s)),
                        "edges_per_step": int(sum(E))},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": "full LUBM-100 query batch per step (oracle index build excluded)"},
@@ -293,6 +304,9 @@ def main():
             G.gsmart_result_free(r)
     torch.cuda.synchronize()
     ksum, kbytes, klaunch = {}, {}, {}
+    # SURVEY §8(d)'s implementation-side count: LSpM entries the GPU path read
+    # whose label matched (seed + filter + expansion device counters), per batch
+    edges_read = sum(st["edges_evaluated"] for st in prof_stats) / max(1, args.steps)
     for st in prof_stats:
         for k, v in st["ms_kernel"].items():
             ksum[k] = ksum.get(k, 0.0) + v
@@ -305,9 +319,9 @@ def main():
     peak, peak_src = peaks()
     roofline = None
     if dom:
-        n_launch = max(1, klaunch[dom] // (3 if dom == "group_filter" else 1))
+        n_launch = max(1, klaunch[dom])
         achieved = kbytes[dom] / (ksum[dom] / 1000) / 1e9
-        traffic = ncu_traffic(dom)
+        traffic = ncu_traffic(dom, args.universities)
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": kbytes[dom] / n_launch,
@@ -361,9 +375,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "universities": args.universities, "triples": int(len(s_h)),
+            "config": {"workload": workload_name(args.universities), "universities": args.universities, "triples": int(len(s_h)),
                        "entities": d.n_entities, "queries": [q.name for q in qs],
-                       "edges_per_step": int(sum(E)), "l2": "flushed between timed steps (256 MiB write)",
+                       "edges_per_step": int(sum(E)), "edges_read_per_step": int(edges_read),
+                       "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": ("partitioned" if partitioned else "replicas") if world > 1 else "single"},
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(3 * 4 * len(s_h)),

@@ -118,8 +118,9 @@ const char* gsmart_last_error(const gsmart_ctx* ctx);
 
 /* Copy n triples (s[i], p[i], o[i]) into device memory owned by ctx
  * (§6.2.1 steps 1-2 input: encoded ids).  flags: GSMART_PTR_HOST or
- * GSMART_PTR_DEVICE for where s/p/o live.  Ids are validated (s,o <
- * n_entities, 1 <= p <= n_predicates) -> GSMART_E_INVALID_ARG.  Replaces any
+ * GSMART_PTR_DEVICE for where s/p/o live.  Ids are validated on the device
+ * after the copy (s,o < n_entities, 1 <= p <= n_predicates) ->
+ * GSMART_E_INVALID_ARG with no triples loaded (build then gives E_STATE).  Replaces any
  * previously loaded triples and invalidates the LSpM.  n may be 0.
  * n_entities < 2^31, n_predicates <= 65535. */
 gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s, const uint32_t* p,
@@ -148,6 +149,11 @@ typedef struct {
   const uint32_t* row_ptr;  /* [n_rows + 1] */
   const uint32_t* col;      /* [nnz] */
   const void* pred;         /* [nnz] uint8 or uint16 */
+  /* [n_rows] row label signatures: bit (l & 31) set iff the row holds an entry
+   * whose label l' has (l' & 31) == (l & 31).  Eqs. 4/5 evaluated
+   * for every label at once; exact presence when n_predicates <= 32, else a
+   * necessary condition.  The group filter tests it before reading a row. */
+  const uint32_t* label_mask;
 } gsmart_lspm_view;
 gsmart_status gsmart_lspm_get(const gsmart_ctx* ctx, uint32_t format, gsmart_lspm_view* out);
 

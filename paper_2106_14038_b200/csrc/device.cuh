@@ -17,7 +17,7 @@ constexpr uint32_t EXP_CHUNK = 256;    // expansion work item = <= 256 segment e
 
 // counters (uint64) in the ctx stats array
 enum Ctr { C_FILTER_ROWS = 0, C_FILTER_SCANNED, C_FILTER_MATCHED, C_SEED, C_EXPAND, C_CLOSING,
-           C_HEAVY, C_NCTR };
+           C_HEAVY, C_FILTER_MASKED, C_NCTR };
 
 // One LSpM format on the device: entries of row r are [rp[r], rp[r+1]) sorted by (pred, col).
 template <typename PT>
@@ -25,7 +25,13 @@ struct Fmt {
   const uint32_t* __restrict__ rp;
   const uint32_t* __restrict__ col;
   const PT* __restrict__ pred;
+  // label signature of every row: bit (l & 31) set iff the row holds an entry
+  // with a label l' where (l' & 31) == (l & 31) — Eqs. 4/5's "row has label l"
+  // for all labels at once (exact when P <= 32, a necessary condition beyond)
+  const uint32_t* __restrict__ lmask;
 };
+
+__host__ __device__ __forceinline__ uint32_t label_bit(uint32_t l) { return 1u << (l & 31u); }
 
 __device__ __forceinline__ uint32_t bit_of(const uint32_t* __restrict__ bm, uint32_t i) {
   return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;

@@ -581,6 +581,7 @@ struct Exec {
       fa[d].rp = ctx->f[d].rp;
       fa[d].col = ctx->f[d].col;
       fa[d].pred = ctx->f[d].pred;
+      fa[d].lmask = ctx->f[d].lmask;
     }
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].closing.size() > (size_t)MAXC)
@@ -838,7 +839,7 @@ struct Exec {
     const uint64_t pb = (uint64_t)ctx->pred_bytes;
     // algorithmic bytes: what each step must move
     uint64_t parents = 0, children = 0;
-    st.bytes[K_FILTER] = 8 * c[C_FILTER_ROWS] + pb * c[C_FILTER_SCANNED] + 4 * c[C_FILTER_MATCHED] +
+    st.bytes[K_FILTER] = 4 * c[C_FILTER_MASKED] + 8 * c[C_FILTER_ROWS] + pb * c[C_FILTER_SCANNED] + 4 * c[C_FILTER_MATCHED] +
                          8ull * filter_main * W;
     st.bytes[K_SEED] = 4 * c[C_SEED];
     for (uint32_t k = 0; k + 1 < st.n_levels && k + 1 < GSMART_MAX_LEVELS; k++) parents += st.level_nodes[k];

@@ -187,6 +187,44 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
   return cudaGetLastError();
 }
 
+// One thread per row.  Entries are sorted by label, so a row's label set is
+// walked label by label: short rows linearly, long rows by jumping to the
+// first entry past the current label (binary search) — O(#labels · log len)
+// even for hub rows.
+template <typename PT>
+__global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restrict__ pred, uint32_t n_rows,
+                             uint32_t* __restrict__ lmask) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+    uint32_t k = rp[r];
+    const uint32_t e = rp[r + 1];
+    uint32_t m = 0;
+    if (e - k <= 16) {
+      for (; k < e; k++) m |= label_bit(pred[k]);
+    } else {
+      while (k < e) {
+        const uint32_t l = pred[k];
+        m |= label_bit(l);
+        uint32_t lo = k + 1, hi = e;  // first entry with label > l
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if ((uint32_t)pred[mid] <= l) lo = mid + 1;
+          else hi = mid;
+        }
+        k = lo;
+      }
+    }
+    lmask[r] = m;
+  }
+}
+
+cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
+                              uint32_t* lmask, cudaStream_t st) {
+  const unsigned g = grid_for(n_rows, 256, 148 * 16);
+  if (pred_bytes == 1) k_label_mask<uint8_t><<<g, 256, 0, st>>>(rp, (const uint8_t*)pred, n_rows, lmask);
+  else k_label_mask<uint16_t><<<g, 256, 0, st>>>(rp, (const uint16_t*)pred, n_rows, lmask);
+  return cudaGetLastError();
+}
+
 // =====================================================================================
 // bitmaps
 // =====================================================================================
@@ -384,6 +422,7 @@ struct FilterArgsT {
   GEdge e[2][MAXG];
   uint32_t ne[2];
   uint32_t minl[2], maxl[2];
+  uint32_t needm[2];  // OR of label_bit() over the direction's edges
   uint32_t* cand;
   uint32_t n_words;
   uint32_t* heavy_rows;
@@ -470,11 +509,33 @@ __device__ __forceinline__ uint32_t short_row_u8(const FilterArgsT<PT>& a, const
 
 // Evaluate the group's edges of one direction set for 32 candidate rows, one per
 // lane (lanes with has == false idle).  Returns per-lane "all edges satisfied".
-template <typename PT, bool SIMD>
+// Label pre-test (Eqs. 4/5 over the row label signatures): a row lacking one of
+// the group's labels fails without touching row_ptr, labels or columns.
+template <typename PT>
+__device__ __forceinline__ bool label_pretest(const FilterArgsT<PT>& a, const uint32_t row, uint32_t& n_masked) {
+  uint32_t m[2] = {~0u, ~0u};
+#pragma unroll
+  for (int d = 0; d < 2; d++)
+    if (a.ne[d] && a.f[d].lmask) {
+      m[d] = __ldg(a.f[d].lmask + row);
+      n_masked++;
+    }
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < 2; d++) ok = ok && (m[d] & a.needm[d]) == a.needm[d];
+  return ok;
+}
+
+// PRE: the caller already ran label_pretest (has == passed)
+template <typename PT, bool SIMD, bool PRE = false>
 __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32_t row, const bool has,
                                           const uint32_t lane, unsigned long long& n_rows,
-                                          unsigned long long& n_scanned, uint32_t& n_matched) {
+                                          unsigned long long& n_scanned, uint32_t& n_matched,
+                                          uint32_t& n_masked) {
   bool ok = has;
+  if constexpr (!PRE) {
+    if (ok) ok = label_pretest(a, row, n_masked);
+  }
 #pragma unroll
   for (int d = 0; d < 2; d++) {
     if (a.ne[d] == 0) continue;
@@ -569,7 +630,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   uint32_t* q = s_q[wib];
   unsigned long long n_rows = 0, n_scanned = 0;
-  uint32_t n_matched = 0;
+  uint32_t n_matched = 0, n_masked = 0;
   // A warp streams chunks of 32 bitmap words (1024 rows; one coalesced load,
   // next chunk prefetched), queues the candidate rows (set bits, ascending) and
   // evaluates them 32 at a time, one row per lane: sparse candidate sets keep
@@ -618,7 +679,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
         if (lane + 32 < qn) q[lane] = extra;
         qn -= 32;
         __syncwarp();
-        const bool ok = eval_rows<PT, SIMD>(a, row, true, lane, n_rows, n_scanned, n_matched);
+        const bool ok = eval_rows<PT, SIMD>(a, row, true, lane, n_rows, n_scanned, n_matched, n_masked);
         clear_failed(a.cand, row, !ok, lane);
       }
     }
@@ -626,7 +687,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   if (qn) {
     const bool has = lane < qn;
     const uint32_t row = has ? q[lane] : 0u;
-    const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched);
+    const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched, n_masked);
     clear_failed(a.cand, row, has && !ok, lane);
   }
   // one atomic per warp per counter
@@ -635,8 +696,10 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
     n_scanned += __shfl_down_sync(GSM_FULL, n_scanned, o);
     n_matched += __shfl_down_sync(GSM_FULL, n_matched, o);
+    n_masked += __shfl_down_sync(GSM_FULL, n_masked, o);
   }
   if (lane == 0) {
+    if (n_masked) atomicAdd(a.ctr + C_FILTER_MASKED, (unsigned long long)n_masked);
     if (n_rows) atomicAdd(a.ctr + C_FILTER_ROWS, n_rows);
     if (n_scanned) atomicAdd(a.ctr + C_FILTER_SCANNED, n_scanned);
     if (n_matched) atomicAdd(a.ctr + C_FILTER_MATCHED, (unsigned long long)n_matched);
@@ -655,20 +718,46 @@ __global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterA
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n = *d_nrows;
   unsigned long long n_rows = 0, n_scanned = 0;
-  uint32_t n_matched = 0;
-  for (uint64_t base = (uint64_t)warp * 32; base < n; base += (uint64_t)nwarps * 32) {
-    const bool has = base + lane < n;
-    const uint32_t row = has ? __ldg(rows + base + lane) : 0u;
-    const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched);
-    clear_failed(a.cand, row, has && !ok, lane);
+  uint32_t n_matched = 0, n_masked = 0;
+  // A warp takes RB batches of 32 rows at once when there are enough rows to
+  // keep every warp busy: the RB row ids, then their label signatures, are
+  // loaded together (RB-fold memory-level parallelism for the pre-test, which
+  // decides most rows of the big groups), then the surviving rows are evaluated
+  // batch by batch.
+  constexpr int RB = 4;
+  const uint32_t rb = n >= (uint64_t)nwarps * 32 * RB ? RB : 1;
+  for (uint64_t base = (uint64_t)warp * 32 * rb; base < n; base += (uint64_t)nwarps * 32 * rb) {
+    uint32_t row[RB], pass = 0, hasm = 0;
+#pragma unroll
+    for (int j = 0; j < RB; j++) {
+      const uint64_t i = base + (uint64_t)j * 32 + lane;
+      const bool has = (uint32_t)j < rb && i < n;
+      row[j] = has ? __ldg(rows + i) : 0u;
+      hasm |= (uint32_t)has << j;
+    }
+#pragma unroll
+    for (int j = 0; j < RB; j++)
+      if ((hasm >> j) & 1u) pass |= (uint32_t)label_pretest(a, row[j], n_masked) << j;
+#pragma unroll 1
+    for (uint32_t j = 0; j < rb; j++) {
+      uint32_t r = row[0];
+#pragma unroll
+      for (int t = 1; t < RB; t++)
+        if (j == (uint32_t)t) r = row[t];
+      const bool has = (hasm >> j) & 1u;
+      const bool ok = eval_rows<PT, SIMD, true>(a, r, (pass >> j) & 1u, lane, n_rows, n_scanned, n_matched, n_masked);
+      clear_failed(a.cand, r, has && !ok, lane);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
     n_scanned += __shfl_down_sync(GSM_FULL, n_scanned, o);
     n_matched += __shfl_down_sync(GSM_FULL, n_matched, o);
+    n_masked += __shfl_down_sync(GSM_FULL, n_masked, o);
   }
   if (lane == 0) {
+    if (n_masked) atomicAdd(a.ctr + C_FILTER_MASKED, (unsigned long long)n_masked);
     if (n_rows) atomicAdd(a.ctr + C_FILTER_ROWS, n_rows);
     if (n_scanned) atomicAdd(a.ctr + C_FILTER_SCANNED, n_scanned);
     if (n_matched) atomicAdd(a.ctr + C_FILTER_MATCHED, (unsigned long long)n_matched);
@@ -735,9 +824,11 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
     t.f[d] = fmt_of<PT>(a.f[d]);
     t.ne[d] = a.ne[d];
     t.minl[d] = 0xffffffffu; t.maxl[d] = 0;
+    t.needm[d] = 0;
     for (int j = 0; j < MAXG; j++) {
       t.e[d][j] = a.e[d][j];
       if (j < (int)a.ne[d]) {
+        t.needm[d] |= label_bit(a.e[d][j].label);
         t.minl[d] = min(t.minl[d], a.e[d][j].label);
         t.maxl[d] = max(t.maxl[d], a.e[d][j].label);
       }

@@ -49,6 +49,9 @@ cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos,
                           cudaStream_t st);
 cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned long long* out2,
                                cudaStream_t st);
+// per-row label signature (Fmt::lmask) from row_ptr + pred
+cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
+                              uint32_t* lmask, cudaStream_t st);
 
 // ----------------------------------------------------------------- bitmaps
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st);
@@ -60,6 +63,7 @@ struct FmtAny {
   const uint32_t* rp;
   const uint32_t* col;
   const void* pred;
+  const uint32_t* lmask;
 };
 template <typename PT>
 __host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
@@ -67,6 +71,7 @@ __host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
   f.rp = a.rp;
   f.col = a.col;
   f.pred = (const PT*)a.pred;
+  f.lmask = a.lmask;
   return f;
 }
 

@@ -161,6 +161,7 @@ static void free_lspm(gsmart_ctx* ctx) {
     dfree(ctx, f.rp);
     dfree(ctx, f.col);
     dfree(ctx, f.pred);
+    dfree(ctx, f.lmask);
     f = Lspm();
   }
   ctx->lspm_gen++;
@@ -203,11 +204,6 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
   if (n >= 0xffffffffull) FAIL(GSMART_E_INVALID_ARG, "n must be < 2^32 - 1");
   if (flags != GSMART_PTR_HOST && flags != GSMART_PTR_DEVICE) FAIL(GSMART_E_INVALID_ARG, "flags must be PTR_HOST or PTR_DEVICE");
   CU(cudaSetDevice(ctx->cfg.device));
-  if (flags == GSMART_PTR_HOST) {
-    for (uint64_t i = 0; i < n; i++)
-      if (s[i] >= n_entities || o[i] >= n_entities || p[i] == 0 || p[i] > n_predicates)
-        FAIL(GSMART_E_INVALID_ARG, "triple id out of range at index " + std::to_string(i));
-  }
   free_lspm(ctx);
   dfree(ctx, ctx->d_s);
   dfree(ctx, ctx->d_p);
@@ -224,7 +220,7 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
     CU(cudaMemcpyAsync(ctx->d_p, p, n * 4, kind, ctx->st));
     CU(cudaMemcpyAsync(ctx->d_o, o, n * 4, kind, ctx->st));
   }
-  if (flags == GSMART_PTR_DEVICE && n) {
+  if (n) {  // ids are validated on the device after the copy (host and device input alike)
     CU(cudaMemsetAsync(ctx->d_ctr + 32, 0, 8, ctx->st));
     k_validate<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0, ctx->st>>>(
         ctx->d_s, ctx->d_p, ctx->d_o, n, n_entities, n_predicates, ctx->d_ctr + 32);
@@ -284,6 +280,8 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
     TRY(sc.get((char**)&stmp, scan_tmp_bytes((uint64_t)N + 1)));
     CU(scan_exclusive_u32(L.rp, L.rp, (uint64_t)N + 1, tot, stmp, ctx->st, nullptr));
   }
+  TRY(dalloc(ctx, &L.lmask, (uint64_t)N + 1));
+  CU(launch_label_mask(L.rp, L.pred, ctx->pred_bytes, N, L.lmask, ctx->st));
   CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
   CU(launch_heavy_stats(L.rp, N, ctx->d_ctr + 42, ctx->st));
   unsigned long long hv[2];
@@ -330,6 +328,7 @@ extern "C" gsmart_status gsmart_lspm_get(const gsmart_ctx* ctx, uint32_t format,
   out->row_ptr = L.rp;
   out->col = L.col;
   out->pred = L.pred;
+  out->label_mask = L.lmask;
   return GSMART_OK;
 }
 

@@ -28,6 +28,7 @@ struct Lspm {
   uint32_t* rp = nullptr;
   uint32_t* col = nullptr;
   void* pred = nullptr;
+  uint32_t* lmask = nullptr;  // [N] row label signatures (Fmt::lmask)
   uint64_t nnz = 0;
   bool built = false;
   unsigned long long heavy_rows = 0, heavy_chunks = 0;

@@ -39,7 +39,8 @@ class gsmart_config(ctypes.Structure):
 
 class gsmart_lspm_view(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_uint32), ("nnz", ctypes.c_uint64), ("pred_bytes", ctypes.c_uint32),
-                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("pred", ctypes.c_void_p)]
+                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("pred", ctypes.c_void_p),
+                ("label_mask", ctypes.c_void_p)]
 
 
 class gsmart_qvertex(ctypes.Structure):
@@ -221,7 +222,7 @@ def gsmart_lspm_get(ctx, fmt):
     v = gsmart_lspm_view()
     _check(_lib.gsmart_lspm_get(ctx, fmt, ctypes.byref(v)), ctx)
     return {"n_rows": v.n_rows, "nnz": v.nnz, "pred_bytes": v.pred_bytes, "row_ptr": v.row_ptr,
-            "col": v.col, "pred": v.pred}
+            "col": v.col, "pred": v.pred, "label_mask": v.label_mask}
 
 
 def _query_struct(q):

@@ -15,4 +15,4 @@ for (i, k), m in sorted(d.items()):
         continue
     t = m.get("gpu__time_duration.sum", 0) / 1000
     b = (m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)) / 1e6
-    print(f"{i:4d} {k[:40]:40s} us={t:9.1f} MB={b:9.1f} GB/s={b / max(t, 1e-9) * 1e-3 * 1e3:8.1f}")
+    print(f"{i:4d} {k[:40]:40s} us={t:9.1f} MB={b:9.1f} GB/s={b / max(t, 1e-9) * 1e3:8.1f}")

@@ -42,4 +42,11 @@ for rep in range(args.reps):
             print(f"{q.name:4s} rows={n:9d} wall_ms={dt:7.3f} launches={sum(st['launches'].values()):3d} "
                   f"levels={st['level_nodes']} filter_rows={st['filter_rows']} scanned={st['filter_entries']} "
                   f"expand={st['expand_entries']}", flush=True)
-            print("     ", {k: v for k, v in st['launches'].items() if v}, "cols", G.gsmart_result_shape(r0)[1] if False else "", flush=True)
+            print("     ", {k: v for k, v in st['launches'].items() if v}, flush=True)
+# per-kernel-class CUDA-event times of each query (GSMART_PROFILE: events on the launch stream)
+for q, pl in zip(qs, plans):
+    r = G.gsmart_execute(eng.ctx, pl, G.GSMART_PROFILE | G.GSMART_KEEP_ON_DEVICE)
+    st = G.gsmart_result_stats(r)
+    G.gsmart_result_free(r)
+    ms = {k: round(v, 4) for k, v in st["ms_kernel"].items() if v > 0}
+    print(f"{q.name:4s} kernel_ms total={sum(ms.values()):.4f}", ms, flush=True)

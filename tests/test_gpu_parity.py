@@ -90,6 +90,12 @@ def test_lspm_arrays_match_definition(G, eng, seed, N, P, M, keep):
         np.testing.assert_array_equal(rp.astype(np.uint64), ref["row_ptr"])
         np.testing.assert_array_equal(col, ref["col"])
         np.testing.assert_array_equal(pred.astype(np.uint32), ref["pred"])
+        # row label signatures: bit (l & 31) of every label present in the row
+        lm = G.gsmart_copy_to_host(eng.ctx, v["label_mask"], N * 4)
+        exp = np.zeros(N, dtype=np.uint64)
+        rows = np.repeat(np.arange(N), np.diff(ref["row_ptr"].astype(np.int64)))
+        np.bitwise_or.at(exp, rows, np.left_shift(1, ref["pred"].astype(np.uint64) & 31))
+        np.testing.assert_array_equal(lm.astype(np.uint64), exp)
 
 
 # ------------------------------------------------------------------ random tiny cases
@@ -334,6 +340,25 @@ def test_edge_cases(G, eng):
         assert _rows(host) == [(2, 0, 1, 0), (2, 0, 1, 5)]
         assert _rows(G.gsmart_result_rows(r)) == [(2, 0, 1, 0), (2, 0, 1, 5)]
         G.gsmart_result_free(r)
+
+
+def test_label_signature_collisions(G, eng):
+    """Row label signatures fold labels mod 32 (P > 32): labels 1, 33 and 65 share
+    a bit, so rows holding only label 1 pass the pre-test for a label-33 edge and
+    must still be rejected by the scan.  Rows vs brute force and the oracle."""
+    rng = np.random.default_rng(5)
+    n, P = 40, 70
+    s = rng.integers(0, n, 600).astype(np.uint32)
+    o = rng.integers(0, n, 600).astype(np.uint32)
+    p = rng.choice(np.array([1, 33, 65, 2, 34], dtype=np.uint32), 600, p=[0.5, 0.05, 0.05, 0.3, 0.1])
+    eng.load(s, p, o, n, P)
+    for q in (Query((None, None), ((0, 33, 1),)),
+              Query((None, None, None), ((0, 33, 1), (0, 2, 2))),
+              Query((None, None, None), ((0, 65, 1), (2, 34, 0), (1, 1, 2))),
+              Query((None, None), ((0, 33, 1), (1, 65, 0)))):
+        got = _rows(eng.query(q))
+        assert got == R.brute_force(s, p, o, n, q), q
+        assert got == _rows(oracle_bgp(s, p, o, q)), q
 
 
 def test_result_overflow_and_empty_load(G):
