@@ -230,7 +230,7 @@ typedef struct {
   double ms_kernel[GSMART_NKERNELS]; /* per kernel class (GSMART_PROFILE), see kernel_names */
   uint64_t launches[GSMART_NKERNELS];
   uint64_t bytes[GSMART_NKERNELS];   /* algorithmic bytes per kernel class */
-  uint64_t edges_evaluated;     /* LSpM entries read whose label matched (seed + filter + expansion) */
+  uint64_t edges_evaluated;     /* LSpM entries read whose label matched (seed + filter + push + expansion) */
   uint64_t filter_rows;         /* rows (candidate bits) processed by the group filter */
   uint64_t filter_entries;      /* LSpM entries scanned by the group filter */
   uint64_t seed_entries;        /* segment entries scattered by seeds */

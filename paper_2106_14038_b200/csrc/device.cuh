@@ -17,7 +17,8 @@ constexpr uint32_t EXP_CHUNK = 256;    // expansion work item = <= 256 segment e
 
 // counters (uint64) in the ctx stats array
 enum Ctr { C_FILTER_ROWS = 0, C_FILTER_SCANNED, C_FILTER_MATCHED, C_SEED, C_EXPAND, C_CLOSING,
-           C_HEAVY, C_FILTER_MASKED, C_NCTR };
+           C_HEAVY, C_FILTER_MASKED, C_FILTER_SKIPPED, C_PUSH, C_PUSH_MATCHED, C_NCTR };
+static_assert(C_NCTR <= 16, "slot counter words [16, 32) hold the SkipIf change sequence");
 
 // One LSpM format on the device: entries of row r are [rp[r], rp[r+1]) sorted by (pred, col).
 template <typename PT>
@@ -84,15 +85,18 @@ __device__ __forceinline__ void warp_label_range(const Fmt<PT>& f, uint32_t r, u
   hi = warp_lower_bound(f.pred, lo, e, l + 1);
 }
 
-// Is (r, l, target) an entry?  (membership of target in seg_l(r))
+// Is (r, l, target) an entry?  (membership of target in seg_l(r)).  A row's
+// entries are sorted by (pred, col): one binary search on that pair (label and
+// column loaded together per step, ~log2(len) dependent steps) instead of two
+// label-bound searches followed by a column search.
 template <typename PT>
 __device__ __forceinline__ bool has_entry(const Fmt<PT>& f, uint32_t r, uint32_t l, uint32_t target) {
-  uint32_t lo, hi;
-  label_range(f, r, l, lo, hi);
+  uint32_t lo = __ldg(f.rp + r), hi = __ldg(f.rp + r + 1);
   while (lo < hi) {
-    uint32_t m = (lo + hi) >> 1;
-    uint32_t c = __ldg(f.col + m);
-    if (c < target) lo = m + 1; else if (c > target) hi = m; else return true;
+    const uint32_t m = (lo + hi) >> 1;
+    const uint32_t p = __ldg(f.pred + m), c = __ldg(f.col + m);
+    if (p == l && c == target) return true;
+    if (p < l || (p == l && c < target)) lo = m + 1; else hi = m;
   }
   return false;
 }

@@ -55,7 +55,7 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
   dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ctr);
   dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
-  dfree(st, s.frows); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2); dfree(st, s.d_tab);
+  dfree(st, s.frows); dfree(st, s.sat); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2); dfree(st, s.d_tab);
   for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second.exec);
   s.graphs.clear();
   cudaStreamSynchronize(st);
@@ -213,6 +213,10 @@ struct Exec {
   FmtAny fa[2];
   int launches[GSMART_NKERNELS] = {0};
   uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
+  uint32_t filter_seq = 0;             // group evaluations issued so far (SkipIf sequence)
+  std::vector<std::vector<uint8_t>> push_dec;  // per group, per edge: push form (label-major)
+  uint64_t push_and = 0;               // k_and_tracked launches (bitmap bytes)
+  std::vector<uint32_t> group_seq;     // per group: sequence of its last evaluation
   int attempts = 0;
   bool seq_open = false;        // a look-back launch sequence was started (end it in finalize)
   bool graph_replayed = false;  // phase 1 came from the plan's cached CUDA graph
@@ -261,7 +265,7 @@ struct Exec {
       x.h_epoch = reinterpret_cast<const volatile uint32_t*>(sl.h_pin + H_EPOCH);
       x.d_epoch = sl.d_epoch;
       x.zero = sl.d_ctr;  // counters
-      x.n_zero = C_NCTR;
+      x.n_zero = 32;  // counters [0, C_NCTR) and the SkipIf change words at [16, 32)
       x.zero2 = sl.d_sz;  // expansion sizes
       x.n_zero2 = 128;
       x.ovf = sl.d_ovf;
@@ -309,7 +313,7 @@ struct Exec {
         for (size_t i = 1; i < ss.size(); i++)
           g.edges.push_back({ss[i]->edge, ss[i]->label, ss[i]->dir == OUT ? (uint32_t)IN : (uint32_t)OUT,
                              0x80000000u | ss[i]->cid});
-        TRY(eval_group(g));
+        TRY(eval_group(g, SIZE_MAX));  // constant-target filter edges: evaluated once
       }
     }
     if (!plan->guards.empty() && !plan->vars.empty()) {
@@ -323,9 +327,76 @@ struct Exec {
 
   // ---- a4: grouped incident-edge evaluation of one group (§5 Eqs. 17/21).
   // nbr with bit 31 set = constant target (extra seed).
-  gsmart_status eval_group(const Group& g) {
-    std::vector<const GroupEdge*> by[2];
-    for (auto& e : g.edges) by[e.dir == OUT ? 0 : 1].push_back(&e);
+  gsmart_status eval_group(const Group& g, size_t gi) {
+    std::vector<const GroupEdge*> by[2], push;
+    const std::vector<uint8_t>* dec = gi < push_dec.size() ? &push_dec[gi] : nullptr;
+    for (size_t ei = 0; ei < g.edges.size(); ei++) {
+      const GroupEdge& e = g.edges[ei];
+      if (dec && (*dec)[ei]) push.push_back(&e);
+      else by[e.dir == OUT ? 0 : 1].push_back(&e);
+    }
+    // cheapest (and most selective) label first: later edges only mark rows that
+    // passed the earlier ones, and stop at once when none did
+    std::stable_sort(push.begin(), push.end(), [&](const GroupEdge* x, const GroupEdge* y) {
+      return ctx->lm.off[x->label + 1] - ctx->lm.off[x->label] < ctx->lm.off[y->label + 1] - ctx->lm.off[y->label];
+    });
+    // change tracking (SkipIf): a re-evaluation is skipped on the device when no
+    // neighbour bitmap changed since this group's previous evaluation (world == 1)
+    const uint32_t seq = ++filter_seq;
+    SkipIf sk;
+    sk.chg = reinterpret_cast<uint32_t*>(sl.d_ctr + 16);
+    const uint32_t prev = gi < group_seq.size() ? group_seq[gi] : 0u;
+    if (prev && ctx->world == 1) {
+      sk.prev = prev;
+      for (auto& e : g.edges)
+        if (!(e.nbr & 0x80000000u) && e.nbr != g.center) sk.nbr_mask |= 1u << slot[e.nbr];
+    }
+    if (gi < group_seq.size()) group_seq[gi] = seq;
+    if (!push.empty()) {
+      // push form (label-major streaming) of the chosen edges: each marks the rows
+      // that also passed the previous one, the last mark set is AND-ed into cand_x
+      const LabelMajor& lm = ctx->lm;
+      const uint32_t* prev_sat = nullptr;
+      prof.begin(K_FILTER);
+      for (size_t i = 0; i < push.size(); i++) {
+        const GroupEdge* e = push[i];
+        uint32_t* out = sl.sat + (i & 1) * (uint64_t)Wpad;
+        unsigned long long* cnt = sl.d_ctr + 32 + (i & 1);
+        CU(cudaMemsetAsync(out, 0, (size_t)W * 4, sl.st));
+        CU(cudaMemsetAsync(cnt, 0, 8, sl.st));
+        PushArgs pa;
+        memset(&pa, 0, sizeof pa);
+        pa.s = lm.s;
+        pa.o = lm.o;
+        pa.beg = lm.off[e->label];
+        pa.end = lm.off[e->label + 1];
+        pa.out = e->dir == OUT ? 1u : 0u;
+        pa.cand = cand(g.center);
+        pa.sat_in = prev_sat;
+        pa.sat_out = out;
+        pa.in_cnt = prev_sat ? sl.d_ctr + 32 + ((i + 1) & 1) : nullptr;
+        pa.out_cnt = cnt;
+        if (e->nbr & 0x80000000u) {
+          pa.mode = GE_CONST;
+          pa.cval = e->nbr & 0x7fffffffu;
+        } else if (e->nbr == g.center) {
+          pa.mode = GE_SELF;
+        } else {
+          pa.mode = GE_PROBE;
+          pa.nbr = cand(e->nbr);
+        }
+        pa.skip = sk;
+        pa.ctr = sl.d_ctr;
+        CU(launch_push_edge(pa, ctx->sm_count, sl.st));
+        launches[K_FILTER]++;
+        prev_sat = out;
+      }
+      CU(launch_and_tracked(cand(g.center), prev_sat, W, sk, (uint32_t)slot[g.center], seq, sl.st, ctx->sm_count));
+      launches[K_FILTER]++;
+      push_and++;
+      prof.end();
+      if (by[0].empty() && by[1].empty()) return GSMART_OK;
+    }
     size_t done[2] = {0, 0};
     // row-list path: compact the center's candidate rows of this rank once per group
     const bool rowlist = (ctx->filter_variant & 4) != 0;
@@ -334,7 +405,7 @@ struct Exec {
       prof.begin(K_COMPACT);
       CU(cudaMemsetAsync(d_nrows, 0, 8, sl.st));
       CU(launch_bitmap_compact_lb(cand(g.center) + wlo, whi > wlo ? whi - wlo : 0, sl.frows, sl.frows_cap, d_nrows,
-                                  sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
+                                  sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32, sk));
       launches[K_COMPACT] += compact_launches(whi > wlo ? whi - wlo : 0);
       prof.end();
     }
@@ -370,6 +441,9 @@ struct Exec {
       a.ctr = sl.d_ctr;
       a.variant = ctx->filter_variant;
       a.claim = next_lb(sl);  // its counter() is fresh and zeroed: no reset launch
+      a.skip = sk;
+      a.center_slot = (uint32_t)slot[g.center];
+      a.seq = seq;
       if (rowlist) {
         a.rows = sl.frows;
         a.d_nrows = d_nrows;
@@ -468,6 +542,60 @@ struct Exec {
     return GSMART_OK;
   }
 
+  // Push or pull per group edge (cached per plan and LSpM generation).  Pull
+  // (k_group_filter_rows) costs ~40-60 DRAM bytes per candidate row of the
+  // center (scattered row_ptr / label / column sectors); push (k_push_edge)
+  // streams 8 bytes per entry of the edge's label.  The center's candidate count
+  // is bounded by its seed segments (row lengths read once here) or N.
+  static constexpr uint64_t PUSH_MIN = 1ull << 22;  // smaller labels: pull (latency-bound either way)
+  static constexpr uint64_t PUSH_RATIO = 6;
+  gsmart_status decide_push() {
+    push_dec.clear();
+    const int v = ctx->filter_variant;
+    if (!ctx->lm.built || ctx->world > 1 || (v & 16) || plan->groups.empty()) return GSMART_OK;
+    auto it = ctx->push_cache.find(plan->uid);
+    if (it != ctx->push_cache.end() && it->second.first == ctx->lspm_gen) {
+      push_dec = it->second.second;
+      return GSMART_OK;
+    }
+    const uint32_t N = ctx->N;
+    std::vector<uint64_t> est(plan->n_vertices, N);
+    std::vector<uint32_t> rp2(2 * plan->seeds.size(), 0);
+    for (size_t i = 0; i < plan->seeds.size(); i++) {
+      const Seed& sd = plan->seeds[i];
+      if (sd.cid >= N) continue;
+      CU(cudaMemcpyAsync(&rp2[2 * i], ctx->f[sd.dir == OUT ? 0 : 1].rp + sd.cid, 8, cudaMemcpyDeviceToHost, sl.st));
+    }
+    if (!plan->seeds.empty()) CU(cudaStreamSynchronize(sl.st));
+    for (size_t i = 0; i < plan->seeds.size(); i++) {
+      const Seed& sd = plan->seeds[i];
+      if (sd.cid < N) est[sd.var] = std::min<uint64_t>(est[sd.var], rp2[2 * i + 1] - rp2[2 * i]);
+    }
+    push_dec.resize(plan->groups.size());
+    for (size_t gi = 0; gi < plan->groups.size(); gi++) {
+      const Group& g = plan->groups[gi];
+      push_dec[gi].assign(g.edges.size(), 0);
+      // in ascending label size (the launch order); a pushed edge bounds the
+      // center's candidates by its label's entry count for the next decision
+      std::vector<size_t> ord(g.edges.size());
+      for (size_t ei = 0; ei < ord.size(); ei++) ord[ei] = ei;
+      auto M_of = [&](size_t ei) {
+        const uint32_t l = g.edges[ei].label;
+        return l + 1 < ctx->lm.off.size() ? ctx->lm.off[l + 1] - ctx->lm.off[l] : 0ull;
+      };
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return M_of(x) < M_of(y); });
+      uint64_t bound = est[g.center];
+      for (size_t ei : ord) {
+        const uint64_t M = M_of(ei);
+        const bool p = (v & 8) || (M >= PUSH_MIN && M <= PUSH_RATIO * bound);
+        push_dec[gi][ei] = p;
+        if (p) bound = std::min(bound, M);
+      }
+    }
+    ctx->push_cache[plan->uid] = {ctx->lspm_gen, push_dec};
+    return GSMART_OK;
+  }
+
   // every workspace buffer phase 1 touches, sized before any launch (a graph
   // replay must see the same addresses; growth bumps sl.ws_gen)
   gsmart_status ensure_workspace() {
@@ -475,6 +603,7 @@ struct Exec {
     TRY(slot_heavy(ctx, sl));
     TRY(slot_buf(ctx, sl, &sl.cand, &sl.cand_words, std::max<uint64_t>((uint64_t)Wpad * nvar, 1)));
     if (ctx->filter_variant & 4) TRY(slot_buf(ctx, sl, &sl.frows, &sl.frows_cap, (uint64_t)W * 32));
+    if (ctx->lm.built && ctx->world == 1) TRY(slot_buf(ctx, sl, &sl.sat, &sl.sat_cap, 2ull * Wpad));
     for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
@@ -485,10 +614,12 @@ struct Exec {
   // stable workspace addresses, launched directly or replayed from a graph
   gsmart_status phase1_kernels() {  // counters/sizes are zeroed by k_init_cands
     bool empty = false;
+    group_seq.assign(plan->groups.size(), 0);
+    filter_seq = 0;
     TRY(seeds_and_guards(&empty));
-    for (auto& g : plan->groups) TRY(eval_group(g));
+    for (size_t i = 0; i < plan->groups.size(); i++) TRY(eval_group(plan->groups[i], i));
     if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
-      for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i]));
+      for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i], i));
     return launch_expansion(true);
   }
 
@@ -509,6 +640,7 @@ struct Exec {
       graph_replayed = true;
       for (int i = 0; i < GSMART_NKERNELS; i++) launches[i] += it->second.launches[i];
       filter_main += it->second.filter_main;
+      push_and += it->second.push_and;
       return GSMART_OK;
     }
     if (it != sl.graphs.end()) {
@@ -517,7 +649,7 @@ struct Exec {
     }
     const uint32_t off0 = sl.seq_off;
     const std::vector<int> l0(launches, launches + GSMART_NKERNELS);
-    const uint64_t fm0 = filter_main;
+    const uint64_t fm0 = filter_main, pa0 = push_and;
     CU(cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal));
     gsmart_status s = body();
     cudaGraph_t graph = nullptr;
@@ -541,6 +673,7 @@ struct Exec {
     ge.launches.resize(GSMART_NKERNELS);
     for (int i = 0; i < GSMART_NKERNELS; i++) ge.launches[i] = launches[i] - l0[i];
     ge.filter_main = filter_main - fm0;
+    ge.push_and = push_and - pa0;
     if (sl.graphs.size() >= 512) {  // bounded cache
       for (auto& kv : sl.graphs) cudaGraphExecDestroy(kv.second.exec);
       sl.graphs.clear();
@@ -586,6 +719,7 @@ struct Exec {
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].closing.size() > (size_t)MAXC)
         FAIL(GSMART_E_UNSUPPORTED, "more than 16 closing edges on one level");
+    TRY(decide_push());
     TRY(ensure_workspace());
     TRY(begin_seq(ctx, sl));
     seq_open = true;
@@ -835,12 +969,15 @@ struct Exec {
     st.seed_entries = c[C_SEED];
     st.expand_entries = c[C_EXPAND];
     st.closing_checks = c[C_CLOSING];
-    st.edges_evaluated = c[C_FILTER_MATCHED] + c[C_SEED] + c[C_EXPAND];
+    st.edges_evaluated = c[C_FILTER_MATCHED] + c[C_SEED] + c[C_EXPAND] + c[C_PUSH];
     const uint64_t pb = (uint64_t)ctx->pred_bytes;
     // algorithmic bytes: what each step must move
     uint64_t parents = 0, children = 0;
+    // launches skipped on the device (SkipIf) move no bitmap bytes
+    const uint64_t skipped = std::min<uint64_t>(c[C_FILTER_SKIPPED], filter_main);
     st.bytes[K_FILTER] = 4 * c[C_FILTER_MASKED] + 8 * c[C_FILTER_ROWS] + pb * c[C_FILTER_SCANNED] + 4 * c[C_FILTER_MATCHED] +
-                         8ull * filter_main * W;
+                         8ull * (filter_main - skipped) * W +
+                         8 * c[C_PUSH] + 12ull * push_and * W;  // push: (s, o) per entry; AND: cand r/w + sat
     st.bytes[K_SEED] = 4 * c[C_SEED];
     for (uint32_t k = 0; k + 1 < st.n_levels && k + 1 < GSMART_MAX_LEVELS; k++) parents += st.level_nodes[k];
     for (uint32_t k = 1; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) children += st.level_nodes[k];
@@ -849,7 +986,8 @@ struct Exec {
     // a5: every compaction reads this rank's bitmap range once and writes 4 B per id
     // (row lists of the groups + level 0); initialisation writes the bitmaps once
     const uint64_t range_bytes = 4ull * (whi - wlo);
-    st.bytes[K_COMPACT] = range_bytes * (uint64_t)launches[K_COMPACT] + 4 * (c[C_FILTER_ROWS] + st.level_nodes[0]);
+    const uint64_t compact_run = (uint64_t)launches[K_COMPACT] - std::min<uint64_t>(skipped, launches[K_COMPACT]);
+    st.bytes[K_COMPACT] = range_bytes * compact_run + 4 * (c[C_FILTER_ROWS] + st.level_nodes[0]);
     st.bytes[K_BITMAP] = 4ull * Wpad * plan->vars.size();
     // a8: mark reads parent (4) + alive (1) per child; compaction reads bind/parent/alive
     // (9) and writes newidx (4) per node, plus 8 B per surviving node

@@ -62,8 +62,9 @@ static uint32_t bc_chunk_words(uint32_t n_words, int sm_count) {
 __global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restrict__ bm, uint32_t n_words,
                                                         uint32_t chunk, uint32_t* __restrict__ ids, uint64_t cap,
                                                         unsigned long long* d_count, int* overflow, LBArgs lb,
-                                                        uint32_t id_base) {
+                                                        uint32_t id_base, SkipIf skip) {
   GSM_PDL_ENTRY();
+  if (skip.skip()) return;
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_p;
   __shared__ uint32_t s_tile;
@@ -193,12 +194,12 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restr
 
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
-                                     cudaStream_t st, uint32_t id_base) {
+                                     cudaStream_t st, uint32_t id_base, SkipIf skip) {
   if (n_words == 0) return cudaMemsetAsync(d_count, 0, 8, st);
   const uint32_t chunk = bc_chunk_words(n_words, sm_count);
   const uint32_t nch = (n_words + chunk - 1) / chunk;
   if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
-  pdl_launch(k_bitmap_compact, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base);
+  pdl_launch(k_bitmap_compact, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
   return cudaGetLastError();
 }
 
@@ -317,13 +318,16 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
         s_tgt[p * TGTC + c] = a.cl[c].self ? 0u : ancestor(a.tab, a.k - 1, nlo + p, a.cl[c].other_level);
       }
     __syncthreads();
-    uint32_t node[EX_I], child[EX_I], keepm = 0;
+    // The EX_I entries of a thread go through each stage together, so their
+    // independent loads (segment begin, column, candidate probe, row bounds,
+    // closing-edge search steps) are in flight at the same time.
+    uint32_t node[EX_I], child[EX_I], epos[EX_I], keepm = 0;
     const uint32_t t0 = base + threadIdx.x * EX_I;
 #pragma unroll
-    for (int j = 0; j < EX_I; j++) {
+    for (int j = 0; j < EX_I; j++) {  // parent of each entry (shared-memory search)
       const uint32_t t = t0 + j;
       node[j] = 0;
-      child[j] = 0;
+      epos[j] = 0;
       if (t > last) continue;
       uint32_t n, o;
       if (soff) {
@@ -338,26 +342,74 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
         n = ub_global(a.off, F1, t) - 1;
         o = __ldg(a.off + n);
       }
-      const uint32_t pos = t - o;
-      const uint32_t c = a.tree ? __ldg(fsrc.col + __ldg(a.seg_beg + n) + pos) : __ldg(a.list + pos);
-      bool keep = bit_of(a.cand, c) != 0;
-      n_exam++;
-      for (uint32_t q = 0; q < a.ncl && keep; q++) {
-        const ClosingDev cl = a.cl[q];
-        uint32_t tgt = c;
-        if (!cl.self) tgt = stgt ? s_tgt[(n - nlo) * TGTC + q] : ancestor(a.tab, a.k - 1, n, cl.other_level);
-        // (c, l, tgt) in the child's row of format dir  <=>  (tgt, l, c) in tgt's row of the
-        // other format: binary-search the shorter row (a hub on one side costs log of the other)
-        const Fmt<PT>& fc = cl.dir ? f1 : f0;
-        const Fmt<PT>& fo = cl.dir ? f0 : f1;
-        const uint32_t lc = __ldg(fc.rp + c + 1) - __ldg(fc.rp + c);
-        const uint32_t lt = __ldg(fo.rp + tgt + 1) - __ldg(fo.rp + tgt);
-        keep = lc <= lt ? has_entry(fc, c, cl.label, tgt) : has_entry(fo, tgt, cl.label, c);
-        n_close++;
-      }
       node[j] = n;
-      child[j] = c;
-      if (keep) keepm |= 1u << j;
+      epos[j] = t - o;
+      keepm |= 1u << j;
+    }
+    const uint32_t actm = keepm;
+    uint32_t sb[EX_I];
+#pragma unroll
+    for (int j = 0; j < EX_I; j++) sb[j] = (a.tree && ((actm >> j) & 1u)) ? __ldg(a.seg_beg + node[j]) : 0u;
+#pragma unroll
+    for (int j = 0; j < EX_I; j++)
+      child[j] = ((actm >> j) & 1u) ? (a.tree ? __ldg(fsrc.col + sb[j] + epos[j]) : __ldg(a.list + epos[j])) : 0u;
+#pragma unroll
+    for (int j = 0; j < EX_I; j++)
+      if (((actm >> j) & 1u) && !bit_of(a.cand, child[j])) keepm &= ~(1u << j);
+    n_exam += __popc(actm);
+    for (uint32_t q = 0; q < a.ncl && keepm; q++) {
+      const ClosingDev cl = a.cl[q];
+      // (c, l, tgt) in the child's row of format dir  <=>  (tgt, l, c) in tgt's row of the
+      // other format: search the shorter row (a hub on one side costs log of the other)
+      const Fmt<PT>& fc = cl.dir ? f1 : f0;
+      const Fmt<PT>& fo = cl.dir ? f0 : f1;
+      uint32_t row[EX_I], key[EX_I], lo[EX_I], hi[EX_I];
+      bool useo[EX_I];
+#pragma unroll
+      for (int j = 0; j < EX_I; j++) {
+        uint32_t tgt = child[j];
+        if (!cl.self && ((keepm >> j) & 1u))
+          tgt = stgt ? s_tgt[(node[j] - nlo) * TGTC + q] : ancestor(a.tab, a.k - 1, node[j], cl.other_level);
+        row[j] = tgt;  // temporarily the target
+      }
+#pragma unroll
+      for (int j = 0; j < EX_I; j++) {
+        const uint32_t c = child[j], tgt = row[j];
+        const bool on = (keepm >> j) & 1u;
+        const uint32_t c0 = on ? __ldg(fc.rp + c) : 0u, c1 = on ? __ldg(fc.rp + c + 1) : 0u;
+        const uint32_t g0 = on ? __ldg(fo.rp + tgt) : 0u, g1 = on ? __ldg(fo.rp + tgt + 1) : 0u;
+        useo[j] = (g1 - g0) < (c1 - c0);
+        row[j] = useo[j] ? tgt : c;
+        key[j] = useo[j] ? c : tgt;
+        lo[j] = useo[j] ? g0 : c0;
+        hi[j] = useo[j] ? g1 : c1;
+      }
+      // lock-step binary searches on (pred, col) for the EX_I entries
+      uint32_t live = keepm, found = 0;
+      while (live) {
+#pragma unroll
+        for (int j = 0; j < EX_I; j++) {
+          if (!((live >> j) & 1u)) continue;
+          if (lo[j] >= hi[j]) {
+            live &= ~(1u << j);
+            continue;
+          }
+          const uint32_t m = (lo[j] + hi[j]) >> 1;
+          const PT* pr = useo[j] ? fo.pred : fc.pred;
+          const uint32_t* co = useo[j] ? fo.col : fc.col;
+          const uint32_t p = __ldg(pr + m), cc = __ldg(co + m);
+          if (p == cl.label && cc == key[j]) {
+            found |= 1u << j;
+            live &= ~(1u << j);
+          } else if (p < cl.label || (p == cl.label && cc < key[j])) {
+            lo[j] = m + 1;
+          } else {
+            hi[j] = m;
+          }
+        }
+      }
+      n_close += __popc(keepm);
+      keepm &= found;
     }
     unsigned long long tot;
     unsigned long long ex = block_exclusive_scan<unsigned long long>((unsigned long long)__popc(keepm), s_red, &tot);

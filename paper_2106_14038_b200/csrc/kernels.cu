@@ -107,6 +107,54 @@ cudaError_t launch_pack_keys(const uint32_t* rowv, const uint32_t* p, const uint
   return cudaGetLastError();
 }
 
+__global__ void k_pack_pso(const uint32_t* __restrict__ s, const uint32_t* __restrict__ p,
+                           const uint32_t* __restrict__ o, uint64_t n, const uint8_t* __restrict__ keep, int nb,
+                           int drop_bit, uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t l = __ldg(p + i);
+    uint64_t k = ((uint64_t)l << (2 * nb)) | ((uint64_t)__ldg(s + i) << nb) | (uint64_t)__ldg(o + i);
+    if (!__ldg(keep + l)) k |= 1ull << drop_bit;
+    keys[i] = k;
+  }
+}
+
+cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n, const uint8_t* keep,
+                            int nb, int drop_bit, uint64_t* keys, cudaStream_t st) {
+  k_pack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(s, p, o, n, keep, nb, drop_bit, keys);
+  return cudaGetLastError();
+}
+
+__global__ void k_unpack_pso(const uint64_t* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ pos,
+                             int drop_bit, int nb, uint32_t* __restrict__ ls, uint32_t* __restrict__ lo,
+                             uint32_t* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t m = (1ull << nb) - 1;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    bool valid = false;
+    uint32_t l = 0xffffffffu;
+    if (i < n) {
+      const uint64_t k = keys[i];
+      valid = !((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k);
+      if (valid) {
+        const uint32_t q = pos[i];
+        l = (uint32_t)(k >> (2 * nb));
+        ls[q] = (uint32_t)((k >> nb) & m);
+        lo[q] = (uint32_t)(k & m);
+      }
+    }
+    const uint32_t peers = __match_any_sync(GSM_FULL, l);
+    const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + l, cnt);
+  }
+}
+
+cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
+                              uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st) {
+  k_unpack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, nb, ls, lo, counts);
+  return cudaGetLastError();
+}
+
 size_t sort_keys_tmp_bytes(uint64_t n, int end_bit) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)n, 0,
@@ -433,6 +481,8 @@ struct FilterArgsT {
   int variant;
   uint32_t word_lo;
   LBArgs claim;
+  SkipIf skip;
+  uint32_t center_slot, seq;
 };
 
 template <typename PT>
@@ -613,17 +663,31 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
   return ok;
 }
 
-// clear the candidate bits of failed rows (one atomicAnd per distinct word per warp)
-__device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row, const bool fail, const uint32_t lane) {
+// clear the candidate bits of failed rows (one atomicAnd per distinct word per
+// warp); `changed` notes whether a bit actually went from 1 to 0
+__device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row, const bool fail, const uint32_t lane,
+                                             bool& changed) {
   const uint32_t word = fail ? (row >> 5) : 0xffffffffu;
   const uint32_t peers = __match_any_sync(GSM_FULL, word);
   const uint32_t bits = __reduce_or_sync(peers, fail ? (1u << (row & 31)) : 0u);
-  if (fail && (int)lane == __ffs(peers) - 1) atomicAnd(cand + word, ~bits);
+  if (fail && (int)lane == __ffs(peers) - 1) changed |= (atomicAnd(cand + word, ~bits) & bits) != 0;
+}
+
+// end of a filter launch: publish "the center's bitmap changed at this sequence"
+template <typename PT>
+__device__ __forceinline__ void note_change(const FilterArgsT<PT>& a, const bool changed) {
+  if (__any_sync(GSM_FULL, changed) && (threadIdx.x & 31) == 0 && a.skip.chg)
+    atomicMax(a.skip.chg + a.center_slot, a.seq);
 }
 
 template <typename PT, bool SIMD>
 __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
   GSM_PDL_ENTRY();
+  if (a.skip.skip()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.ctr + C_FILTER_SKIPPED, 1ull);
+    return;
+  }
+  bool changed = false;
   constexpr uint32_t QCAP = 64;
   __shared__ uint32_t s_q[8][QCAP];  // per-warp queue of candidate rows (< 64)
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -680,7 +744,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
         qn -= 32;
         __syncwarp();
         const bool ok = eval_rows<PT, SIMD>(a, row, true, lane, n_rows, n_scanned, n_matched, n_masked);
-        clear_failed(a.cand, row, !ok, lane);
+        clear_failed(a.cand, row, !ok, lane, changed);
       }
     }
   }
@@ -688,9 +752,10 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     const bool has = lane < qn;
     const uint32_t row = has ? q[lane] : 0u;
     const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched, n_masked);
-    clear_failed(a.cand, row, has && !ok, lane);
+    clear_failed(a.cand, row, has && !ok, lane, changed);
   }
   // one atomic per warp per counter
+  note_change(a, changed);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
@@ -714,6 +779,11 @@ template <typename PT, bool SIMD>
 __global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterArgsT<PT> a, const uint32_t* __restrict__ rows,
                                                           const unsigned long long* __restrict__ d_nrows) {
   GSM_PDL_ENTRY();
+  if (a.skip.skip()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.ctr + C_FILTER_SKIPPED, 1ull);
+    return;
+  }
+  bool changed = false;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n = *d_nrows;
@@ -746,9 +816,10 @@ __global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterA
         if (j == (uint32_t)t) r = row[t];
       const bool has = (hasm >> j) & 1u;
       const bool ok = eval_rows<PT, SIMD, true>(a, r, (pass >> j) & 1u, lane, n_rows, n_scanned, n_matched, n_masked);
-      clear_failed(a.cand, r, has && !ok, lane);
+      clear_failed(a.cand, r, has && !ok, lane, changed);
     }
   }
+  note_change(a, changed);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_rows += __shfl_down_sync(GSM_FULL, n_rows, o);
@@ -807,7 +878,10 @@ __global__ void k_filter_finalize(FilterArgsT<PT> a) {
     const uint32_t row = rec & 0x7fffffffu;
     const int d = (int)(rec >> 31);
     const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
-    if (a.heavy_sat[i] != need) atomicAnd(a.cand + (row >> 5), ~(1u << (row & 31)));
+    if (a.heavy_sat[i] != need) {
+      const uint32_t b = 1u << (row & 31);
+      if ((atomicAnd(a.cand + (row >> 5), ~b) & b) && a.skip.chg) atomicMax(a.skip.chg + a.center_slot, a.seq);
+    }
     a.heavy_sat[i] = 0;
   }
   __syncthreads();
@@ -837,6 +911,7 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
   t.cand = a.cand; t.n_words = a.n_words;
   t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
   t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant; t.word_lo = a.word_lo; t.claim = a.claim;
+  t.skip = a.skip; t.center_slot = a.center_slot; t.seq = a.seq;
   return t;
 }
 
@@ -865,6 +940,117 @@ static cudaError_t group_filter_t(const FilterArgs& a, int sm_count, cudaStream_
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
+}
+
+// ---- push form (label-major streaming).  Each thread takes 8 consecutive
+// entries per step (two 16-byte loads of s and two of o; the label's range is
+// widened to 4-aligned bounds and masked) and already holds the next step's
+// loads while it probes the current ones (software pipeline: ~128 B of stream
+// in flight per thread).  The probes of an entry (center bit, previous marks,
+// neighbour bit) are issued together.  Marks are OR-ed per distinct word
+// across the warp (entries are sorted by (s, o): OUT edges aggregate well).
+constexpr int PU_G = 2;  // 4-entry groups per thread per step
+__device__ __forceinline__ void push_load(const PushArgs& a, uint64_t b4, uint64_t n4, uint64_t g0, uint4 (&vs)[PU_G],
+                                          uint4 (&vo)[PU_G]) {
+#pragma unroll
+  for (int h = 0; h < PU_G; h++) {
+    const uint64_t g = g0 + h;
+    vs[h] = g < n4 ? __ldcs(reinterpret_cast<const uint4*>(a.s + b4) + g) : make_uint4(0, 0, 0, 0);
+    vo[h] = g < n4 ? __ldcs(reinterpret_cast<const uint4*>(a.o + b4) + g) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) k_push_edge(PushArgs a) {
+  GSM_PDL_ENTRY();
+  if (a.skip.skip()) return;
+  if (a.in_cnt && *(volatile const unsigned long long*)a.in_cnt == 0) return;  // no row left to mark
+  const uint64_t b4 = a.beg & ~3ull;
+  const uint64_t n4 = (a.end - b4 + 3) >> 2;  // 4-entry groups
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * PU_G;
+  uint32_t matched = 0;
+  uint64_t base = (uint64_t)blockIdx.x * blockDim.x * PU_G;
+  uint4 vs[PU_G], vo[PU_G];
+  push_load(a, b4, n4, base + (uint64_t)threadIdx.x * PU_G, vs, vo);
+  for (; base < n4; base += step) {  // warp-uniform trip count
+    const uint64_t g0 = base + (uint64_t)threadIdx.x * PU_G;
+    uint32_t ss[4 * PU_G], oo[4 * PU_G];
+#pragma unroll
+    for (int h = 0; h < PU_G; h++) {
+      ss[4 * h] = vs[h].x; ss[4 * h + 1] = vs[h].y; ss[4 * h + 2] = vs[h].z; ss[4 * h + 3] = vs[h].w;
+      oo[4 * h] = vo[h].x; oo[4 * h + 1] = vo[h].y; oo[4 * h + 2] = vo[h].z; oo[4 * h + 3] = vo[h].w;
+    }
+    if (base + step < n4) push_load(a, b4, n4, g0 + step, vs, vo);  // next step, in flight during the probes
+    uint32_t x[4 * PU_G], pc[4 * PU_G], pp[4 * PU_G], pn[4 * PU_G];
+    uint32_t inr = 0;
+#pragma unroll
+    for (int j = 0; j < 4 * PU_G; j++) {
+      const uint64_t k = b4 + 4 * g0 + j;
+      x[j] = a.out ? ss[j] : oo[j];
+      const uint32_t w = a.out ? oo[j] : ss[j];
+      const bool in = k >= a.beg && k < a.end;
+      inr |= (uint32_t)in << j;
+      pc[j] = in ? __ldg(a.cand + (x[j] >> 5)) : 0u;
+      pp[j] = (in && a.sat_in) ? __ldg(a.sat_in + (x[j] >> 5)) : ~0u;
+      pn[j] = (in && a.mode == GE_PROBE) ? __ldg(a.nbr + (w >> 5)) : 0u;
+      oo[j] = w;  // reuse: the neighbour end
+    }
+    // a thread's entries are consecutive: marks of one word are OR-ed locally and
+    // flushed with one atomicOr when the word changes (OUT edges: a row's entries
+    // and neighbouring rows share words; IN edges: one atomic per marked entry)
+    uint32_t cur_w = 0xffffffffu, cur_b = 0;
+#pragma unroll
+    for (int j = 0; j < 4 * PU_G; j++) {
+      const uint32_t w = oo[j];
+      const bool m = a.mode == GE_PROBE ? ((pn[j] >> (w & 31)) & 1u) != 0 : (w == (a.mode == GE_SELF ? x[j] : a.cval));
+      const bool ok = ((inr >> j) & 1u) && ((pc[j] & pp[j]) >> (x[j] & 31) & 1u) && m;
+      if (ok) {
+        const uint32_t word = x[j] >> 5;
+        if (word != cur_w) {
+          if (cur_b) atomicOr(a.sat_out + cur_w, cur_b);
+          cur_w = word;
+          cur_b = 0;
+        }
+        cur_b |= 1u << (x[j] & 31);
+        matched++;
+      }
+    }
+    if (cur_b) atomicOr(a.sat_out + cur_w, cur_b);
+  }
+  matched = __reduce_add_sync(GSM_FULL, matched);
+  if ((threadIdx.x & 31) == 0 && matched) {
+    atomicAdd(a.ctr + C_PUSH_MATCHED, (unsigned long long)matched);
+    atomicAdd(a.out_cnt, (unsigned long long)matched);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.ctr + C_PUSH, (unsigned long long)(a.end - a.beg));
+}
+
+cudaError_t launch_push_edge(const PushArgs& a, int sm_count, cudaStream_t st) {
+  const uint64_t n4 = a.end > a.beg ? (a.end - (a.beg & ~3ull) + 3) / 4 : 0;
+  const uint64_t per_cta = 256ull * PU_G;
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n4 + per_cta - 1) / per_cta, (uint64_t)sm_count * 3));
+  return pdl_launch(k_push_edge, g, 256, st, a);
+}
+
+__global__ void __launch_bounds__(256) k_and_tracked(uint32_t* __restrict__ cand, const uint32_t* __restrict__ sat,
+                                                    uint32_t n_words, SkipIf skip, uint32_t center_slot,
+                                                    uint32_t seq) {
+  GSM_PDL_ENTRY();
+  if (skip.skip()) return;
+  bool changed = false;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
+    const uint32_t c = cand[w], v = c & __ldcs(sat + w);
+    if (v != c) {
+      cand[w] = v;
+      changed = true;
+    }
+  }
+  if (__any_sync(GSM_FULL, changed) && (threadIdx.x & 31) == 0 && skip.chg) atomicMax(skip.chg + center_slot, seq);
+}
+
+cudaError_t launch_and_tracked(uint32_t* cand, const uint32_t* sat, uint32_t n_words, SkipIf skip,
+                               uint32_t center_slot, uint32_t seq, cudaStream_t st, int sm_count) {
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_words + 255) / 256, (uint64_t)sm_count * 8));
+  return pdl_launch(k_and_tracked, g, 256, st, cand, sat, n_words, skip, center_slot, seq);
 }
 
 cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_count, cudaStream_t st,

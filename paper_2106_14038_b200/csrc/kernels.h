@@ -49,6 +49,13 @@ cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos,
                           cudaStream_t st);
 cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned long long* out2,
                                cudaStream_t st);
+// label-major entry lists (the per-predicate form of SURVEY §8 a1): keys
+// (p << 2nb | s << nb | o), sorted and de-duplicated like the CSR keys, unpacked
+// into s/o arrays grouped by label; counts[p] += entries of label p
+cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n, const uint8_t* keep,
+                            int nb, int drop_bit, uint64_t* keys, cudaStream_t st);
+cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
+                              uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st);
 // per-row label signature (Fmt::lmask) from row_ptr + pred
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
                               uint32_t* lmask, cudaStream_t st);
@@ -74,6 +81,30 @@ __host__ __device__ __forceinline__ Fmt<PT> fmt_of(const FmtAny& a) {
   f.lmask = a.lmask;
   return f;
 }
+
+// Change tracking of the candidate bitmaps within one execute: chg[v] = sequence
+// number of the last group evaluation that cleared a bit of variable slot v
+// (0 = unchanged since the seeds).  A re-evaluation of a group (DESIGN.md
+// R-refine) whose neighbour bitmaps are all unchanged since its previous
+// evaluation cannot clear anything: its compaction and filter launches exit at
+// entry (decided on the device, so the per-plan CUDA graph stays valid).
+struct SkipIf {
+  uint32_t* chg = nullptr;   // [32] per variable slot (slot counters, zeroed by k_init_cands)
+  uint32_t nbr_mask = 0;     // variable slots the group probes
+  uint32_t prev = 0;         // sequence of the group's previous evaluation; 0 = never skip
+#ifdef __CUDACC__
+  __device__ __forceinline__ bool skip() const {
+    if (prev == 0) return false;
+    uint32_t m = nbr_mask;
+    while (m) {
+      const int v = __ffs(m) - 1;
+      m &= m - 1;
+      if (*(volatile const uint32_t*)(chg + v) > prev) return false;
+    }
+    return true;
+  }
+#endif
+};
 
 // decoupled look-back state of one launch (lookback.cuh).  The epoch is
 // device-resident (base of the current launch sequence + this launch's offset)
@@ -129,7 +160,34 @@ struct FilterArgs {
   LBArgs claim;             // its counter() is this launch's zeroed chunk counter (dynamic claiming)
   const uint32_t* rows;     // non-null: the center's candidate rows, compacted (row-list path)
   const unsigned long long* d_nrows;  // their count (device)
+  SkipIf skip;              // re-evaluation guard
+  uint32_t center_slot;     // chg[center_slot] = seq when this launch clears a bit
+  uint32_t seq;
 };
+// a4, push form of one incident edge (x, l, w, dir): stream the label-major
+// entries of l, mark sat_out(x) for every entry whose center row x is a
+// candidate (and in sat_in, the previous push edge of the group, if any) and
+// whose other end matches (cand_w probe / constant / self-loop)
+struct PushArgs {
+  const uint32_t* s;
+  const uint32_t* o;
+  uint64_t beg, end;        // entries of label l: [beg, end)
+  uint32_t out;             // 1: center = subject (OUT edge), 0: center = object (IN edge)
+  const uint32_t* cand;     // center bitmap
+  const uint32_t* sat_in;   // nullptr for the group's first push edge
+  uint32_t* sat_out;        // zeroed before the launch
+  const unsigned long long* in_cnt;  // marks of the previous push edge (nullptr: first); 0 -> nothing to do
+  unsigned long long* out_cnt;       // this edge's marks (zeroed before the launch)
+  const uint32_t* nbr;      // GE_PROBE
+  uint32_t mode, cval;
+  SkipIf skip;
+  unsigned long long* ctr;
+};
+cudaError_t launch_push_edge(const PushArgs& a, int sm_count, cudaStream_t st);
+// cand[0, n_words) &= sat (the group's push edges), change-tracked and skippable like the filter
+cudaError_t launch_and_tracked(uint32_t* cand, const uint32_t* sat, uint32_t n_words, SkipIf skip,
+                               uint32_t center_slot, uint32_t seq, cudaStream_t st, int sm_count);
+
 // extra work of the first kernel of an execute (all optional)
 struct InitExtra {
   const volatile uint32_t* h_epoch = nullptr;  // pinned host word: the look-back epoch base
@@ -186,7 +244,7 @@ struct ExpArgs2 {
 inline int compact_launches(uint32_t n_words) { return n_words ? 1 : 0; }
 cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint32_t* ids, uint64_t cap,
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
-                                     cudaStream_t st, uint32_t id_base = 0);
+                                     cudaStream_t st, uint32_t id_base = 0, SkipIf skip = SkipIf());
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,

@@ -164,6 +164,9 @@ static void free_lspm(gsmart_ctx* ctx) {
     dfree(ctx, f.lmask);
     f = Lspm();
   }
+  dfree(ctx, ctx->lm.s);
+  dfree(ctx, ctx->lm.o);
+  ctx->lm = LabelMajor();
   ctx->lspm_gen++;
 }
 
@@ -293,6 +296,49 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
   return GSMART_OK;
 }
 
+// label-major lists (only when the (p, s, o) key fits 63 bits; else the
+// grouped evaluation uses the pull form only)
+static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep) {
+  LabelMajor& L = ctx->lm;
+  const uint64_t n = ctx->n_triples;
+  const int nb = bits_for(ctx->N - 1), pb = bits_for(ctx->P);
+  const int drop_bit = 2 * nb + pb;
+  if (drop_bit >= 64) return GSMART_OK;
+  Scratch sc(ctx);
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  uint32_t *flags = nullptr, *cnt = nullptr;
+  TRY(sc.get(&cnt, (uint64_t)ctx->P + 2));
+  CU(cudaMemsetAsync(cnt, 0, ((size_t)ctx->P + 2) * 4, ctx->st));
+  unsigned long long* tot = ctx->d_ctr + 40;
+  unsigned long long M = 0;
+  if (n) {
+    TRY(sc.get(&keys, n));
+    TRY(sc.get(&keys2, n));
+    TRY(sc.get(&flags, n + 1));
+    CU(launch_pack_pso(ctx->d_s, ctx->d_p, ctx->d_o, n, d_keep, nb, drop_bit, keys, ctx->st));
+    size_t tb = sort_keys_tmp_bytes(n, drop_bit + 1);
+    void* tmp = nullptr;
+    TRY(sc.get((char**)&tmp, tb));
+    CU(sort_keys_u64(tmp, tb, keys, keys2, n, drop_bit + 1, ctx->st));
+    CU(launch_unique_flags(keys2, n, drop_bit, flags, ctx->st));
+    void* stmp = nullptr;
+    TRY(sc.get((char**)&stmp, scan_tmp_bytes(n)));
+    CU(scan_exclusive_u32(flags, flags, n, tot, stmp, ctx->st, nullptr));
+    TRY(readback(ctx, tot, 1, &M));
+  }
+  TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
+  TRY(dalloc(ctx, &L.o, M + 4));
+  if (M) CU(launch_unpack_pso(keys2, n, flags, drop_bit, nb, L.s, L.o, cnt, ctx->st));
+  std::vector<uint32_t> h(ctx->P + 2);
+  CU(cudaMemcpyAsync(h.data(), cnt, h.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  L.off.assign(ctx->P + 2, 0);
+  for (uint32_t l = 0; l + 1 < ctx->P + 2; l++) L.off[l + 1] = L.off[l] + h[l];
+  L.M = M;
+  L.built = true;
+  return GSMART_OK;
+}
+
 extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep_preds, uint32_t n_keep,
                                            uint32_t formats) {
   if (!ctx) return GSMART_E_INVALID_ARG;
@@ -314,6 +360,7 @@ extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep
   CU(cudaMemcpyAsync(d_keep, keep.data(), keep.size(), cudaMemcpyHostToDevice, ctx->st));
   for (int fmt = 0; fmt < 2; fmt++)
     if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_keep));
+  if (formats == (GSMART_CSR | GSMART_CSC)) TRY(build_label_major(ctx, d_keep));
   CU(cudaStreamSynchronize(ctx->st));
   return GSMART_OK;
 }

@@ -34,6 +34,17 @@ struct Lspm {
   unsigned long long heavy_rows = 0, heavy_chunks = 0;
 };
 
+// Label-major entry lists: the kept, de-duplicated triples grouped by predicate,
+// (s, o) ascending within a label: entries of label l are [off[l], off[l+1]).
+// The push form of the grouped evaluation streams them.
+struct LabelMajor {
+  uint32_t* s = nullptr;
+  uint32_t* o = nullptr;
+  std::vector<uint64_t> off;  // host copy, P + 2 entries
+  uint64_t M = 0;
+  bool built = false;
+};
+
 inline int bits_for(uint64_t v) {  // bits to represent values in [0, v]
   int b = 1;
   while (b < 64 && (v >> b) != 0) b++;
@@ -71,6 +82,8 @@ struct Slot {
   uint64_t heavy_gen = ~0ull;          // LSpM generation the heavy buffers were sized for
   uint32_t* frows = nullptr;           // group filter: compacted candidate rows of the center
   uint64_t frows_cap = 0;
+  uint32_t* sat = nullptr;             // push form: two row-mark bitmaps (ping-pong)
+  uint64_t sat_cap = 0;
   uint32_t* cand = nullptr;            // candidate bitmaps of the running plan (stable for graph replay)
   uint64_t cand_words = 0;
   OutTab* h_tab = nullptr;             // pinned: this execute's phase-2 output pointers
@@ -85,7 +98,7 @@ struct Slot {
     uint64_t ws_gen = 0, lspm_gen = 0;
     uint32_t flags = 0, n_lb = 0, off0 = 0;
     std::vector<int> launches;  // kernel launches inside the graph, per kernel class
-    uint64_t filter_main = 0;
+    uint64_t filter_main = 0, push_and = 0;
   };
   std::unordered_map<uint64_t, GraphEntry> graphs;  // (plan uid << 3 | phase tag) -> captured work
 };
@@ -130,6 +143,9 @@ struct gsmart_ctx {
   uint32_t *d_s = nullptr, *d_p = nullptr, *d_o = nullptr;
   int pred_bytes = 1;
   gsm::Lspm f[2];
+  gsm::LabelMajor lm;
+  // push/pull choice per plan (uid -> lspm_gen, per group per edge), DESIGN.md §5
+  std::unordered_map<uint64_t, std::pair<uint64_t, std::vector<std::vector<uint8_t>>>> push_cache;
   uint64_t lspm_gen = 0;
   int filter_variant = 6;               // FilterArgs::variant bits + 4: row-list path (GSMART_FILTER_VARIANT)
   unsigned long long* d_ctr = nullptr;  // load/build scratch

@@ -20,3 +20,11 @@ for K in k_bitmap_compact k_group_filter_rows; do
   fi
 done
 python scripts/make_traffic.py $D/ncu_launches_bench_lubm100.csv profiles/ncu_traffic.json > /dev/null
+python scripts/make_traffic.py $D/ncu_launches_queries_lubm10k.csv profiles/ncu_traffic_u10000.json > /dev/null
+for P in prof_u10000_filter prof_u10000_expand; do
+  if [ -f gpurun_out/$P.ncu-rep ]; then
+    ncu -i gpurun_out/$P.ncu-rep --page raw --csv > $D/ncu_full_${P#prof_}.csv 2>/dev/null
+    python scripts/ncu_summary.py gpurun_out/$P.ncu-rep > $D/ncu_full_${P#prof_}_summary.txt
+    python scripts/ncu_source.py gpurun_out/$P.ncu-rep 25 > $D/ncu_source_${P#prof_}.txt
+  fi
+done

@@ -8,7 +8,7 @@ timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; e
 U=${U:-10000}
 python scripts/prof_queries.py --universities $U --reps 3 2>&1 | grep -v "^ "
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none \
-  -k regex:'k_(init|seed|guard|group|filter|zero|bitmap|seg|expand|prune|compact|enumerate|iota|gather|rank|scatter)' \
+  -k regex:'k_(init|seed|guard|group|filter|zero|bitmap|seg|expand|prune|compact|enumerate|iota|gather|rank|scatter|push|and)' \
   --csv --log-file gpurun_out/qlaunches_u$U.csv python scripts/prof_queries.py --universities $U --reps 1 --queries ${QS:-L1,L7} > gpurun_out/ncu_qprof_u$U.log 2>&1
 echo "ncu rc=$?"; python scripts/ncu_launches.py gpurun_out/qlaunches_u$U.csv | head -80
 timeout 300 python scripts/trace_latency.py > gpurun_out/trace.log 2>&1; echo "trace rc=$?"

@@ -10,7 +10,8 @@ CLASS = {"k_group_filter": "group_filter", "k_group_filter_rows": "group_filter"
          "k_filter_heavy": "group_filter_heavy", "k_expand_lb": "expand_emit",
          "k_seg_scan": "expand_seg", "k_seed_scatter": "seed", "k_bitmap_compact": "compact",
          "k_compact_alive_lb": "prune", "k_prune_mark_d": "prune_mark", "k_enumerate": "enumerate",
-         "k_init_cands": "bitmap", "k_rank_rows": "sort_rows", "k_scatter_rows": "sort_rows"}
+         "k_init_cands": "bitmap", "k_rank_rows": "sort_rows", "k_scatter_rows": "sort_rows",
+         "k_push_edge": "group_filter", "k_and_tracked": "group_filter"}
 
 src, dst = sys.argv[1], sys.argv[2]
 rows = list(csv.reader(open(src)))

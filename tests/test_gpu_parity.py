@@ -409,3 +409,65 @@ def test_pruned_trie_invariants(G, eng):
                 prev_n = n
             assert prev_n == n_rows or L == 0
             G.gsmart_result_free(r)
+
+
+# ------------------------------------------------------------------ push form of a4
+@pytest.fixture(scope="module")
+def eng_push(G):
+    """An engine whose grouped evaluation streams the label-major lists for every
+    edge (GSMART_FILTER_VARIANT bit 8: push form forced, no size threshold)."""
+    import os
+    old = os.environ.get("GSMART_FILTER_VARIANT")
+    os.environ["GSMART_FILTER_VARIANT"] = "14"
+    try:
+        e = G.Engine(0)
+    finally:
+        if old is None:
+            del os.environ["GSMART_FILTER_VARIANT"]
+        else:
+            os.environ["GSMART_FILTER_VARIANT"] = old
+    yield e
+    e.close()
+
+
+def test_push_form_tiny_rows_and_candidates(G, eng_push):
+    """Push (label-major streaming) and pull evaluate the same Eq. 17/21
+    conjunction: rows == brute force and every candidate bitmap ==
+    filter_schedule, refine on and off (skips included)."""
+    for seed in range(400):
+        (s, p, o), n, P, q = tiny.random_case(seed)
+        eng_push.load(s, p, o, n, P)
+        exp = R.brute_force(s, p, o, n, q)
+        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+            rows, cs, _ = _cands(G, eng_push, q, flags)
+            assert _rows(rows) == exp, (seed, q)
+            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine)
+            for v in q.variables:
+                assert _bits_to_set(cs[v], n) == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
+
+
+@pytest.mark.parametrize("src", ["lubm10", "watdiv", "skewed", "powerlaw"])
+def test_push_form_vs_oracle(G, eng_push, src):
+    if src == "lubm10":
+        d = lubm.generate(10)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        qs, N, P = lubm.queries(d), d.n_entities, d.n_predicates
+    elif src == "watdiv":
+        from synth import watdiv
+        d = watdiv.generate(0.01)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        qs, N, P = watdiv.queries(d), d.n_entities, d.n_predicates
+    elif src == "powerlaw":
+        from synth import powerlaw
+        d = powerlaw.generate(400_000, 20_000, 200)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        qs, N, P = powerlaw.queries(d, 10, seed=3), d.n_entities, d.n_predicates
+    else:
+        s, p, o = tiny.random_graph(11, 2000, 3, 150000, skew=1.3)
+        N, P = 2000, 3
+        qs = _data_queries(np.random.default_rng(11), s, p, o, 12)
+    eng_push.load(s, p, o, N, P)
+    ix = OracleIndex(s, p, o)
+    for q, got in zip(qs, eng_push.query_batch(qs)):
+        e = ix.query(q)
+        assert got.shape == e.shape and np.array_equal(got, e), q
