@@ -47,11 +47,17 @@ __device__ __forceinline__ uint32_t ancestor(const LevelTab& t, uint32_t k, uint
 //      non-empty slice hits L2.
 // (A decoupled look-back over thousands of small tiles spent most of its time
 // walking back to the last inclusive prefix.)
-constexpr int BC_T = 256, BC_W = 8, BC_SLICE = BC_W * 32, BC_SUB = BC_SLICE * (BC_T / 32);
+// BC_W words per lane per slice: 8 (32-byte lane loads) for large bitmaps; 1 for
+// small ones, so that a small bitmap still spreads over many CTAs and every
+// warp emits few rounds (latency, not bandwidth, bounds those launches).
+constexpr int BC_T = 256;
 constexpr uint32_t BC_MAX_SLICES = 2048;  // slices per chunk (their counts live in smem)
 constexpr uint32_t BC_MAX_CHUNKS = 8192;
+constexpr uint32_t BC_SMALL_WORDS = 1u << 18;  // bitmaps up to 8M bits use BC_W = 1
 
+template <int BC_W>
 static uint32_t bc_chunk_words(uint32_t n_words, int sm_count) {
+  constexpr uint32_t BC_SLICE = BC_W * 32, BC_SUB = BC_SLICE * (BC_T / 32);
   const uint64_t want = (uint64_t)sm_count * 4;
   const uint64_t per = std::max<uint64_t>(((uint64_t)n_words + want - 1) / want,
                                           ((uint64_t)n_words + BC_MAX_CHUNKS - 1) / BC_MAX_CHUNKS);
@@ -59,12 +65,14 @@ static uint32_t bc_chunk_words(uint32_t n_words, int sm_count) {
   return (uint32_t)std::min<uint64_t>(c, (uint64_t)BC_MAX_SLICES * BC_SLICE);
 }
 
+template <int BC_W>
 __global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restrict__ bm, uint32_t n_words,
                                                         uint32_t chunk, uint32_t* __restrict__ ids, uint64_t cap,
                                                         unsigned long long* d_count, int* overflow, LBArgs lb,
                                                         uint32_t id_base, SkipIf skip) {
   GSM_PDL_ENTRY();
   if (skip.skip()) return;
+  constexpr uint32_t BC_SLICE = BC_W * 32, BC_SUB = BC_SLICE * (BC_T / 32);
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_p;
   __shared__ uint32_t s_tile;
@@ -81,15 +89,17 @@ __global__ void __launch_bounds__(BC_T) k_bitmap_compact(const uint32_t* __restr
   uint32_t wtot = 0;
 #pragma unroll 4
   for (uint32_t si = wib; si < nsl; si += BC_T / 32) {
-    const uint64_t lw = w0 + (uint64_t)si * BC_SLICE + lane * 8;  // this lane's 8 words
+    const uint64_t lw = w0 + (uint64_t)si * BC_SLICE + lane * BC_W;  // this lane's BC_W words
     uint32_t c = 0;
-    if (vec && lw + 8 <= w1) {
+    if (BC_W == 1) {
+      c = lw < w1 ? __popc(__ldcg(bm + lw)) : 0u;
+    } else if (vec && lw + 8 <= w1) {
       const uint4 x = __ldcg(reinterpret_cast<const uint4*>(bm + lw));
       const uint4 y = __ldcg(reinterpret_cast<const uint4*>(bm + lw + 4));
       c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w) + __popc(y.x) + __popc(y.y) + __popc(y.z) +
           __popc(y.w);
     } else {
-      for (uint64_t i = lw; i < std::min<uint64_t>(lw + 8, w1); i++) c += __popc(__ldcg(bm + i));
+      for (uint64_t i = lw; i < std::min<uint64_t>(lw + BC_W, w1); i++) c += __popc(__ldcg(bm + i));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(GSM_FULL, c, o);
@@ -196,10 +206,14 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
                                      cudaStream_t st, uint32_t id_base, SkipIf skip) {
   if (n_words == 0) return cudaMemsetAsync(d_count, 0, 8, st);
-  const uint32_t chunk = bc_chunk_words(n_words, sm_count);
+  const bool small = n_words <= BC_SMALL_WORDS;
+  const uint32_t chunk = small ? bc_chunk_words<1>(n_words, sm_count) : bc_chunk_words<8>(n_words, sm_count);
   const uint32_t nch = (n_words + chunk - 1) / chunk;
   if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
-  pdl_launch(k_bitmap_compact, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
+  if (small)
+    pdl_launch(k_bitmap_compact<1>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
+  else
+    pdl_launch(k_bitmap_compact<8>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
   return cudaGetLastError();
 }
 
@@ -227,18 +241,63 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
     const uint64_t base = (uint64_t)tile * SS_TILE + threadIdx.x * SS_I;
     uint32_t len[SS_I];
     unsigned long long sum = 0;
+    // the SS_I parents of a thread go through each step together (ancestor,
+    // row bounds, lock-step label searches), so their loads overlap
+    uint32_t act = 0, lo[SS_I], hi[SS_I], e[SS_I];
+#pragma unroll
+    for (int j = 0; j < SS_I; j++) {
+      lo[j] = hi[j] = e[j] = 0;
+      if (base + j < F) act |= 1u << j;
+    }
+    if (a.tree) {
+      uint32_t b[SS_I];
+#pragma unroll
+      for (int j = 0; j < SS_I; j++)
+        b[j] = ((act >> j) & 1u) ? ancestor(a.tab, a.k - 1, (uint32_t)(base + j), a.parent_level) : 0u;
+#pragma unroll
+      for (int j = 0; j < SS_I; j++)
+        if ((act >> j) & 1u) {
+          lo[j] = __ldg(f.rp + b[j]);
+          e[j] = hi[j] = __ldg(f.rp + b[j] + 1);
+        }
+      // first entry with label >= l, then first with label > l
+#pragma unroll
+      for (int pass = 0; pass < 2; pass++) {
+        const uint32_t key = a.label + (uint32_t)pass;
+        uint32_t live = act;
+        while (live) {
+#pragma unroll
+          for (int j = 0; j < SS_I; j++) {
+            if (!((live >> j) & 1u)) continue;
+            if (lo[j] >= hi[j]) {
+              live &= ~(1u << j);
+              continue;
+            }
+            const uint32_t m = (lo[j] + hi[j]) >> 1;
+            if ((uint32_t)__ldg(f.pred + m) < key) lo[j] = m + 1; else hi[j] = m;
+          }
+        }
+        if (pass == 0) {
+#pragma unroll
+          for (int j = 0; j < SS_I; j++) {
+            b[j] = lo[j];  // segment begin
+            hi[j] = e[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < SS_I; j++) {
+            hi[j] = lo[j];  // segment end
+            lo[j] = b[j];
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int j = 0; j < SS_I; j++) {
       len[j] = 0;
       const uint64_t n = base + j;
-      if (n < F) {
-        uint32_t beg = 0, l = list_len;
-        if (a.tree) {
-          uint32_t b = ancestor(a.tab, a.k - 1, (uint32_t)n, a.parent_level), lo, hi;
-          label_range(f, b, a.label, lo, hi);
-          beg = lo;
-          l = hi - lo;
-        }
+      if ((act >> j) & 1u) {
+        const uint32_t beg = a.tree ? lo[j] : 0u, l = a.tree ? hi[j] - lo[j] : list_len;
         a.seg_beg[n] = beg;
         len[j] = l;
         sum += l;
