@@ -47,13 +47,12 @@ __device__ __forceinline__ uint32_t ancestor(const LevelTab& t, uint32_t k, uint
 //      non-empty slice hits L2.
 // (A decoupled look-back over thousands of small tiles spent most of its time
 // walking back to the last inclusive prefix.)
-// BC_W words per lane per slice: 8 (32-byte lane loads) for large bitmaps; 1 for
-// small ones, so that a small bitmap still spreads over many CTAs and every
-// warp emits few rounds (latency, not bandwidth, bounds those launches).
-constexpr int BC_T = 256;
+// BC_W words per lane per slice (8: 32-byte lane loads).  BC_W = 1 for small
+// bitmaps (more, shorter CTAs) was measured slower at LUBM-100 (0.29 vs 0.255
+// ms of compaction per batch), so one width serves every size.
+constexpr int BC_T = 256, BC_W_DEFAULT = 8;
 constexpr uint32_t BC_MAX_SLICES = 2048;  // slices per chunk (their counts live in smem)
 constexpr uint32_t BC_MAX_CHUNKS = 8192;
-constexpr uint32_t BC_SMALL_WORDS = 1u << 18;  // bitmaps up to 8M bits use BC_W = 1
 
 template <int BC_W>
 static uint32_t bc_chunk_words(uint32_t n_words, int sm_count) {
@@ -206,14 +205,11 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
                                      cudaStream_t st, uint32_t id_base, SkipIf skip) {
   if (n_words == 0) return cudaMemsetAsync(d_count, 0, 8, st);
-  const bool small = n_words <= BC_SMALL_WORDS;
-  const uint32_t chunk = small ? bc_chunk_words<1>(n_words, sm_count) : bc_chunk_words<8>(n_words, sm_count);
+  const uint32_t chunk = bc_chunk_words<BC_W_DEFAULT>(n_words, sm_count);
   const uint32_t nch = (n_words + chunk - 1) / chunk;
   if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
-  if (small)
-    pdl_launch(k_bitmap_compact<1>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
-  else
-    pdl_launch(k_bitmap_compact<8>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base, skip);
+  pdl_launch(k_bitmap_compact<BC_W_DEFAULT>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb,
+             id_base, skip);
   return cudaGetLastError();
 }
 
