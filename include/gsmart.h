@@ -75,6 +75,7 @@ typedef enum {
 #define GSMART_PROFILE 8u         /* per-kernel CUDA-event timing into gsmart_stats (no graph replay) */
 #define GSMART_KEEP_CANDIDATES 16u /* keep the candidate bitmaps for gsmart_result_candidates */
 #define GSMART_NO_GRAPH 32u       /* launch kernels one by one instead of replaying the plan's CUDA graph */
+#define GSMART_NO_SPECULATE 64u   /* always wait for the level sizes before pruning/rows (no speculative phase 2) */
 
 typedef struct gsmart_ctx gsmart_ctx;
 typedef struct gsmart_plan_s gsmart_plan_t;

@@ -733,6 +733,11 @@ struct Exec {
       if (g.s >= N || g.o >= N) empty = true;
     if (nvar > 0 && !empty) {  // the common path: all device work of phase 1, then one event
       TRY(run_phase1());
+      if (can_speculate()) {  // phase 2 goes behind phase 1 once every plan's phase 1 is queued
+        spec_pending = true;
+        state = S_EXPANDING;
+        return GSMART_OK;
+      }
       CU(cudaEventRecord(sl.ev, sl.st));
       state = S_EXPANDING;
       return GSMART_OK;
@@ -761,6 +766,49 @@ struct Exec {
     TRY(keep_candidates());
     state = S_DONE;
     return GSMART_OK;
+  }
+
+  // Speculative phase 2: a plan re-executed on the same LSpM with the same flags
+  // produces the same level sizes, so phase 2 is sized from the previous run and
+  // queued right behind phase 1 — no host round trip between the phases.  A
+  // device guard (k_phase2_guard) turns every phase-2 kernel into a no-op if a
+  // level would not fit; after the drain the host compares the real sizes with
+  // the guess and, on a mismatch, redoes phase 2 the ordinary way.
+  bool spec = false, spec_pending = false;
+  bool can_speculate() const {
+    if (ctx->world > 1 || (flags & GSMART_NO_SPECULATE)) return false;
+    auto it = ctx->p2_guess.find(plan->uid);
+    if (it == ctx->p2_guess.end() || it->second.gen != ctx->lspm_gen || it->second.flags != flags ||
+        it->second.F.size() != L)
+      return false;
+    for (uint32_t k = 0; k < L; k++)
+      if (it->second.F[k] > sl.lv[k].cap) return false;
+    return true;
+  }
+  gsmart_status speculate() {
+    spec_pending = false;
+    F = ctx->p2_guess.find(plan->uid)->second.F;
+    if (ctx->spec_test && F[L - 1]) F[L - 1] += (ctx->spec_test++ & 1) ? 1 : -1;  // test hook: force a wrong guess
+    for (uint32_t k = 0; k < L && k < GSMART_MAX_LEVELS; k++) R->stats.level_nodes[k] = F[k];
+    TRY(phase2());
+    spec = true;
+    return GSMART_OK;
+  }
+  // after the drain of a speculative run: did phase 1 produce the guessed sizes?
+  bool spec_holds() const {
+    const unsigned long long* hv = sl.h_pin;
+    if (hv[127] & 0xffffffffu) return false;
+    for (uint32_t k = 0; k < L; k++)
+      if (hv[k] != F[k]) return false;
+    return true;
+  }
+  gsmart_status redo_phase2() {  // mis-speculation: the ordinary path from the real sizes
+    spec = false;
+    R->levels.clear();
+    R->d_rows = nullptr;
+    R->n_rows = 0;
+    ctr_pinned = false;
+    return after_expand();
   }
 
   // called once sl.ev completed
@@ -861,13 +909,16 @@ struct Exec {
     }
     std::vector<uint32_t> col_of_level(L);
     for (uint32_t k = 0; k < L; k++) col_of_level[k] = (uint32_t)plan->col_of[plan->levels[k].var];
+    for (uint32_t k = 0; k < L && k < (uint32_t)MAXL; k++) ot.cap[k] = F[k];
+    ot.small_sort = mode == M_SORT_SMALL;
     auto body = [&]() -> gsmart_status {
       CU(cudaMemcpyAsync(sl.d_tab, sl.h_tab, sizeof(OutTab), cudaMemcpyHostToDevice, sl.st));
+      CU(launch_phase2_guard(sl.d_tab, dsz, sl.d_ovf, L, sl.st));
       // phase 1 wrote every counter: read them back with the rest of the stream
       CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
       prof.begin(K_PRUNE);
       for (uint32_t k = L - 1; k >= 1; k--) {
-        CU(launch_prune_mark_d(sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
+        CU(launch_prune_mark_d(sl.d_tab, sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
                                ctx->sm_count, sl.st));
         launches[K_PRUNE]++;
       }
@@ -1055,7 +1106,18 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
     static const bool trace = getenv("GSMART_TRACE") != nullptr;
     const auto tb = std::chrono::steady_clock::now();
     auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb).count(); };
-    for (uint32_t i = 0; i < m; i++) st[i] = ex[i]->start();
+    // start the plans that were the most work last time first (the batch ends
+    // with its longest plan; slots keep their plan, so cached graphs stay valid)
+    std::vector<uint32_t> order(m);
+    for (uint32_t i = 0; i < m; i++) order[i] = i;
+    auto cost = [&](uint32_t i) {
+      auto it = ctx->plan_cost.find(plans[base + i]->uid);
+      return it == ctx->plan_cost.end() ? 0ull : it->second;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cost(x) > cost(y); });
+    for (uint32_t i : order) st[i] = ex[i]->start();
+    for (uint32_t i : order)  // speculative phase 2s, queued while the phase 1s run
+      if (st[i] == GSMART_OK && ex[i]->spec_pending) st[i] = ex[i]->speculate();
     if (trace) fprintf(stderr, "[gsmart] %u plans: phase-1 launched at %.1f us\n", m, us());
     // serve the plans in completion order (a slow plan never holds back the
     // host work of the others): expansion readback -> re-launch on overflow or
@@ -1084,8 +1146,29 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
         progressed = true;
         if (trace) fprintf(stderr, "[gsmart]   plan %u drained at %.1f us\n", i, us());
         if (e != cudaSuccess && st[i] == GSMART_OK) st[i] = cuda_fail(ctx, e, "execute sync", __LINE__);
+        if (st[i] == GSMART_OK && ex[i]->spec) {
+          ex[i]->spec = false;
+          if (!ex[i]->spec_holds()) {
+            if (trace) fprintf(stderr, "[gsmart]   plan %u mis-speculated at %.1f us\n", i, us());
+            st[i] = ex[i]->redo_phase2();
+            if (st[i] == GSMART_OK) continue;  // expanding again or phase 2 queued: drain later
+          }
+        }
+        const bool reached_p2 = ex[i]->state == Exec::S_PHASE2;
         if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
         else ex[i]->prof.flush();
+        if (st[i] == GSMART_OK && reached_p2 && ctx->world == 1) {
+          auto& g = ctx->p2_guess[plans[base + i]->uid];
+          g.gen = ctx->lspm_gen;
+          g.flags = flags;
+          g.F = ex[i]->F;
+        }
+        if (st[i] == GSMART_OK) {
+          const gsmart_stats& s = res[i]->stats;
+          unsigned long long c = s.edges_evaluated + s.filter_rows;
+          for (uint32_t k = 0; k < s.n_levels && k < GSMART_MAX_LEVELS; k++) c += s.level_nodes[k];
+          ctx->plan_cost[plans[base + i]->uid] = c;
+        }
         if (trace) fprintf(stderr, "[gsmart]   plan %u finalized at %.1f us\n", i, us());
         done[i] = 1;
         left--;

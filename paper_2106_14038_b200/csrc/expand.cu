@@ -510,17 +510,33 @@ cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cu
 }
 
 // ------------------------------------------------------------------ a8 prune + compaction
-__global__ void k_prune_mark_d(const uint32_t* __restrict__ parent, const uint8_t* __restrict__ alive,
-                               const unsigned long long* d_n, uint8_t* __restrict__ alive_prev) {
+__global__ void k_phase2_guard(OutTab* ot, const unsigned long long* d_sz, const int* ovf, uint32_t L) {
   GSM_PDL_ENTRY();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int go = *(volatile const int*)ovf == 0;
+  for (uint32_t k = 0; k < L; k++) go = go && d_sz[k] <= ot->cap[k];
+  if (ot->small_sort && L) go = go && d_sz[L - 1] <= SORT_SMALL_MAXN;
+  ot->go = go;
+}
+
+cudaError_t launch_phase2_guard(OutTab* ot, const unsigned long long* d_sz, const int* ovf, uint32_t L,
+                                cudaStream_t st) {
+  return pdl_launch(k_phase2_guard, 1, 32, st, ot, d_sz, ovf, L);
+}
+
+__global__ void k_prune_mark_d(const OutTab* __restrict__ ot, const uint32_t* __restrict__ parent,
+                               const uint8_t* __restrict__ alive, const unsigned long long* d_n,
+                               uint8_t* __restrict__ alive_prev) {
+  GSM_PDL_ENTRY();
+  if (!ot->go) return;
   const uint64_t n = *d_n;
   for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < n; m += (uint64_t)gridDim.x * blockDim.x)
     if (!alive || alive[m]) alive_prev[__ldg(parent + m)] = 1;
 }
 
-cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
-                                uint8_t* alive_prev, int sm_count, cudaStream_t st) {
-  pdl_launch(k_prune_mark_d, (unsigned)sm_count * 8, 256, st, parent, alive, d_n, alive_prev);
+cudaError_t launch_prune_mark_d(const OutTab* ot, const uint32_t* parent, const uint8_t* alive,
+                                const unsigned long long* d_n, uint8_t* alive_prev, int sm_count, cudaStream_t st) {
+  pdl_launch(k_prune_mark_d, (unsigned)sm_count * 8, 256, st, ot, parent, alive, d_n, alive_prev);
   return cudaGetLastError();
 }
 
@@ -535,6 +551,7 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
                                                           uint32_t* __restrict__ newidx,
                                                           unsigned long long* d_count, LBArgs lb) {
   GSM_PDL_ENTRY();
+  if (!ot->go) return;
   uint32_t* __restrict__ out_parent = k ? ot->parent[k] : nullptr;
   uint32_t* __restrict__ out_bind = ot->bind[k];
   __shared__ uint32_t s_tile;

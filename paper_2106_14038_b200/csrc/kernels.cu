@@ -1069,6 +1069,7 @@ struct ColMap {
 __global__ void k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
                             const unsigned long long* __restrict__ d_n_last, uint32_t n_cols) {
   GSM_PDL_ENTRY();
+  if (!ot->go) return;
   const uint32_t n_last = (uint32_t)*d_n_last;
   uint32_t* __restrict__ rows = ot->rows;
   uint32_t* __restrict__ rank = ot->rank;
@@ -1132,6 +1133,7 @@ __global__ void __launch_bounds__(SR_T) k_rank_rows(const OutTab* __restrict__ o
                                                    const unsigned long long* __restrict__ d_n, uint32_t nc) {
   GSM_PDL_ENTRY();
   __shared__ uint32_t s_rows[SR_SMEM_W];
+  if (!ot->go) return;
   const uint32_t n = (uint32_t)*d_n;
   if (blockIdx.x * SR_T >= n) return;
   const uint32_t* __restrict__ rows = ot->rows;
@@ -1162,6 +1164,7 @@ __global__ void __launch_bounds__(SR_T) k_rank_rows(const OutTab* __restrict__ o
 __global__ void k_scatter_rows(const OutTab* __restrict__ ot, const unsigned long long* __restrict__ d_n,
                                uint32_t nc) {
   GSM_PDL_ENTRY();
+  if (!ot->go) return;
   const uint32_t n = (uint32_t)*d_n;
   const uint32_t* __restrict__ rows = ot->rows;
   const uint32_t* __restrict__ rank = ot->rank;

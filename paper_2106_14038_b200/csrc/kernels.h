@@ -247,7 +247,8 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
                                      cudaStream_t st, uint32_t id_base = 0, SkipIf skip = SkipIf());
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
-cudaError_t launch_prune_mark_d(const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
+struct OutTab;
+cudaError_t launch_prune_mark_d(const OutTab* ot, const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
                                 uint8_t* alive_prev, int sm_count, cudaStream_t st);
 // Where phase 2 writes one execute's output.  Phase-2 kernels read these pointers
 // from a device copy of a table the host fills per execute, so a captured phase-2
@@ -258,7 +259,14 @@ struct OutTab {
   uint32_t* rows;          // enumeration output [n_rows x n_cols]
   uint32_t* sorted;        // rank-sort output (rows sorted lexicographically)
   uint32_t* rank;          // rank-sort scratch [SORT_SMALL_MAXN], zeroed by the enumeration
+  unsigned long long cap[MAXL];  // nodes of level k the host sized the outputs for
+  int go;                  // written by k_phase2_guard: every phase-2 kernel exits at entry when 0
+  int small_sort;          // outputs laid out for the rank sort (needs <= SORT_SMALL_MAXN rows)
 };
+// Phase-2 guard (speculative launch): go = no expansion overflow
+// and every level fits the capacity the outputs were sized for.
+cudaError_t launch_phase2_guard(OutTab* ot, const unsigned long long* d_sz, const int* ovf, uint32_t L,
+                                cudaStream_t st);
 constexpr uint32_t SORT_SMALL_MAXN = 8192, SORT_SMALL_MAXC = 16;
 
 cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind, const uint8_t* alive,

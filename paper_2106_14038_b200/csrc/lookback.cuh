@@ -41,8 +41,12 @@ __device__ __forceinline__ uint64_t lb_prefix(unsigned long long* status, uint32
         unsigned long long s = idx >= 0 ? *((volatile unsigned long long*)(status + idx)) : lb_pack(epoch, 2, 0);
         uint32_t ep = (uint32_t)(s >> 48), fl = (uint32_t)((s >> 46) & 3u);
         bool ready = ep == epoch && fl != 0;
-        if (__any_sync(GSM_FULL, !ready)) continue;
-        uint32_t inc = __ballot_sync(GSM_FULL, fl == 2);
+        // only the predecessors up to the nearest inclusive one must be ready
+        // (waiting for the whole 32-tile window stalls on unrelated slow tiles)
+        const uint32_t inc = __ballot_sync(GSM_FULL, ready && fl == 2);
+        const uint32_t notready = __ballot_sync(GSM_FULL, !ready);
+        const uint32_t need = inc ? ((2u << (__ffs(inc) - 1)) - 1u) : GSM_FULL;
+        if (notready & need) continue;
         uint64_t v = s & LB_VMASK;
         if (inc) {
           int k = __ffs(inc) - 1;

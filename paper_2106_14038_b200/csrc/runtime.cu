@@ -107,6 +107,7 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   ctx->cfg = *cfg;
   ctx->sm_count = prop.multiProcessorCount;
   if (const char* fv = getenv("GSMART_FILTER_VARIANT")) ctx->filter_variant = atoi(fv);
+  if (const char* sv = getenv("GSMART_SPEC_TEST")) ctx->spec_test = atoi(sv) ? 1u : 0u;
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     g_static_err = "cudaSetDevice failed";
     return GSMART_E_CUDA;

@@ -146,6 +146,10 @@ struct gsmart_ctx {
   gsm::LabelMajor lm;
   // push/pull choice per plan (uid -> lspm_gen, per group per edge), DESIGN.md §5
   std::unordered_map<uint64_t, std::pair<uint64_t, std::vector<std::vector<uint8_t>>>> push_cache;
+  std::unordered_map<uint64_t, unsigned long long> plan_cost;  // uid -> work of its last execute (batch start order)
+  struct P2Guess { uint64_t gen = 0; uint32_t flags = 0; std::vector<uint64_t> F; };
+  std::unordered_map<uint64_t, P2Guess> p2_guess;
+  uint32_t spec_test = 0;  // GSMART_SPEC_TEST=1: every speculation guesses a wrong row count (tests)  // uid -> level sizes of its last execute (speculative phase 2)
   uint64_t lspm_gen = 0;
   int filter_variant = 6;               // FilterArgs::variant bits + 4: row-list path (GSMART_FILTER_VARIANT)
   unsigned long long* d_ctr = nullptr;  // load/build scratch

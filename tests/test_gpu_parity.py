@@ -471,3 +471,47 @@ def test_push_form_vs_oracle(G, eng_push, src):
     for q, got in zip(qs, eng_push.query_batch(qs)):
         e = ix.query(q)
         assert got.shape == e.shape and np.array_equal(got, e), q
+
+
+# ------------------------------------------------------------------ speculative phase 2
+def test_speculative_phase2_repeats(G, eng):
+    """Re-executions queue phase 2 sized from the previous run (one host wait);
+    rows must equal the oracle on every repeat, single and batched."""
+    d = lubm.generate(3)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = lubm.queries(d)
+    exp = [ix.query(q) for q in qs]
+    with eng.plan(qs[0]) as pl0:
+        for _ in range(3):
+            got = pl0.run(0)
+            assert np.array_equal(got, exp[0])
+    for _ in range(3):
+        for q, e, got in zip(qs, exp, eng.query_batch(qs)):
+            assert got.shape == e.shape and np.array_equal(got, e), q.name
+        assert eng.query(qs[1], flags=G.GSMART_COUNT_ONLY) == exp[1].shape[0]
+
+
+def test_speculative_phase2_wrong_guess(G):
+    """GSMART_SPEC_TEST makes every speculation guess a wrong row count (one
+    fewer: the device guard voids phase 2; one more: the host check rejects it);
+    the ordinary phase 2 must then produce the oracle's rows."""
+    import os
+    os.environ["GSMART_SPEC_TEST"] = "1"
+    try:
+        e = G.Engine(0)
+    finally:
+        del os.environ["GSMART_SPEC_TEST"]
+    try:
+        d = lubm.generate(2)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        e.load(s, p, o, d.n_entities, d.n_predicates)
+        ix = OracleIndex(s, p, o)
+        qs = lubm.queries(d)
+        exp = [ix.query(q) for q in qs]
+        for _ in range(3):
+            for q, x, got in zip(qs, exp, e.query_batch(qs)):
+                assert got.shape == x.shape and np.array_equal(got, x), q.name
+    finally:
+        e.close()
