@@ -869,9 +869,12 @@ struct Exec {
                      : identity ? M_IDENTITY
                                 : (sort_small_ok(n_rows, nc) ? M_SORT_SMALL : M_SORT_BIG);
     auto al = [](uint64_t b) { return (b + 255) / 256 * 256; };
+    // one variable in trie order: the rows are the compacted level-0 bindings
+    // themselves (no enumeration, no second copy)
+    const bool alias_rows = mode == M_IDENTITY && L == 1 && nc == 1;
     uint64_t arena_bytes = 0;
     for (uint32_t k = 0; k < L; k++) arena_bytes += al(F[k] * 4) * (k > 0 ? 2 : 1);
-    if (want_rows) arena_bytes += al(n_rows * nc * 4);
+    if (want_rows && !alias_rows) arena_bytes += al(n_rows * nc * 4);
     char* arena = nullptr;
     TRY(alloc_result((void**)&arena, arena_bytes));
     auto take = [&](uint64_t b) {
@@ -889,7 +892,7 @@ struct Exec {
     }
     size_t tb = 0;
     if (want_rows) {
-      R->d_rows = (uint32_t*)take(n_rows * nc * 4);
+      R->d_rows = alias_rows ? ot.bind[0] : (uint32_t*)take(n_rows * nc * 4);
       ot.rows = ot.sorted = R->d_rows;
       if (mode != M_IDENTITY) {  // enumerate into slot scratch, then sort into the result
         tb = mode == M_SORT_SMALL ? SORT_SMALL_MAXN * 4 : sort_rows_tmp_bytes(n_rows, nc);
@@ -932,7 +935,7 @@ struct Exec {
       }
       prof.end();
       CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
-      if (mode != M_COUNT) {
+      if (mode != M_COUNT && !alias_rows) {
         prof.begin(K_ENUMERATE);
         CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), dsz + 96 + (L - 1), nc, ctx->sm_count, sl.st));
         launches[K_ENUMERATE]++;
