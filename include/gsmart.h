@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define GSMART_ABI_VERSION 1
+#define GSMART_ABI_VERSION 2
 
 typedef enum {
   GSMART_OK = 0,
@@ -181,6 +181,9 @@ gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uint32_t trave
  * paths).  Writes at most cap bytes (NUL-terminated when cap > 0) and sets
  * *need to the full length + 1. */
 gsmart_status gsmart_plan_describe(const gsmart_plan_t* plan, char* buf, size_t cap, size_t* need);
+/* Frees the plan and drops every per-plan cache entry (push/pull decisions,
+ * speculative sizes, captured CUDA graphs) of every live context.  Must not run
+ * concurrently with an execute of any context. */
 void gsmart_plan_free(gsmart_plan_t* plan);
 
 /* Execute plan on the built LSpM: seeds -> grouped incident-edge evaluation
@@ -241,6 +244,8 @@ typedef struct {
   uint64_t level_nodes[GSMART_MAX_LEVELS];   /* F_k before pruning */
   uint64_t level_alive[GSMART_MAX_LEVELS];   /* F_k after pruning */
   uint64_t allgather_bytes;     /* world > 1 */
+  uint32_t spec_phase2;         /* 1: phase 2 (prune, rows) was queued speculatively behind phase 1 */
+  uint32_t spec_redo;           /* 1: the speculation guessed wrong sizes; phase 2 was redone */
   const char* kernel_names[GSMART_NKERNELS];
 } gsmart_stats;
 gsmart_status gsmart_result_stats(const gsmart_result* r, gsmart_stats* out);

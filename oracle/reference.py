@@ -181,6 +181,33 @@ def binding_vector(M):
     return out
 
 
+def binding_matrix_rows(A, v, p):
+    """Eqs. 15/18-19: M = p x I (x) (diag(v) x A):
+    entries of label p in the rows selected by the binding vector v."""
+    A = np.asarray(A)
+    S = np.diag(np.asarray(v, dtype=int))
+    return predicate_positions(row_selection(S, A), p)
+
+
+def binding_matrix_cols(A, v, p):
+    """Eqs. 22-23: M = p x I (x) (A x diag(v)): entries of
+    label p in the columns selected by v (M(k, i) = 1 iff A(k, i) = p, v(i))."""
+    A = np.asarray(A)
+    S = np.diag(np.asarray(v, dtype=int))
+    return predicate_positions(column_selection(A, S), p)
+
+
+def neighbour_bindings(A, v_x, p, x_is_subject):
+    """Binding vector of the other end w of an evaluated edge (x, p, w) or
+    (w, p, x), given x's binding vector v_x: Eq. 14 over the binding matrix of
+    Eqs. 15/19 (x the subject: v_w = OR of the rows of M_xw) or of Eqs. 22-23
+    (x the object: M_wx has x in the columns, v_w = OR of the rows of
+    M_wx^T)."""
+    if x_is_subject:
+        return binding_vector(binding_matrix_rows(A, v_x, p))
+    return binding_vector(binding_matrix_cols(A, v_x, p).T)
+
+
 def grouped_eval_out_out(A, p_xy, p_xz):
     """Eq. 17 (P:L307): v_x = (A (x) u_pxy) AND (A (x) u_pxz)."""
     return vector_and(row_predicate_test(A, p_xy), row_predicate_test(A, p_xz))
@@ -254,15 +281,6 @@ def lspm_arrays(s, p, o, n_entities, keep=None, fmt="csr"):
     return {"row_ptr": row_ptr, "col": col, "pred": pred, "label_pairs": pairs, "max_pred": P}
 
 
-def label_row_lists(s, p, o, n_predicates, keep=None, fmt="csr"):
-    """For each label l in 1..P the ascending rows with >= 1 entry of l."""
-    T = triple_set(s, p, o, keep)
-    out = {l: set() for l in range(1, int(n_predicates) + 1)}
-    for a, b, c in T:
-        out.setdefault(b, set()).add(a if fmt == "csr" else c)
-    return {l: sorted(v) for l, v in out.items()}
-
-
 # --------------------------------------------------------------------------
 # §6.1.2 degree-driven traversal (P:L385-L398) + trie order (§7.1)
 # --------------------------------------------------------------------------
@@ -278,6 +296,8 @@ def plan_degree(q):
       roots   : Root_r in order
       groups  : list of (center, [(edge, dir, neighbour)]) in evaluation order;
                 dir OUT = the center is the edge's subject (CSR row), IN = object
+      back    : per group, the center's variable-variable patterns evaluated
+                at earlier centers, same (edge, dir, neighbour) form
       level   : per group, DFS depth of its center (edge level, R-level)
       pi      : variable visitation order (trie levels; DESIGN "trie")
       tree    : {var: (edge, parent_var, dir-from-parent)} for non-root vars
@@ -300,7 +320,7 @@ def plan_degree(q):
     def unev_out(v):
         return sum(1 for k, (a, _, b) in enumerate(E) if k not in F and a == v)
 
-    groups, roots, glevel = [], [], []
+    groups, roots, glevel, back = [], [], [], []
     depth = {}
     first_parent = {}
     while len(F) < len(E):
@@ -316,6 +336,10 @@ def plan_degree(q):
         S = [root]
         while S:                                         # step 3
             v = S.pop()
+            # patterns of v already evaluated at an earlier center (variables at
+            # both ends): Eq. 16 restricts v's rows by their binding vectors
+            bk = [(k, OUT if a == v else IN, b if a == v else a) for k, (a, _, b) in enumerate(E)
+                  if k in F and (a == v or b == v) and a != b and not is_c[a] and not is_c[b]]
             grp = []
             for k, (a, l, b) in enumerate(E):           # step 4
                 if k in F or (a != v and b != v):
@@ -338,6 +362,7 @@ def plan_degree(q):
             if grp:
                 groups.append((v, grp))
                 glevel.append(depth[v])
+                back.append(bk)
     # trie order pi, tree edges, closing edges
     pi, tree, closing = [], {}, {}
     pos = {}
@@ -384,29 +409,41 @@ def plan_degree(q):
                     out.append(acc + [w])
         walk(r, [r])
         paths[r] = out
-    return {"seeds": seeds, "roots": roots, "groups": groups, "level": glevel,
+    return {"seeds": seeds, "roots": roots, "groups": groups, "back": back, "level": glevel,
             "pi": pi, "tree": tree, "closing": closing, "paths": paths}
 
 
 # --------------------------------------------------------------------------
-# Filter schedule: seeds (light edges) then grouped incident-
-# edge evaluation (§5 Eqs. 17/21) per group in plan order, then one backward
-# re-evaluation of the groups (R-refine).  Bitmaps as bool arrays.
+# Filter schedule: seeds (light edges), then every group center
+# in plan order is "revised" against all its incident patterns (§5 Eqs. 17/21
+# for the group's unevaluated edges; Eqs. 14-16 for the already evaluated
+# ones, whose binding vectors restrict the center's rows), then the centers
+# again in reverse order (R-refine).  Bitmaps as bool arrays.
 # --------------------------------------------------------------------------
 
 
 def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
-    """Candidate sets per variable after the product's documented schedule:
-      1. cand_v = [0, N) for every variable;
-      2. each seed edge in edge-index order: (c -l-> v): cand_v &= {o:(c,l,o)};
-         (v -l-> c): cand_v &= {s:(s,l,c)}; const-const: guard (false => all
-         candidate sets empty);
-      3. each group (x, E_x) in plan order: cand_x &= AND_e y_e with
-         y_e(i) = OR_{j} [(i,l,j) in T] ^ cand_w(j) for OUT edges,
-                  OR_{j} [(j,l,i) in T] ^ cand_w(j) for IN edges,
-         self-loop: y(i) = [(i,l,i) in T]          (Eqs. 17/21, 14-16)
-      4. if refine: groups again in reverse plan order, skipping the last.
-    Returns {var: np.bool_ array of length N}, guard flag."""
+    """Candidate sets per variable after the schedule DESIGN.md states:
+      1. cand_v = [0, N) for every variable (Eq. 4/5 with no constraint yet);
+      2. each seed edge in edge-index order (light edges):
+         (c -l-> v): cand_v &= {o : (c,l,o) in T}; (v -l-> c): cand_v &=
+         {s : (s,l,c) in T} (a constant absent from the data, id >= N
+         included, has no entries: the set is empty, R12); const-const
+         pattern: a guard (R13); a false guard makes the conjunction
+         unsatisfiable, so every candidate set is emptied;
+      3. revise(x) for each group center x in plan order, where
+         revise(x): cand_x &= AND_e y_e over EVERY pattern e incident to x
+         whose other end is a variable (or x itself):
+           e = (x, l, w): y_e(i) = OR_j [(i,l,j) in T] ^ cand_w(j)   (Eq. 17)
+           e = (w, l, x): y_e(i) = OR_j [(j,l,i) in T] ^ cand_w(j)   (Eq. 21)
+           e = (x, l, x): y_e(i) = [(i,l,i) in T]                    (R7)
+         For the group's unevaluated edges this is §5 (Eqs. 17/21 with the
+         neighbours' binding vectors as the diag(.) selections of Eqs.
+         15-16); for edges already evaluated at an earlier center c it is
+         Eq. 16's restriction of x's rows to c's Eq. 14 binding vector;
+      4. if refine: revise(x) for the centers in reverse plan order, the last
+         one skipped (nothing it reads changed after it).
+    Returns ({var: np.bool_ array of length N}, guards_hold)."""
     N = int(n_entities)
     T = triple_set(s, p, o)
     plan = plan or plan_degree(q)
@@ -419,9 +456,6 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
     for k in plan["seeds"]:
         a, l, b = q.edges[k]
         ca, cb = q.vertices[a], q.vertices[b]
-        if (ca is not None and ca >= N) or (cb is not None and cb >= N):
-            ok = False   # a constant absent from the data: empty answer (R12)
-            continue
         if ca is not None and cb is not None:
             ok = ok and ((ca, l, cb) in T)
             continue
@@ -438,27 +472,30 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
         for v in cand:
             cand[v][:] = False
 
-    def eval_group(x, grp):
+    def revise(x):
         y_all = np.ones(N, dtype=bool)
-        for k, d, w in grp:
-            l = q.edges[k][1]
+        for a, l, b in q.edges:
+            if x not in (a, b) or q.vertices[a] is not None or q.vertices[b] is not None:
+                continue
             y = np.zeros(N, dtype=bool)
             for i in range(N):
                 if not cand[x][i]:
                     continue
-                if w == x:
+                if a == b:
                     y[i] = (i, l, i) in T
+                elif a == x:
+                    y[i] = any(cand[b][j] for j in out_nb.get((i, l), []))
                 else:
-                    nb = out_nb.get((i, l), []) if d == OUT else in_nb.get((i, l), [])
-                    y[i] = any(cand[w][j] for j in nb)
+                    y[i] = any(cand[a][j] for j in in_nb.get((i, l), []))
             y_all &= y
         cand[x] &= y_all
 
-    for x, grp in plan["groups"]:
-        eval_group(x, grp)
+    centers = [x for x, _ in plan["groups"]]
+    for x in centers:
+        revise(x)
     if refine:
-        for x, grp in list(reversed(plan["groups"]))[1:]:
-            eval_group(x, grp)
+        for x in list(reversed(centers))[1:]:
+            revise(x)
     return cand, ok
 
 
@@ -470,8 +507,12 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
 
 def query_hops(q, var):
     """Largest undirected distance (in pattern edges) from variable `var` to any
-    vertex of q: every triple of a solution touches a vertex within hops-1 of
-    var's binding, so the triples within `hops` of it contain the solution."""
+    vertex of q, walking through variables only: every triple of a solution
+    has an endpoint bound to a variable within hops-1 of var's binding, so the
+    triples within `hops` of it contain the solution.  A walk does not pass
+    through a constant (its entity may be a hub joined to unrelated data), so a
+    variable reachable from `var` only through a constant makes the local
+    method inapplicable: ValueError (never a silently incomplete subset)."""
     adj = {i: set() for i in range(q.n_vertices)}
     for a, _, b in q.edges:
         adj[a].add(b)
@@ -480,13 +521,16 @@ def query_hops(q, var):
     while frontier:
         nxt = []
         for v in frontier:
-            if q.vertices[v] is not None and v != var:
-                continue  # constants do not extend a walk: their triples are reached from a variable
+            if q.vertices[v] is not None:
+                continue  # a constant ends the walk (its own patterns were reached from a variable)
             for w in adj[v]:
                 if w not in dist:
                     dist[w] = dist[v] + 1
                     nxt.append(w)
         frontier = nxt
+    missing = [v for v in q.variables if v not in dist]
+    if missing:
+        raise ValueError(f"variables {missing} are joined to {var} only through constants")
     return max(dist.values())
 
 

@@ -214,7 +214,8 @@ struct Exec {
   int launches[GSMART_NKERNELS] = {0};
   uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
   uint32_t filter_seq = 0;             // group evaluations issued so far (SkipIf sequence)
-  std::vector<std::vector<uint8_t>> push_dec;  // per group, per edge: push form (label-major)
+  std::vector<std::vector<GroupEdge>> gedges;  // per group: its edges, then its back edges (Eq. 16)
+  std::vector<std::vector<uint8_t>> push_dec;  // per group, per edge of gedges: push form (label-major)
   uint64_t push_and = 0;               // k_and_tracked launches (bitmap bytes)
   std::vector<uint32_t> group_seq;     // per group: sequence of its last evaluation
   int attempts = 0;
@@ -243,18 +244,11 @@ struct Exec {
 
   // ---- a3: seeds (light edges) and guards.  The first seed of a variable is
   // scattered into its bitmap; further seeds become constant-target filter edges.
-  gsmart_status seeds_and_guards(bool* empty) {
+  // A constant id >= N is an entity absent from the data (R12): its segments are
+  // empty, so a seed from it empties its variable's candidate set (no scatter)
+  // and a guard on it is false.
+  gsmart_status seeds_and_guards() {
     const uint32_t N = ctx->N;
-    *empty = false;
-    for (auto& sd : plan->seeds)
-      if (sd.cid >= N) *empty = true;
-    for (auto& g : plan->guards)
-      if (g.s >= N || g.o >= N) *empty = true;
-    if (*empty) {  // a constant outside the data: every candidate set is empty (R12)
-      if (!plan->vars.empty())
-        CU(cudaMemsetAsync(sl.cand, 0, (size_t)Wpad * plan->vars.size() * 4, sl.st));
-      return GSMART_OK;
-    }
     std::vector<std::vector<const Seed*>> by_var(plan->n_vertices);
     for (auto& sd : plan->seeds) by_var[sd.var].push_back(&sd);
     uint32_t ones = 0;
@@ -276,9 +270,12 @@ struct Exec {
     }
     int* flag = (int*)(sl.d_ctr + 48);
     if (!plan->guards.empty()) {
-      CU(cudaMemsetAsync(flag, 0xff, 4, sl.st));  // nonzero = guards hold
+      bool absent = false;
+      for (auto& g : plan->guards) absent = absent || g.s >= N || g.o >= N;
+      CU(cudaMemsetAsync(flag, absent ? 0 : 0xff, 4, sl.st));  // nonzero = guards hold
       prof.begin(K_SEED);
       for (auto& g : plan->guards) {
+        if (absent) break;
         CU(launch_guard(fa[0], ctx->pred_bytes, g.s, g.label, g.o, flag, sl.st));
         launches[K_SEED]++;
       }
@@ -290,7 +287,7 @@ struct Exec {
     sb.f[1] = fa[1];
     for (uint32_t v : plan->vars) {
       const auto& ss = by_var[v];
-      if (ss.empty()) continue;
+      if (ss.empty() || ss[0]->cid >= N) continue;  // absent constant: the zeroed bitmap is the seed
       if (sb.n == MAX_SEEDS) FAIL(GSMART_E_UNSUPPORTED, "more than 16 seeded variables");
       sb.dir[sb.n] = ss[0]->dir == OUT ? 0 : 1;
       sb.c[sb.n] = ss[0]->cid;
@@ -310,9 +307,9 @@ struct Exec {
         // (c -l-> v): v's CSC row must hold (l, c); (v -l-> c): v's CSR row must hold (l, c)
         Group g;
         g.center = v;
-        for (size_t i = 1; i < ss.size(); i++)
+        for (size_t i = 1; i < ss.size(); i++)  // an absent constant (>= N) matches no column
           g.edges.push_back({ss[i]->edge, ss[i]->label, ss[i]->dir == OUT ? (uint32_t)IN : (uint32_t)OUT,
-                             0x80000000u | ss[i]->cid});
+                             0x80000000u | std::min(ss[i]->cid, N)});
         TRY(eval_group(g, SIZE_MAX));  // constant-target filter edges: evaluated once
       }
     }
@@ -330,8 +327,9 @@ struct Exec {
   gsmart_status eval_group(const Group& g, size_t gi) {
     std::vector<const GroupEdge*> by[2], push;
     const std::vector<uint8_t>* dec = gi < push_dec.size() ? &push_dec[gi] : nullptr;
-    for (size_t ei = 0; ei < g.edges.size(); ei++) {
-      const GroupEdge& e = g.edges[ei];
+    const std::vector<GroupEdge>& GE = gi < gedges.size() ? gedges[gi] : g.edges;
+    for (size_t ei = 0; ei < GE.size(); ei++) {
+      const GroupEdge& e = GE[ei];
       if (dec && (*dec)[ei]) push.push_back(&e);
       else by[e.dir == OUT ? 0 : 1].push_back(&e);
     }
@@ -348,7 +346,7 @@ struct Exec {
     const uint32_t prev = gi < group_seq.size() ? group_seq[gi] : 0u;
     if (prev && ctx->world == 1) {
       sk.prev = prev;
-      for (auto& e : g.edges)
+      for (auto& e : GE)
         if (!(e.nbr & 0x80000000u) && e.nbr != g.center) sk.nbr_mask |= 1u << slot[e.nbr];
     }
     if (gi < group_seq.size()) group_seq[gi] = seq;
@@ -574,13 +572,14 @@ struct Exec {
     push_dec.resize(plan->groups.size());
     for (size_t gi = 0; gi < plan->groups.size(); gi++) {
       const Group& g = plan->groups[gi];
-      push_dec[gi].assign(g.edges.size(), 0);
+      const std::vector<GroupEdge>& GE = gedges[gi];
+      push_dec[gi].assign(GE.size(), 0);
       // in ascending label size (the launch order); a pushed edge bounds the
       // center's candidates by its label's entry count for the next decision
-      std::vector<size_t> ord(g.edges.size());
+      std::vector<size_t> ord(GE.size());
       for (size_t ei = 0; ei < ord.size(); ei++) ord[ei] = ei;
       auto M_of = [&](size_t ei) {
-        const uint32_t l = g.edges[ei].label;
+        const uint32_t l = GE[ei].label;
         return l + 1 < ctx->lm.off.size() ? ctx->lm.off[l + 1] - ctx->lm.off[l] : 0ull;
       };
       std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return M_of(x) < M_of(y); });
@@ -613,10 +612,9 @@ struct Exec {
   // phase 1 = seeds + grouped evaluation + expansion: pure device work on
   // stable workspace addresses, launched directly or replayed from a graph
   gsmart_status phase1_kernels() {  // counters/sizes are zeroed by k_init_cands
-    bool empty = false;
     group_seq.assign(plan->groups.size(), 0);
     filter_seq = 0;
-    TRY(seeds_and_guards(&empty));
+    TRY(seeds_and_guards());
     for (size_t i = 0; i < plan->groups.size(); i++) TRY(eval_group(plan->groups[i], i));
     if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
       for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i], i));
@@ -719,6 +717,11 @@ struct Exec {
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].closing.size() > (size_t)MAXC)
         FAIL(GSMART_E_UNSUPPORTED, "more than 16 closing edges on one level");
+    gedges.resize(plan->groups.size());
+    for (size_t gi = 0; gi < plan->groups.size(); gi++) {
+      gedges[gi] = plan->groups[gi].edges;
+      gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
+    }
     TRY(decide_push());
     TRY(ensure_workspace());
     TRY(begin_seq(ctx, sl));
@@ -726,12 +729,7 @@ struct Exec {
     F.assign(L, 0);
     R->stats.n_levels = L;
 
-    bool empty = false;
-    for (auto& sd : plan->seeds)
-      if (sd.cid >= N) empty = true;
-    for (auto& g : plan->guards)
-      if (g.s >= N || g.o >= N) empty = true;
-    if (nvar > 0 && !empty) {  // the common path: all device work of phase 1, then one event
+    if (nvar > 0) {  // the common path: all device work of phase 1, then one event
       TRY(run_phase1());
       if (can_speculate()) {  // phase 2 goes behind phase 1 once every plan's phase 1 is queued
         spec_pending = true;
@@ -742,28 +740,16 @@ struct Exec {
       state = S_EXPANDING;
       return GSMART_OK;
     }
+    // only guards (or nothing): one empty row iff all hold
     CU(cudaMemsetAsync(sl.d_ctr, 0, C_NCTR * 8, sl.st));
-    TRY(seeds_and_guards(&empty));
-    if (nvar == 0) {  // only guards (or nothing): one empty row iff all hold
-      uint64_t rows = 0;
-      if (!empty) {
-        int flag = 1;
-        if (!plan->guards.empty()) {
-          CU(cudaMemcpyAsync(&flag, sl.d_ctr + 48, 4, cudaMemcpyDeviceToHost, sl.st));
-          CU(cudaStreamSynchronize(sl.st));
-        }
-        rows = flag ? 1 : 0;
-      }
-      R->n_rows = rows;
-      R->host_valid = true;
-      state = S_DONE;
-      return GSMART_OK;
+    TRY(seeds_and_guards());
+    int flag = 1;
+    if (!plan->guards.empty()) {
+      CU(cudaMemcpyAsync(&flag, sl.d_ctr + 48, 4, cudaMemcpyDeviceToHost, sl.st));
+      CU(cudaStreamSynchronize(sl.st));
     }
-    // a constant outside the data: empty result, all candidate sets empty
-    R->n_rows = 0;
+    R->n_rows = flag ? 1 : 0;
     R->host_valid = true;
-    for (auto& Lv : plan->levels) R->levels.push_back({Lv.var, 0, nullptr, nullptr});
-    TRY(keep_candidates());
     state = S_DONE;
     return GSMART_OK;
   }
@@ -785,13 +771,16 @@ struct Exec {
       if (it->second.F[k] > sl.lv[k].cap) return false;
     return true;
   }
+  size_t spec_owned0 = 0;  // R->owned entries before the speculative phase 2
   gsmart_status speculate() {
     spec_pending = false;
     F = ctx->p2_guess.find(plan->uid)->second.F;
     if (ctx->spec_test && F[L - 1]) F[L - 1] += (ctx->spec_test++ & 1) ? 1 : -1;  // test hook: force a wrong guess
     for (uint32_t k = 0; k < L && k < GSMART_MAX_LEVELS; k++) R->stats.level_nodes[k] = F[k];
+    spec_owned0 = R->owned.size();
     TRY(phase2());
     spec = true;
+    R->stats.spec_phase2 = 1;
     return GSMART_OK;
   }
   // after the drain of a speculative run: did phase 1 produce the guessed sizes?
@@ -804,6 +793,12 @@ struct Exec {
   }
   gsmart_status redo_phase2() {  // mis-speculation: the ordinary path from the real sizes
     spec = false;
+    R->stats.spec_redo = 1;
+    // the speculative outputs (arena, candidate copy) are dead: free them before
+    // the redo allocates its own (the stream is drained)
+    for (size_t i = spec_owned0; i < R->owned.size(); i++) dfree(sl.st, R->owned[i]);
+    R->owned.resize(spec_owned0);
+    R->d_cand = nullptr;
     R->levels.clear();
     R->d_rows = nullptr;
     R->n_rows = 0;
@@ -1056,9 +1051,7 @@ struct Exec {
     for (int i = 0; i < GSMART_NKERNELS; i++) st.launches[i] = (uint64_t)launches[i];
     for (int i = 0; i < GSMART_NKERNELS; i++) st.kernel_names[i] = kKernelNames[i];
     if (!(flags & (GSMART_KEEP_ON_DEVICE | GSMART_COUNT_ONLY)) && R->d_rows && R->n_rows) {
-      R->h_rows.resize(R->n_rows * R->n_cols);
-      CU(cudaMemcpy(R->h_rows.data(), R->d_rows, R->n_rows * R->n_cols * 4, cudaMemcpyDeviceToHost));
-      R->host_valid = true;
+      if (ctx->world == 1 || ctx->rank == 0) TRY(rows_to_host(ctx, R, sl.st));
     } else if (!R->n_rows && !(flags & GSMART_COUNT_ONLY)) {
       R->host_valid = true;
     }

@@ -22,6 +22,10 @@ struct Group {
   uint32_t center;
   uint32_t level;  // DFS depth of the center from its root (edge level)
   std::vector<GroupEdge> edges;
+  // the center's variable-variable patterns already evaluated at earlier
+  // centers: Eq. 16 restricts the center's rows by their binding
+  // vectors, so every evaluation of the group also tests them
+  std::vector<GroupEdge> back;
 };
 struct Seed {      // light edge: constant c, variable v
   uint32_t edge, var, label, cid;

@@ -1,8 +1,6 @@
 // sm_100a kernels of the gSmart hot path (§5-§8).
 // Every kernel here is HBM/L2-bound integer/boolean work: no tensor cores
 // (not a dense contraction — BASELINE.json north_star).
-#include <cub/device/device_radix_sort.cuh>
-
 #include "kernels.h"
 
 namespace gsm {
@@ -155,18 +153,6 @@ cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* 
   return cudaGetLastError();
 }
 
-size_t sort_keys_tmp_bytes(uint64_t n, int end_bit) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)n, 0,
-                                 end_bit);
-  return bytes;
-}
-
-cudaError_t sort_keys_u64(void* tmp, size_t tmp_bytes, const uint64_t* in, uint64_t* out, uint64_t n, int end_bit,
-                          cudaStream_t st) {
-  return cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, in, out, (int64_t)n, 0, end_bit, st);
-}
-
 __global__ void k_unique_flags(const uint64_t* __restrict__ keys, uint64_t n, int drop_bit,
                                uint32_t* __restrict__ flags) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -217,6 +203,91 @@ cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos,
     k_unpack<uint8_t><<<g, 256, 0, st>>>(keys, n, pos, drop_bit, sh_row, sh_pred, col, (uint8_t*)pred, counts);
   else
     k_unpack<uint16_t><<<g, 256, 0, st>>>(keys, n, pos, drop_bit, sh_row, sh_pred, col, (uint16_t*)pred, counts);
+  return cudaGetLastError();
+}
+
+// ---- keys wider than 63 bits (e.g. 27 + 14 + 27 bits: 100M entities, 10,000
+// labels): hi = row << pb | pred (drop flag at bit drop_hi), lo = col; sorted
+// by lo then stably by hi (two LSD key groups, radix.cu)
+// mode 0 (LSpM format): hi = a << sh | pred; mode 1 (label-major): hi = pred << sh | a; lo = b
+__global__ void k_pack_keys2(const uint32_t* __restrict__ a, const uint32_t* __restrict__ p,
+                             const uint32_t* __restrict__ b, uint64_t n, const uint8_t* __restrict__ keep, int mode,
+                             int sh, int drop_hi, uint64_t* __restrict__ hi, uint32_t* __restrict__ lo) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t l = __ldg(p + i);
+    const uint64_t x = __ldg(a + i);
+    uint64_t h = mode == 0 ? ((x << sh) | (uint64_t)l) : (((uint64_t)l << sh) | x);
+    if (!__ldg(keep + l)) h |= 1ull << drop_hi;
+    hi[i] = h;
+    lo[i] = __ldg(b + i);
+  }
+}
+
+cudaError_t launch_pack_keys2(const uint32_t* a, const uint32_t* p, const uint32_t* b, uint64_t n, const uint8_t* keep,
+                              int mode, int sh, int drop_hi, uint64_t* hi, uint32_t* lo, cudaStream_t st) {
+  k_pack_keys2<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(a, p, b, n, keep, mode, sh, drop_hi, hi, lo);
+  return cudaGetLastError();
+}
+
+__global__ void k_unique_flags2(const uint64_t* __restrict__ hi, const uint32_t* __restrict__ lo, uint64_t n,
+                                int drop_hi, uint32_t* __restrict__ flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = hi[i];
+    const uint32_t l = lo[i];
+    flags[i] = (!((h >> drop_hi) & 1ull) && (i == 0 || hi[i - 1] != h || lo[i - 1] != l)) ? 1u : 0u;
+  }
+}
+
+cudaError_t launch_unique_flags2(const uint64_t* hi, const uint32_t* lo, uint64_t n, int drop_hi, uint32_t* flags,
+                                 cudaStream_t st) {
+  k_unique_flags2<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(hi, lo, n, drop_hi, flags);
+  return cudaGetLastError();
+}
+
+// unpack of the two-word keys: mode 0 = LSpM format (row = hi >> pb, pred = low
+// pb bits of hi, col = lo; row counts), mode 1 = label-major (label = hi >> nb,
+// s = low nb bits of hi, o = lo; label counts)
+template <typename PT>
+__global__ void k_unpack2(const uint64_t* __restrict__ hi, const uint32_t* __restrict__ lo, uint64_t n,
+                          const uint32_t* __restrict__ pos, int drop_hi, int sh, int mode, uint32_t* __restrict__ a_out,
+                          PT* __restrict__ pred, uint32_t* __restrict__ b_out, uint32_t* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lowmask = (1ull << sh) - 1;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    bool valid = false;
+    uint32_t key = 0xffffffffu;
+    if (i < n) {
+      const uint64_t h = hi[i];
+      const uint32_t l = lo[i];
+      valid = !((h >> drop_hi) & 1ull) && (i == 0 || hi[i - 1] != h || lo[i - 1] != l);
+      if (valid) {
+        const uint32_t q = pos[i];
+        const uint32_t top = (uint32_t)((h & ~(1ull << drop_hi)) >> sh), low = (uint32_t)(h & lowmask);
+        if (mode == 0) {  // LSpM: col, pred; count rows
+          a_out[q] = l;
+          pred[q] = (PT)low;
+        } else {          // label-major: s, o; count labels
+          a_out[q] = low;
+          b_out[q] = l;
+        }
+        key = top;
+      }
+    }
+    const uint32_t peers = __match_any_sync(GSM_FULL, key);
+    const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + key, cnt);
+  }
+}
+
+cudaError_t launch_unpack2(const uint64_t* hi, const uint32_t* lo, uint64_t n, const uint32_t* pos, int drop_hi, int sh,
+                           int mode, uint32_t* a_out, void* pred, int pred_bytes, uint32_t* b_out, uint32_t* counts,
+                           cudaStream_t st) {
+  const unsigned g = grid_for(n, 256, 148 * 32);
+  if (pred_bytes == 1)
+    k_unpack2<uint8_t><<<g, 256, 0, st>>>(hi, lo, n, pos, drop_hi, sh, mode, a_out, (uint8_t*)pred, b_out, counts);
+  else
+    k_unpack2<uint16_t><<<g, 256, 0, st>>>(hi, lo, n, pos, drop_hi, sh, mode, a_out, (uint16_t*)pred, b_out, counts);
   return cudaGetLastError();
 }
 
@@ -1188,17 +1259,15 @@ cudaError_t sort_rows_small(const OutTab* ot, const unsigned long long* d_n, uin
 static int sort_chunk_cols(int key_bits) { return std::max(1, 64 / std::max(key_bits, 1)); }
 
 size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (int64_t)n, 0, 64);
   const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
-  return 2 * s4 + 2 * s8 + cub_bytes + 256;
+  (void)n_cols;
+  return 2 * s4 + 2 * s8 + radix_tmp_bytes(n) + 256;
 }
 
 // Lexicographic sort of distinct rows.  Only columns [0, n_key) need sorting: the
 // input order already sorts rows that agree on them (the caller derives n_key from
-// the trie order).  LSD over <= 64-bit keys of packed columns, stable.
+// the trie order).  LSD over <= 64-bit keys of packed columns (hand-written radix
+// sort, radix.cu, permutation as payload), least significant chunk first; stable.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
                       int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches) {
   const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
@@ -1206,8 +1275,8 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
   uint32_t* perm2 = (uint32_t*)((char*)tmp + s4);
   unsigned long long* keys = (unsigned long long*)((char*)tmp + 2 * s4);
   unsigned long long* keys2 = (unsigned long long*)((char*)tmp + 2 * s4 + s8);
-  void* ctmp = (char*)tmp + 2 * s4 + 2 * s8;
-  size_t cbytes = tmp_bytes - 2 * s4 - 2 * s8;
+  void* rtmp = (char*)tmp + 2 * s4 + 2 * s8;
+  const size_t rbytes = tmp_bytes - 2 * s4 - 2 * s8;
   unsigned g = grid_for(n, 256, 148 * 32);
   pdl_launch(k_iota, g, 256, st, perm, n);
   int nl = 1;
@@ -1215,11 +1284,12 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
   for (int c1 = (int)std::min(n_key, n_cols); c1 > 0; c1 -= per) {
     const int c0 = std::max(0, c1 - per);
     pdl_launch(k_gather_key, g, 256, st, rows, perm, n, n_cols, (uint32_t)c0, (uint32_t)c1, key_bits, keys);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(ctmp, cbytes, keys, keys2, perm, perm2, (int64_t)n, 0,
-                                                    (c1 - c0) * key_bits, st);
+    int second = 0;
+    cudaError_t e = radix_sort_pairs_u64_u32((uint64_t*)keys, (uint64_t*)keys2, perm, perm2, n, 0,
+                                             (c1 - c0) * key_bits, rtmp, rbytes, st, &second, &nl, false);
     if (e != cudaSuccess) return e;
-    std::swap(perm, perm2);
-    nl += 2;
+    if (second) std::swap(perm, perm2);
+    nl += 1;
   }
   pdl_launch(k_gather_rows, grid_for(n * n_cols, 256, 148 * 32), 256, st, rows, perm, n, n_cols, rows_out);
   if (launches) *launches += nl + 1;

@@ -39,11 +39,33 @@ cudaError_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint64_t n,
 cudaError_t launch_pack_keys(const uint32_t* rowv, const uint32_t* p, const uint32_t* colv, uint64_t n,
                              const uint8_t* keep, int sh_row, int sh_pred, int drop_bit,
                              uint64_t* keys, cudaStream_t st);
-size_t sort_keys_tmp_bytes(uint64_t n, int end_bit);
-cudaError_t sort_keys_u64(void* tmp, size_t tmp_bytes, const uint64_t* in, uint64_t* out, uint64_t n,
-                          int end_bit, cudaStream_t st);
+// hand-written onesweep LSD radix sort (radix.cu): sorts by key bits [b0, b1);
+// (k0, v0) hold the input, (k1, v1) are same-sized ping-pong buffers; on
+// return *in_second says which pair holds the sorted output.  Stable.
+// skip_trivial: read the digit histograms on the host (one sync) and skip
+// passes whose digit is the same for every key.
+size_t radix_tmp_bytes(uint64_t n);
+cudaError_t radix_sort_keys_u64(uint64_t* k0, uint64_t* k1, uint64_t n, int b0, int b1, void* tmp, size_t tmp_bytes,
+                                cudaStream_t st, int* in_second, int* launches, bool skip_trivial);
+cudaError_t radix_sort_pairs_u64_u32(uint64_t* k0, uint64_t* k1, uint32_t* v0, uint32_t* v1, uint64_t n, int b0,
+                                     int b1, void* tmp, size_t tmp_bytes, cudaStream_t st, int* in_second,
+                                     int* launches, bool skip_trivial);
+cudaError_t radix_sort_pairs_u32_u64(uint32_t* k0, uint32_t* k1, uint64_t* v0, uint64_t* v1, uint64_t n, int b0,
+                                     int b1, void* tmp, size_t tmp_bytes, cudaStream_t st, int* in_second,
+                                     int* launches, bool skip_trivial);
 cudaError_t launch_unique_flags(const uint64_t* keys, uint64_t n, int drop_bit, uint32_t* flags,
                                 cudaStream_t st);
+// keys wider than 63 bits (+ drop flag at drop_hi), lo = b:
+// mode 0 (LSpM format): hi = a << sh | pred; mode 1 (label-major): hi = pred << sh | a
+cudaError_t launch_pack_keys2(const uint32_t* a, const uint32_t* p, const uint32_t* b, uint64_t n, const uint8_t* keep,
+                              int mode, int sh, int drop_hi, uint64_t* hi, uint32_t* lo, cudaStream_t st);
+cudaError_t launch_unique_flags2(const uint64_t* hi, const uint32_t* lo, uint64_t n, int drop_hi, uint32_t* flags,
+                                 cudaStream_t st);
+// mode 0: a_out = col, pred, counts per row (sh = pb); mode 1: a_out = s, b_out = o,
+// counts per label (sh = nb)
+cudaError_t launch_unpack2(const uint64_t* hi, const uint32_t* lo, uint64_t n, const uint32_t* pos, int drop_hi, int sh,
+                           int mode, uint32_t* a_out, void* pred, int pred_bytes, uint32_t* b_out, uint32_t* counts,
+                           cudaStream_t st);
 cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int sh_row,
                           int sh_pred, uint32_t* col, void* pred, int pred_bytes, uint32_t* counts,
                           cudaStream_t st);

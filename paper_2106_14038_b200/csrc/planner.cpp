@@ -82,8 +82,15 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
       uint32_t v = S.back(); S.pop_back();
       Group g; g.center = v; g.level = depth[v];
       for (uint32_t k = 0; k < ne; k++) {      // Step 4: all unevaluated incident edges
-        if (F[k]) continue;
         const auto& e = q->e[k];
+        if (F[k]) {
+          // evaluated at an earlier center (variables at both ends): a back edge
+          if (e.src != e.dst && !is_c[e.src] && !is_c[e.dst]) {
+            if (e.src == v) g.back.push_back({k, e.pred, OUT, e.dst});
+            else if (e.dst == v) g.back.push_back({k, e.pred, IN, e.src});
+          }
+          continue;
+        }
         if (e.src == v) g.edges.push_back({k, e.pred, OUT, e.dst});
         else if (e.dst == v) g.edges.push_back({k, e.pred, IN, e.src});
       }
@@ -187,6 +194,12 @@ std::string describe_plan(const gsmart_plan_t& p) {
     o << (i ? "," : "") << "{\"center\":" << g.center << ",\"level\":" << g.level << ",\"edges\":[";
     for (size_t j = 0; j < g.edges.size(); j++) {
       auto& e = g.edges[j];
+      o << (j ? "," : "") << "{\"edge\":" << e.edge << ",\"label\":" << e.label << ",\"dir\":\""
+        << (e.dir == OUT ? "out" : "in") << "\",\"nbr\":" << e.nbr << "}";
+    }
+    o << "],\"back\":[";
+    for (size_t j = 0; j < g.back.size(); j++) {
+      auto& e = g.back[j];
       o << (j ? "," : "") << "{\"edge\":" << e.edge << ",\"label\":" << e.label << ",\"dir\":\""
         << (e.dir == OUT ? "out" : "in") << "\",\"nbr\":" << e.nbr << "}";
     }

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <set>
 
 #include "runtime.h"
 
@@ -22,6 +23,10 @@ const char* kKernelNames[GSMART_NKERNELS] = {
     "collective"};
 
 thread_local std::string g_static_err;
+
+// live contexts, so gsmart_plan_free can drop the plan's cache entries in each
+static std::mutex g_live_mu;
+static std::set<gsmart_ctx*> g_live;
 
 gsmart_status cuda_fail(gsmart_ctx* ctx, cudaError_t e, const char* what, int line) {
   if (e == cudaErrorMemoryAllocation) {
@@ -154,6 +159,10 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
     }
   }
   *out = ctx.release();
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live.insert(*out);
+  }
   return GSMART_OK;
 }
 
@@ -173,6 +182,10 @@ static void free_lspm(gsmart_ctx* ctx) {
 
 extern "C" void gsmart_destroy(gsmart_ctx* ctx) {
   if (!ctx) return;
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live.erase(ctx);
+  }
   cudaSetDevice(ctx->cfg.device);
   slots_free(ctx);
   free_lspm(ctx);
@@ -184,6 +197,9 @@ extern "C" void gsmart_destroy(gsmart_ctx* ctx) {
     const NcclApi* api = nccl_api();
     if (api) api->CommDestroy(ctx->comm);
   }
+  stage_ring_free(ctx);
+  ctx->pinned.clear();
+  ctx->workers.reset();
   cudaFree(ctx->d_ctr);
   cudaFreeHost(ctx->h_pin);
   if (ctx->own_stream) cudaStreamDestroy(ctx->st);
@@ -218,11 +234,14 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
   TRY(dalloc(ctx, &ctx->d_s, n));
   TRY(dalloc(ctx, &ctx->d_p, n));
   TRY(dalloc(ctx, &ctx->d_o, n));
-  cudaMemcpyKind kind = flags == GSMART_PTR_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  if (n) {
-    CU(cudaMemcpyAsync(ctx->d_s, s, n * 4, kind, ctx->st));
-    CU(cudaMemcpyAsync(ctx->d_p, p, n * 4, kind, ctx->st));
-    CU(cudaMemcpyAsync(ctx->d_o, o, n * 4, kind, ctx->st));
+  if (n && flags == GSMART_PTR_HOST) {  // pinned: one copy each; pageable: staged through pinned chunks
+    TRY(h2d_staged(ctx, ctx->d_s, s, n * 4, ctx->st));
+    TRY(h2d_staged(ctx, ctx->d_p, p, n * 4, ctx->st));
+    TRY(h2d_staged(ctx, ctx->d_o, o, n * 4, ctx->st));
+  } else if (n) {
+    CU(cudaMemcpyAsync(ctx->d_s, s, n * 4, cudaMemcpyDeviceToDevice, ctx->st));
+    CU(cudaMemcpyAsync(ctx->d_p, p, n * 4, cudaMemcpyDeviceToDevice, ctx->st));
+    CU(cudaMemcpyAsync(ctx->d_o, o, n * 4, cudaMemcpyDeviceToDevice, ctx->st));
   }
   if (n) {  // ids are validated on the device after the copy (host and device input alike)
     CU(cudaMemsetAsync(ctx->d_ctr + 32, 0, 8, ctx->st));
@@ -242,43 +261,95 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
 }
 
 // ------------------------------------------------------------------------ build (a1)
+// Sorted, de-duplicated entry keys of the kept triples (§6.2.1 steps 1-4,
+// P:L406-L413): mode 0 orders (a, pred, b) (an LSpM format: a = row, b = col),
+// mode 1 orders (pred, a, b) (the label-major lists: a = s, b = o).  Keys that
+// fit 63 bits are packed into one word (one radix sort over 2nb + pb + 1
+// bits); wider keys (e.g. 100M entities x 10,000 labels: 27 + 14 + 27 bits)
+// are two words, hi = the first two fields, lo = b, sorted by lo and then
+// stably by hi.  flags[i] becomes the output position of sorted key i
+// (exclusive scan of "kept and first of its run"); *M = kept entries.
+struct SortedKeys {
+  bool wide = false;
+  int drop = 0;        // narrow: drop bit of the packed key; wide: drop bit of hi
+  uint64_t* k = nullptr;  // narrow keys, or hi
+  uint32_t* lo = nullptr;
+  uint32_t* pos = nullptr;
+  unsigned long long M = 0;
+};
+
+static gsmart_status sort_triple_keys(gsmart_ctx* ctx, Scratch& sc, const uint32_t* a, const uint32_t* b, int mode,
+                                      const uint8_t* d_keep, SortedKeys* out) {
+  const uint64_t n = ctx->n_triples;
+  const int nb = bits_for(ctx->N - 1), pb = bits_for(ctx->P);
+  unsigned long long* tot = ctx->d_ctr + 40;
+  out->wide = 2 * nb + pb >= 64;
+  TRY(sc.get(&out->pos, n + 1));
+  if (!n) {
+    CU(cudaMemsetAsync(tot, 0, 8, ctx->st));
+    out->M = 0;
+    return GSMART_OK;
+  }
+  void* rtmp = nullptr;
+  const size_t rb = radix_tmp_bytes(n);
+  TRY(sc.get((char**)&rtmp, rb));
+  int second = 0;
+  if (!out->wide) {
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    TRY(sc.get(&k0, n));
+    TRY(sc.get(&k1, n));
+    out->drop = 2 * nb + pb;
+    if (mode == 0) CU(launch_pack_keys(a, ctx->d_p, b, n, d_keep, nb + pb, nb, out->drop, k0, ctx->st));
+    else CU(launch_pack_pso(a, ctx->d_p, b, n, d_keep, nb, out->drop, k0, ctx->st));
+    CU(radix_sort_keys_u64(k0, k1, n, 0, out->drop + 1, rtmp, rb, ctx->st, &second, nullptr, true));
+    out->k = second ? k1 : k0;
+    CU(launch_unique_flags(out->k, n, out->drop, out->pos, ctx->st));
+  } else {
+    uint64_t *h0 = nullptr, *h1 = nullptr;
+    uint32_t *l0 = nullptr, *l1 = nullptr;
+    TRY(sc.get(&h0, n));
+    TRY(sc.get(&h1, n));
+    TRY(sc.get(&l0, n));
+    TRY(sc.get(&l1, n));
+    out->drop = nb + pb;
+    CU(launch_pack_keys2(a, ctx->d_p, b, n, d_keep, mode, mode == 0 ? pb : nb, out->drop, h0, l0, ctx->st));
+    // LSD: the low word first (hi as payload), then the high word (lo as payload)
+    CU(radix_sort_pairs_u32_u64(l0, l1, h0, h1, n, 0, nb, rtmp, rb, ctx->st, &second, nullptr, true));
+    uint64_t *hc = second ? h1 : h0, *ho = second ? h0 : h1;
+    uint32_t *lc = second ? l1 : l0, *lo_ = second ? l0 : l1;
+    CU(radix_sort_pairs_u64_u32(hc, ho, lc, lo_, n, 0, out->drop + 1, rtmp, rb, ctx->st, &second, nullptr, true));
+    out->k = second ? ho : hc;
+    out->lo = second ? lo_ : lc;
+    CU(launch_unique_flags2(out->k, out->lo, n, out->drop, out->pos, ctx->st));
+  }
+  void* stmp = nullptr;
+  TRY(sc.get((char**)&stmp, scan_tmp_bytes(n)));
+  CU(scan_exclusive_u32(out->pos, out->pos, n, tot, stmp, ctx->st, nullptr));
+  TRY(readback(ctx, tot, 1, &out->M));
+  return GSMART_OK;
+}
+
 static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
   Lspm& L = ctx->f[fmt];
   const uint64_t n = ctx->n_triples;
   const uint32_t N = ctx->N;
   const int nb = bits_for(N - 1), pb = bits_for(ctx->P);
-  const int sh_pred = nb, sh_row = nb + pb, drop_bit = 2 * nb + pb;
-  if (drop_bit >= 64) FAIL(GSMART_E_UNSUPPORTED, "packed (row,pred,col) key exceeds 63 bits");
   Scratch sc(ctx);
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  uint32_t* flags = nullptr;
-  TRY(sc.get(&keys, n));
-  TRY(sc.get(&keys2, n));
-  TRY(sc.get(&flags, n + 1));
   const uint32_t* rowv = fmt == 0 ? ctx->d_s : ctx->d_o;
   const uint32_t* colv = fmt == 0 ? ctx->d_o : ctx->d_s;
   unsigned long long* tot = ctx->d_ctr + 40;
-  if (n) {
-    CU(launch_pack_keys(rowv, ctx->d_p, colv, n, d_keep, sh_row, sh_pred, drop_bit, keys, ctx->st));
-    size_t tb = sort_keys_tmp_bytes(n, drop_bit + 1);
-    void* tmp = nullptr;
-    TRY(sc.get((char**)&tmp, tb));
-    CU(sort_keys_u64(tmp, tb, keys, keys2, n, drop_bit + 1, ctx->st));
-    CU(launch_unique_flags(keys2, n, drop_bit, flags, ctx->st));
-    void* stmp = nullptr;
-    TRY(sc.get((char**)&stmp, scan_tmp_bytes(n)));
-    CU(scan_exclusive_u32(flags, flags, n, tot, stmp, ctx->st, nullptr));
-  } else {
-    CU(cudaMemsetAsync(tot, 0, 8, ctx->st));
-  }
-  unsigned long long M = 0;
-  TRY(readback(ctx, tot, 1, &M));
+  SortedKeys sk;
+  TRY(sort_triple_keys(ctx, sc, rowv, colv, 0, d_keep, &sk));
+  const unsigned long long M = sk.M;
   if (M >= 0xffffffffull) FAIL(GSMART_E_UNSUPPORTED, "more than 2^32-2 entries in one LSpM format");
   TRY(dalloc(ctx, &L.rp, (uint64_t)N + 1));
   TRY(dalloc(ctx, &L.col, M));
   TRY(dalloc(ctx, (uint8_t**)&L.pred, M * ctx->pred_bytes + 64));  // +64: 16-byte label loads may overrun
   CU(cudaMemsetAsync(L.rp, 0, ((uint64_t)N + 1) * 4, ctx->st));
-  if (n) CU(launch_unpack(keys2, n, flags, drop_bit, sh_row, sh_pred, L.col, L.pred, ctx->pred_bytes, L.rp, ctx->st));
+  if (n && !sk.wide)
+    CU(launch_unpack(sk.k, n, sk.pos, sk.drop, nb + pb, nb, L.col, L.pred, ctx->pred_bytes, L.rp, ctx->st));
+  else if (n)
+    CU(launch_unpack2(sk.k, sk.lo, n, sk.pos, sk.drop, pb, 0, L.col, L.pred, ctx->pred_bytes, nullptr, L.rp, ctx->st));
   {
     void* stmp = nullptr;
     TRY(sc.get((char**)&stmp, scan_tmp_bytes((uint64_t)N + 1)));
@@ -297,39 +368,22 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
   return GSMART_OK;
 }
 
-// label-major lists (only when the (p, s, o) key fits 63 bits; else the
-// grouped evaluation uses the pull form only)
+// label-major lists: the kept, de-duplicated triples sorted by (p, s, o)
 static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep) {
   LabelMajor& L = ctx->lm;
   const uint64_t n = ctx->n_triples;
-  const int nb = bits_for(ctx->N - 1), pb = bits_for(ctx->P);
-  const int drop_bit = 2 * nb + pb;
-  if (drop_bit >= 64) return GSMART_OK;
+  const int nb = bits_for(ctx->N - 1);
   Scratch sc(ctx);
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  uint32_t *flags = nullptr, *cnt = nullptr;
+  uint32_t* cnt = nullptr;
   TRY(sc.get(&cnt, (uint64_t)ctx->P + 2));
   CU(cudaMemsetAsync(cnt, 0, ((size_t)ctx->P + 2) * 4, ctx->st));
-  unsigned long long* tot = ctx->d_ctr + 40;
-  unsigned long long M = 0;
-  if (n) {
-    TRY(sc.get(&keys, n));
-    TRY(sc.get(&keys2, n));
-    TRY(sc.get(&flags, n + 1));
-    CU(launch_pack_pso(ctx->d_s, ctx->d_p, ctx->d_o, n, d_keep, nb, drop_bit, keys, ctx->st));
-    size_t tb = sort_keys_tmp_bytes(n, drop_bit + 1);
-    void* tmp = nullptr;
-    TRY(sc.get((char**)&tmp, tb));
-    CU(sort_keys_u64(tmp, tb, keys, keys2, n, drop_bit + 1, ctx->st));
-    CU(launch_unique_flags(keys2, n, drop_bit, flags, ctx->st));
-    void* stmp = nullptr;
-    TRY(sc.get((char**)&stmp, scan_tmp_bytes(n)));
-    CU(scan_exclusive_u32(flags, flags, n, tot, stmp, ctx->st, nullptr));
-    TRY(readback(ctx, tot, 1, &M));
-  }
+  SortedKeys sk;
+  TRY(sort_triple_keys(ctx, sc, ctx->d_s, ctx->d_o, 1, d_keep, &sk));
+  const unsigned long long M = sk.M;
   TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
   TRY(dalloc(ctx, &L.o, M + 4));
-  if (M) CU(launch_unpack_pso(keys2, n, flags, drop_bit, nb, L.s, L.o, cnt, ctx->st));
+  if (M && !sk.wide) CU(launch_unpack_pso(sk.k, n, sk.pos, sk.drop, nb, L.s, L.o, cnt, ctx->st));
+  else if (M) CU(launch_unpack2(sk.k, sk.lo, n, sk.pos, sk.drop, nb, 1, L.s, nullptr, ctx->pred_bytes, L.o, cnt, ctx->st));
   std::vector<uint32_t> h(ctx->P + 2);
   CU(cudaMemcpyAsync(h.data(), cnt, h.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
   CU(cudaStreamSynchronize(ctx->st));
@@ -410,7 +464,36 @@ extern "C" gsmart_status gsmart_plan_describe(const gsmart_plan_t* plan, char* b
   return GSMART_OK;
 }
 
-extern "C" void gsmart_plan_free(gsmart_plan_t* plan) { delete plan; }
+extern "C" void gsmart_plan_free(gsmart_plan_t* plan) {
+  if (!plan) return;
+  const uint64_t uid = plan->uid;
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    int dev0 = -1;
+    for (gsmart_ctx* ctx : g_live) {
+      ctx->push_cache.erase(uid);
+      ctx->p2_guess.erase(uid);
+      ctx->plan_cost.erase(uid);
+      bool any = false;
+      for (auto& sp : ctx->slots)
+        for (auto& kv : sp->graphs) any = any || (kv.first >> 3) == uid;
+      if (!any) continue;
+      if (dev0 < 0) cudaGetDevice(&dev0);
+      cudaSetDevice(ctx->cfg.device);
+      for (auto& sp : ctx->slots)
+        for (auto it = sp->graphs.begin(); it != sp->graphs.end();) {
+          if ((it->first >> 3) == uid) {
+            cudaGraphExecDestroy(it->second.exec);
+            it = sp->graphs.erase(it);
+          } else {
+            ++it;
+          }
+        }
+    }
+    if (dev0 >= 0) cudaSetDevice(dev0);
+  }
+  delete plan;
+}
 
 // ------------------------------------------------------------------------ results
 extern "C" gsmart_status gsmart_result_shape(const gsmart_result* r, uint64_t* n_rows, uint32_t* n_cols,
@@ -427,13 +510,11 @@ extern "C" gsmart_status gsmart_result_rows(gsmart_result* r, const uint32_t** r
   if (r->count_only) return GSMART_E_STATE;
   if (!r->host_valid) {
     if (!r->d_rows) return GSMART_E_STATE;
-    r->h_rows.resize(r->n_rows * r->n_cols);
-    cudaSetDevice(r->ctx->cfg.device);
-    if (cudaMemcpy(r->h_rows.data(), r->d_rows, r->n_rows * r->n_cols * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-      return GSMART_E_CUDA;
-    r->host_valid = true;
+    gsmart_ctx* ctx = r->ctx;
+    CU(cudaSetDevice(ctx->cfg.device));
+    TRY(rows_to_host(ctx, r, r->st ? r->st : ctx->st));
   }
-  *rows = r->h_rows.data();
+  *rows = r->h_rows;
   return GSMART_OK;
 }
 
@@ -476,6 +557,7 @@ extern "C" void gsmart_result_free(gsmart_result* r) {
     cudaSetDevice(r->ctx->cfg.device);
     cudaStream_t st = r->st ? r->st : r->ctx->st;
     for (void* p : r->owned) cudaFreeAsync(p, st);
+    if (r->h_rows) r->ctx->pinned.put(r->h_rows, r->h_cls);
   }
   delete r;
 }

@@ -3,7 +3,10 @@
 #pragma once
 #include <algorithm>
 #include <condition_variable>
+#include <functional>
+#include <map>
 #include <memory>
+#include <thread>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -103,6 +106,45 @@ struct Slot {
   std::unordered_map<uint64_t, GraphEntry> graphs;  // (plan uid << 3 | phase tag) -> captured work
 };
 
+// Small persistent host thread pool (hostio.cu): run(f) calls f(i) on every
+// worker i and waits.  Used for the pageable -> pinned staging memcpys.
+struct HostWorkers {
+  explicit HostWorkers(int n);
+  ~HostWorkers();
+  void run(const std::function<void(int)>& f);
+  size_t size() const { return th.size(); }
+ private:
+  void loop(int idx);
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::function<void(int)> job;
+  uint64_t gen = 0;
+  int pending = 0;
+  bool stop = false;
+};
+
+// Ring of pinned chunks for H2D of pageable caller arrays (hostio.cu).
+struct StageRing {
+  static constexpr int K = 4;
+  static constexpr size_t CHUNK = 32u << 20;
+  void* buf[K] = {};
+  cudaEvent_t ev[K] = {};
+  bool used[K] = {};
+  uint64_t next = 0;
+};
+
+// Caching pool of pinned host blocks (power-of-two size classes >= 64 KiB)
+// for result rows; bounded, the rest is released.
+struct PinnedPool {
+  static constexpr size_t CAP = 8ull << 30;
+  std::multimap<size_t, void*> free_blocks;
+  size_t cached = 0;
+  void* get(size_t bytes, size_t* cls);
+  void put(void* p, size_t cls);
+  void clear();
+};
+
 }  // namespace gsm
 
 // In-process communicator: `world` ranks, one host thread each (any devices).
@@ -158,6 +200,9 @@ struct gsmart_ctx {
   gsmart_comm* lcomm = nullptr;  // world > 1 with an in-process communicator
   int rank = 0, world = 1;
   std::vector<std::unique_ptr<gsm::Slot>> slots;
+  std::unique_ptr<gsm::HostWorkers> workers;  // staging memcpy threads (lazy)
+  gsm::StageRing ring;                        // pinned H2D staging chunks (lazy)
+  gsm::PinnedPool pinned;                     // pinned blocks for result rows
   uint64_t cap() const { return cfg.max_result_rows ? cfg.max_result_rows : 0x7fffffffull; }
 };
 
@@ -168,7 +213,8 @@ struct gsmart_result {
   uint32_t n_cols = 0;
   std::vector<uint32_t> var_of_col;
   uint32_t* d_rows = nullptr;
-  std::vector<uint32_t> h_rows;
+  uint32_t* h_rows = nullptr;      // pinned block of ctx->pinned (class h_cls)
+  size_t h_cls = 0;
   bool host_valid = false;
   bool count_only = false;
   uint32_t* d_cand = nullptr;
@@ -245,6 +291,12 @@ gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_p
                        int n, unsigned long long* host);
 
 void slots_free(gsmart_ctx* ctx);
+
+// hostio.cu
+bool host_is_pinned(const void* p);
+gsmart_status h2d_staged(gsmart_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
+void stage_ring_free(gsmart_ctx* ctx);
+gsmart_status rows_to_host(gsmart_ctx* ctx, gsmart_result* r, cudaStream_t st);
 
 // ---- 1-D vertex-range partition of the bitmaps: rank r owns
 // words [r*slice, min((r+1)*slice, n_words)) with slice a multiple of 32 words.

@@ -65,6 +65,7 @@ class gsmart_stats(ctypes.Structure):
                 ("expand_entries", ctypes.c_uint64), ("closing_checks", ctypes.c_uint64),
                 ("n_levels", ctypes.c_uint32), ("level_nodes", ctypes.c_uint64 * MAX_LEVELS),
                 ("level_alive", ctypes.c_uint64 * MAX_LEVELS), ("allgather_bytes", ctypes.c_uint64),
+                ("spec_phase2", ctypes.c_uint32), ("spec_redo", ctypes.c_uint32),
                 ("kernel_names", ctypes.c_char_p * NKERNELS)]
 
 
@@ -199,7 +200,13 @@ def _ptr_kind(a):
             a = a.numpy()
     except ImportError:
         pass
-    arr = np.ascontiguousarray(np.asarray(a).astype(np.uint32, copy=False))
+    arr = np.asarray(a)
+    if arr.size and arr.dtype != np.uint32:
+        if arr.dtype.kind not in "iu":
+            raise TypeError("triple arrays must hold integers")
+        if arr.min() < 0 or arr.max() >= 2 ** 32:
+            raise ValueError("triple ids must lie in [0, 2^32)")  # never wrap silently
+    arr = np.ascontiguousarray(arr.astype(np.uint32, copy=False))
     return arr.ctypes.data, arr, GSMART_PTR_HOST
 
 
@@ -291,13 +298,16 @@ def gsmart_result_shape(r):
     return n.value, c.value, [voc[i] for i in range(c.value)]
 
 
-def gsmart_result_rows(r):
+def gsmart_result_rows(r, copy=True):
+    """Host rows [n_rows, n_cols] uint32.  copy=False returns a view of the
+    result's pinned host block, valid until gsmart_result_free(r)."""
     n, c, _ = gsmart_result_shape(r)
     ptr = ctypes.POINTER(ctypes.c_uint32)()
     _check(_lib.gsmart_result_rows(r, ctypes.byref(ptr)))
     if n == 0 or c == 0:
         return np.zeros((n, c), dtype=np.uint32)
-    return np.ctypeslib.as_array(ptr, shape=(n * c,)).copy().reshape(n, c)
+    a = np.ctypeslib.as_array(ptr, shape=(n * c,)).reshape(n, c)
+    return a.copy() if copy else a
 
 
 def gsmart_result_rows_device(r):
@@ -338,6 +348,7 @@ def gsmart_result_stats(r):
         "level_nodes": [int(s.level_nodes[i]) for i in range(s.n_levels)],
         "level_alive": [int(s.level_alive[i]) for i in range(s.n_levels)],
         "allgather_bytes": int(s.allgather_bytes),
+        "spec_phase2": int(s.spec_phase2), "spec_redo": int(s.spec_redo),
     }
 
 

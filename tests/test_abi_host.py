@@ -38,7 +38,7 @@ def test_header_symbols_exported(G):
 
 
 def test_abi_version_and_build_info(G):
-    assert G.gsmart_abi_version() == 1
+    assert G.gsmart_abi_version() == 2
     assert "sm_100a" in G.gsmart_build_info()
 
 
@@ -58,7 +58,8 @@ def _pydesc(q):
     return {
         "roots": pl["roots"],
         "seeds": pl["seeds"],
-        "groups": [{"center": c, "edges": [(k, D[d], w) for k, d, w in g]} for c, g in pl["groups"]],
+        "groups": [{"center": c, "edges": [(k, D[d], w) for k, d, w in g], "back": [(k, D[d], w) for k, d, w in b]}
+                   for (c, g), b in zip(pl["groups"], pl["back"])],
         "level": pl["level"],
         "pi": pl["pi"],
         "tree": {v: (k, p, D[d]) for v, (k, p, d) in pl["tree"].items()},
@@ -83,8 +84,8 @@ def _cdesc(G, q):
     return {
         "roots": d["roots"],
         "seeds": [s["edge"] for s in d["seeds"]] + [],
-        "groups": [{"center": g["center"], "edges": [(e["edge"], e["dir"], e["nbr"]) for e in g["edges"]]}
-                   for g in d["groups"]],
+        "groups": [{"center": g["center"], "edges": [(e["edge"], e["dir"], e["nbr"]) for e in g["edges"]],
+                    "back": [(e["edge"], e["dir"], e["nbr"]) for e in g["back"]]} for g in d["groups"]],
         "level": [g["level"] for g in d["groups"]],
         "pi": pi,
         "tree": tree,

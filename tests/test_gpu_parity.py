@@ -98,6 +98,66 @@ def test_lspm_arrays_match_definition(G, eng, seed, N, P, M, keep):
         np.testing.assert_array_equal(lm.astype(np.uint64), exp)
 
 
+def test_lspm_wide_keys_match_definition(G):
+    """(row, pred, col) keys wider than 63 bits (2^26 + 5 entities = 27 bits,
+    10,000 labels = 14 bits: 68 bits, configs[4]'s shape) take the two-word
+    sort path (low word first, then the high word, both with the
+    hand-written radix sort): CSR/CSC arrays and the label-major lists equal
+    the definition; ids span the whole range (top bits exercised), with
+    duplicates and a keep-set."""
+    N, P, M = (1 << 26) + 5, 10_000, 300_000
+    rng = np.random.default_rng(68)
+    s = rng.integers(0, N, M).astype(np.uint32)
+    o = rng.integers(0, N, M).astype(np.uint32)
+    s[:1000] = N - 1 - rng.integers(0, 3, 1000)   # rows at the top of the id range
+    p = rng.integers(1, P + 1, M).astype(np.uint32)
+    s = np.concatenate([s, s[:5000]]); p = np.concatenate([p, p[:5000]]); o = np.concatenate([o, o[:5000]])
+    e = G.Engine(0)
+    try:
+        for keep in (None, list(range(1, P + 1, 3))):
+            e.load(s, p, o, N, P, keep=keep)
+            for fmt, name in ((G.GSMART_CSR, "csr"), (G.GSMART_CSC, "csc")):
+                v = G.gsmart_lspm_get(e.ctx, fmt)
+                ref = R.lspm_arrays(s, p, o, N, keep=keep, fmt=name)
+                assert v["nnz"] == len(ref["col"])
+                rp = G.gsmart_copy_to_host(e.ctx, v["row_ptr"], (N + 1) * 4)
+                col = G.gsmart_copy_to_host(e.ctx, v["col"], v["nnz"] * 4)
+                pred = G.gsmart_copy_to_host(e.ctx, v["pred"], v["nnz"] * 2, dtype=np.uint16)
+                np.testing.assert_array_equal(rp.astype(np.uint64), ref["row_ptr"])
+                np.testing.assert_array_equal(col, ref["col"])
+                np.testing.assert_array_equal(pred.astype(np.uint32), ref["pred"])
+        # queries through the wide-key LSpM and label-major lists (push form forced too)
+        e.load(s, p, o, N, P)
+        ix = OracleIndex(s, p, o)
+        hub = int(np.bincount(p).argmax())
+        qs = [Query((None, None), ((0, hub, 1),)),
+              Query((None, None, None), ((0, int(p[0]), 1), (0, int(p[1]), 2))),
+              Query((None, None, int(o[7])), ((0, int(p[7]), 2), (0, int(p[8]), 1)))]
+        for q in qs:
+            assert np.array_equal(e.query(q), ix.query(q)), q
+    finally:
+        e.close()
+
+
+def test_powerlaw_wide_keys_vs_oracle(G):
+    """configs[4]'s id widths at reduced triple count: 100M entities, 10,000
+    labels (68-bit keys), 3M power-law triples; random-walk queries == C oracle."""
+    from synth import powerlaw
+    d = powerlaw.generate(3_000_000, 100_000_000, 10_000)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    e = G.Engine(0)
+    try:
+        G.gsmart_load_triples(e.ctx, d.s.cuda(), d.p.cuda(), d.o.cuda(), d.n_entities, d.n_predicates)
+        G.gsmart_build_lspm(e.ctx)
+        ix = OracleIndex(s, p, o)
+        qs = powerlaw.queries(d, 15, seed=5)
+        for q, got in zip(qs, e.query_batch(qs)):
+            x = ix.query(q)
+            assert got.shape == x.shape and np.array_equal(got, x), q
+    finally:
+        e.close()
+
+
 # ------------------------------------------------------------------ random tiny cases
 @pytest.mark.parametrize("chunk", range(5))
 def test_random_tiny_rows_and_candidates(G, eng, chunk):
@@ -342,6 +402,25 @@ def test_edge_cases(G, eng):
         G.gsmart_result_free(r)
 
 
+def test_absent_constants_candidates(G, eng):
+    """A constant absent from the data (id >= N, up to 2^32 - 1) has no
+    entries: as a seed it empties only its own variable's candidate set (the
+    schedule then propagates), as a guard it is false (R12, R13).  Rows and
+    every candidate bitmap equal filter_schedule."""
+    s, p, o = fixtures.fig1_triples()
+    eng.load(s, p, o, 8, 4)
+    for q in (Query((None, None, 99), ((0, 1, 1), (1, 1, 2))),
+              Query((None, None, 0xFFFFFFF0, 0x80000005), ((0, 1, 1), (2, 1, 1), (3, 2, 1))),
+              Query((None, None, 8), ((0, 2, 1), (1, 1, 2), (1, 1, 0))),
+              Query((None, None, 8, 3), ((0, 3, 1), (2, 1, 3))),
+              Query((None, None, 1, 3), ((0, 3, 1), (2, 1, 3)))):
+        rows, cs, _ = _cands(G, eng, q, 0)
+        assert _rows(rows) == R.brute_force(s, p, o, 8, q), q
+        ref, _ = R.filter_schedule(s, p, o, 8, q, refine=True)
+        for v in q.variables:
+            assert _bits_to_set(cs[v], 8) == set(np.nonzero(ref[v])[0].tolist()), (q, v)
+
+
 def test_label_signature_collisions(G, eng):
     """Row label signatures fold labels mod 32 (P > 32): labels 1, 33 and 65 share
     a bit, so rows holding only label 1 pass the pre-test for a label-33 edge and
@@ -474,29 +553,45 @@ def test_push_form_vs_oracle(G, eng_push, src):
 
 
 # ------------------------------------------------------------------ speculative phase 2
+def _run_plans(G, ctx, plans, batch):
+    """rows + stats of each plan, through one batch or one execute per plan"""
+    res = G.gsmart_execute_batch(ctx, plans, 0) if batch else [G.gsmart_execute(ctx, pl, 0) for pl in plans]
+    out = []
+    for r in res:
+        out.append((G.gsmart_result_rows(r), G.gsmart_result_stats(r)))
+        G.gsmart_result_free(r)
+    return out
+
+
 def test_speculative_phase2_repeats(G, eng):
-    """Re-executions queue phase 2 sized from the previous run (one host wait);
-    rows must equal the oracle on every repeat, single and batched."""
+    """Re-executions of the SAME plan handles queue phase 2 sized from the
+    previous run (one host wait): the first run never speculates, every later
+    run does (stats.spec_phase2), guesses right (no redo) and gives the oracle's
+    rows — single executes and batches alike."""
     d = lubm.generate(3)
     s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
     eng.load(s, p, o, d.n_entities, d.n_predicates)
     ix = OracleIndex(s, p, o)
     qs = lubm.queries(d)
     exp = [ix.query(q) for q in qs]
-    with eng.plan(qs[0]) as pl0:
-        for _ in range(3):
-            got = pl0.run(0)
-            assert np.array_equal(got, exp[0])
-    for _ in range(3):
-        for q, e, got in zip(qs, exp, eng.query_batch(qs)):
-            assert got.shape == e.shape and np.array_equal(got, e), q.name
-        assert eng.query(qs[1], flags=G.GSMART_COUNT_ONLY) == exp[1].shape[0]
+    plans = [G.gsmart_plan(eng.ctx, q) for q in qs]
+    try:
+        for rep in range(4):
+            for q, e, (got, st) in zip(qs, exp, _run_plans(G, eng.ctx, plans, batch=rep % 2 == 1)):
+                assert got.shape == e.shape and np.array_equal(got, e), (q.name, rep)
+                assert st["spec_phase2"] == (1 if rep > 0 else 0), (q.name, rep, st["spec_phase2"])
+                assert st["spec_redo"] == 0, q.name
+    finally:
+        for pl in plans:
+            G.gsmart_plan_free(pl)
 
 
 def test_speculative_phase2_wrong_guess(G):
-    """GSMART_SPEC_TEST makes every speculation guess a wrong row count (one
-    fewer: the device guard voids phase 2; one more: the host check rejects it);
-    the ordinary phase 2 must then produce the oracle's rows."""
+    """GSMART_SPEC_TEST makes every speculation guess a wrong row count,
+    alternately one fewer (the device guard k_phase2_guard voids phase 2) and
+    one more (the host size check rejects it).  Plans are re-executed on the
+    same handles, so speculation really happens; the redo must give the
+    oracle's rows and the stats must record the speculation and the redo."""
     import os
     os.environ["GSMART_SPEC_TEST"] = "1"
     try:
@@ -510,8 +605,33 @@ def test_speculative_phase2_wrong_guess(G):
         ix = OracleIndex(s, p, o)
         qs = lubm.queries(d)
         exp = [ix.query(q) for q in qs]
-        for _ in range(3):
-            for q, x, got in zip(qs, exp, e.query_batch(qs)):
-                assert got.shape == x.shape and np.array_equal(got, x), q.name
+        plans = [G.gsmart_plan(e.ctx, q) for q in qs]
+        redos = 0
+        try:
+            for rep in range(4):
+                for q, x, (got, st) in zip(qs, exp, _run_plans(G, e.ctx, plans, batch=rep % 2 == 0)):
+                    assert got.shape == x.shape and np.array_equal(got, x), (q.name, rep)
+                    if rep > 0 and len(x) > 0:
+                        assert st["spec_phase2"] == 1 and st["spec_redo"] == 1, (q.name, rep, st)
+                        redos += 1
+        finally:
+            for pl in plans:
+                G.gsmart_plan_free(pl)
+        assert redos >= 3 * 6
     finally:
         e.close()
+
+
+def test_plan_free_drops_caches(G, eng):
+    """gsmart_plan_free drops the plan's cached graphs/decisions: many short-lived
+    plans keep working and results stay exact (cache growth)."""
+    s, p, o = fixtures.fig1_triples()
+    eng.load(s, p, o, 8, 4)
+    q = fixtures.fig2_query()
+    for _ in range(50):
+        pl = G.gsmart_plan(eng.ctx, q)
+        for _ in range(2):
+            r = G.gsmart_execute(eng.ctx, pl, 0)
+            assert _rows(G.gsmart_result_rows(r)) == [(2, 0, 1, 0), (2, 0, 1, 5)]
+            G.gsmart_result_free(r)
+        G.gsmart_plan_free(pl)

@@ -59,9 +59,34 @@ def test_eq10_eq11_vector_ops():
     np.testing.assert_array_equal(R.vector_or([1, 0, 1], [0, 0, 1]), [1, 0, 1])
 
 
-def test_eq14_binding_vector():
-    M = np.array([[0, 1, 0], [0, 0, 0], [1, 1, 0]])
-    np.testing.assert_array_equal(R.binding_vector(M), [1, 1, 0])
+def test_eq14_neighbour_bindings_fig1(golden_fig):
+    """Eq. 14 over the binding matrices of Eqs. 15/19 (center = subject) and
+    22-23 (center = object): the binding vectors of v2's neighbours given
+    v2 = {1, 5}, hand-derived from the Fig. 1a triples (golden)."""
+    s, p, o = fixtures.fig1_triples()
+    A = R.label_matrix(s, p, o, 8)
+    F, D = fixtures.PREDICATE_IDS["follows"], fixtures.PREDICATE_IDS["director"]
+    v2 = np.zeros(8, dtype=int)
+    v2[golden_fig["level0_candidates"]] = 1
+    g = golden_fig["eq14_neighbour_bindings_of_v2_1_5"]
+    assert R.neighbour_bindings(A, v2, F, x_is_subject=True).nonzero()[0].tolist() == g["v1_out_follows"]
+    assert R.neighbour_bindings(A, v2, D, x_is_subject=False).nonzero()[0].tolist() == g["v0_in_director"]
+    assert R.neighbour_bindings(A, v2, F, x_is_subject=False).nonzero()[0].tolist() == g["v3_in_follows"]
+    # Eq. 14 alone: OR over the rows of a binding matrix = the set of its columns
+    M = R.binding_matrix_rows(A, v2, F)
+    assert R.binding_vector(M).nonzero()[0].tolist() == sorted({j for i, j in zip(*M.nonzero())})
+
+
+def test_eq17_out_out_fig1(golden_fig):
+    """Eq. 17: rows holding both labels (Fig. 1a: actor and director)."""
+    s, p, o = fixtures.fig1_triples()
+    A = R.label_matrix(s, p, o, 8)
+    P = fixtures.PREDICATE_IDS
+    v = R.grouped_eval_out_out(A, P["actor"], P["director"])
+    assert v.nonzero()[0].tolist() == golden_fig["eq17_actor_and_director_rows"]
+    # label order is irrelevant, a label no row holds empties it
+    assert R.grouped_eval_out_out(A, P["director"], P["actor"]).tolist() == v.tolist()
+    assert not R.grouped_eval_out_out(A, P["actor"], 9).any()
 
 
 def test_level0_bitmaps_fig1(golden_fig):
@@ -83,21 +108,69 @@ def test_level0_bitmaps_fig1(golden_fig):
     assert R.grouped_eval_in_out(A, D, F).nonzero()[0].tolist() == [1, 4, 5]
 
 
-def test_filter_schedule_level0_fig1(golden_fig):
+def test_filter_schedule_fig1_steps(golden_fig):
+    """Every step of the filter schedule on Fig. 1/2 (golden, hand-derived):
+    group 0 -> {1,5} (Ex. 7.2), group 1 -> v0 = {2}, backward -> v2 = {1}."""
     s, p, o = fixtures.fig1_triples()
     q = fixtures.fig2_query()
-    cand, ok = R.filter_schedule(s, p, o, 8, q, refine=False)
-    assert ok
     plan = R.plan_degree(q)
-    root = plan["roots"][0]
-    # after the root group only, = level-0 set of Ex. 7.2; check via a schedule
-    # truncated to the first group
+    g = golden_fig["schedule_fig1"]
     one = dict(plan, groups=plan["groups"][:1])
-    c1, _ = R.filter_schedule(s, p, o, 8, q, plan=one, refine=False)
-    assert c1[root].nonzero()[0].tolist() == golden_fig["level0_candidates"]
-    # Ex. 7.2: of {1,5} only 1 survives once v0's group (level 1) is applied
-    c2, _ = R.filter_schedule(s, p, o, 8, q, refine=True)
-    assert c2[root].nonzero()[0].tolist() == [1]
+    c1, ok = R.filter_schedule(s, p, o, 8, q, plan=one, refine=False)
+    assert ok
+    assert c1[2].nonzero()[0].tolist() == g["after_group0_v2"] == golden_fig["level0_candidates"]
+    c2, _ = R.filter_schedule(s, p, o, 8, q, refine=False)
+    assert c2[0].nonzero()[0].tolist() == g["after_group1_v0"]
+    assert c2[2].nonzero()[0].tolist() == g["after_group0_v2"]
+    c3, _ = R.filter_schedule(s, p, o, 8, q, refine=True)
+    assert c3[2].nonzero()[0].tolist() == g["after_refine_v2"]
+    assert c3[0].nonzero()[0].tolist() == g["after_group1_v0"]
+    for v in g["never_centers"]:
+        assert c3[v].all()
+
+
+def _tree_no_multi(q):
+    """True if the variable graph (patterns between two distinct variables) is
+    a spanning tree of the variables with at most one pattern per pair."""
+    pairs = [(min(a, b), max(a, b)) for a, _, b in q.edges
+             if a != b and not q.is_const(a) and not q.is_const(b)]
+    if len(set(pairs)) != len(pairs):
+        return False
+    parent = {v: v for v in q.variables}
+
+    def find(x):
+        while parent[x] != x:
+            x = parent[x]
+        return x
+    for a, b in pairs:
+        ra, rb = find(a), find(b)
+        if ra == rb:
+            return False
+        parent[ra] = rb
+    return len({find(v) for v in q.variables}) == 1
+
+
+def test_filter_schedule_root_exact_acyclic():
+    """Exactness, not just soundness: for a connected query whose variable graph
+    is a tree (constants and self-loops allowed), the forward pass followed by
+    the backward re-evaluation is a bottom-up semijoin reduction, so the root's
+    candidate set equals the projection of the brute-force answer on the root.
+    A dropped term, a wrong direction or a wrong neighbour fails it."""
+    checked = 0
+    for seed in range(1500):
+        (s, p, o), n, P, q = tiny.random_case(seed)
+        if not _tree_no_multi(q):
+            continue
+        plan = R.plan_degree(q)
+        if len(plan["roots"]) != 1:
+            continue
+        rows = R.brute_force(s, p, o, n, q)
+        cand, ok = R.filter_schedule(s, p, o, n, q, plan=plan, refine=True)
+        r = plan["roots"][0]
+        proj = sorted({row[q.variables.index(r)] for row in rows})
+        assert cand[r].nonzero()[0].tolist() == proj, (seed, q)
+        checked += 1
+    assert checked > 300
 
 
 # ---------------------------------------------------------------- §6.1 planner
