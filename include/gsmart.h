@@ -82,13 +82,28 @@ typedef struct gsmart_plan_s gsmart_plan_t;
 typedef struct gsmart_result gsmart_result;
 typedef struct gsmart_comm gsmart_comm;
 
+/* how ranks exchange candidate bitmaps when world > 1 */
+#define GSMART_XCHG_PEER 0u  /* default: symmetric device memory, the filter clears bits on every rank (peer atomics) */
+#define GSMART_XCHG_NCCL 1u  /* baseline: NCCL all-gather (grouped broadcasts) of each rank's slice after a group */
+
 typedef struct {
   int device;                 /* CUDA device ordinal */
-  int rank, world;            /* world >= 1; world > 1 = 1-D vertex-range partition over ranks */
-  const void* nccl_unique_id; /* 128 bytes from gsmart_get_nccl_id on rank 0 (world > 1 over NCCL) */
+  int rank, world;            /* world >= 1 (<= 8); world > 1 = 1-D vertex-range partition of the LSpM */
+  const void* nccl_unique_id; /* 128 bytes from gsmart_get_nccl_id on rank 0, broadcast to every rank (processes:
+                                 rendezvous of the ranks, and the NCCL communicator when exchange == NCCL;
+                                 world == 1: optional, creates a 1-rank NCCL communicator) */
   void* stream;               /* cudaStream_t to run on, or NULL: the library creates one */
   uint64_t max_result_rows;   /* capacity for rows and for each trie level; 0 = 2^31 - 1 */
-  gsmart_comm* local_comm;    /* world > 1 inside one process (one thread per rank) instead of NCCL; else NULL */
+  gsmart_comm* local_comm;    /* world > 1 inside one process (one thread per rank); else NULL */
+  uint32_t exchange;          /* GSMART_XCHG_PEER (default) or GSMART_XCHG_NCCL */
+  /* optional device allocator (e.g. a framework's caching allocator): every
+   * device buffer the library owns, except the world > 1 symmetric regions
+   * (which need the virtual-memory API), comes from alloc(bytes, stream, user)
+   * and returns through free(ptr, stream, user), ordered on `stream`.  NULL:
+   * cudaMallocAsync / cudaFreeAsync on the device's default memory pool. */
+  void* (*alloc)(size_t bytes, void* stream, void* user);
+  void (*free)(void* ptr, void* stream, void* user);
+  void* alloc_user;
 } gsmart_config;
 
 /* In-process communicator for `world` ranks driven by `world` host threads of
@@ -98,11 +113,24 @@ typedef struct {
 gsmart_status gsmart_comm_create_local(int world, gsmart_comm** out);
 void gsmart_comm_destroy(gsmart_comm* comm);
 
-/* The bitmap word range [word_lo, word_hi) (32 entities per word) that rank
- * `rank` of `world` owns in the 1-D vertex-range partition: the ranks filter
- * their own candidate rows and root bindings (host helper, no device). */
-gsmart_status gsmart_partition_words(uint32_t n_entities, int world, int rank, uint32_t* word_lo,
-                                     uint32_t* word_hi);
+/* Split points of the 1-D vertex-range partition (host helper, no device; the
+ * build uses it on the GPU-computed histogram).  bucket[i] = out+in entries of
+ * vertices [i * 2^19, (i+1) * 2^19) (n_buckets = ceil(n_entities / 2^19)).
+ * Writes v[0..world]: v[0] = 0, v[world] = n_entities, every inner split a
+ * multiple of 2^19 (2 MiB of row pointers = one symmetric mapping granule),
+ * non-decreasing, rank r owning [v[r], v[r+1]); split r is the first bucket
+ * boundary where the running total reaches r/world of the entries. */
+gsmart_status gsmart_partition_split(const uint64_t* bucket, uint32_t n_buckets, uint32_t n_entities, int world,
+                                     uint32_t* v);
+/* The split points of a built world > 1 context (v[0..world]). */
+gsmart_status gsmart_partition_get(const gsmart_ctx* ctx, uint32_t* v);
+
+/* Host-side self-check of the channel that ranks running as separate
+ * processes use (no device needed): rendezvous on the 128-byte id, all-gather
+ * `value` into all_values[world], and hand one file descriptor per rank to
+ * every other rank (the path the symmetric chunks' POSIX handles take).
+ * Collective over the `world` processes. */
+gsmart_status gsmart_rendezvous_check(const void* id128, int rank, int world, uint64_t value, uint64_t* all_values);
 
 /* ABI version and a build string (static storage). */
 int gsmart_abi_version(void);
@@ -123,7 +151,10 @@ const char* gsmart_last_error(const gsmart_ctx* ctx);
  * after the copy (s,o < n_entities, 1 <= p <= n_predicates) ->
  * GSMART_E_INVALID_ARG with no triples loaded (build then gives E_STATE).  Replaces any
  * previously loaded triples and invalidates the LSpM.  n may be 0.
- * n_entities < 2^31, n_predicates <= 65535. */
+ * n_entities < 2^31, n_predicates <= 65534 (labels are stored as uint8 when
+ * n_predicates <= 254, else uint16; the all-ones value is a sentinel).
+ * world > 1: every rank passes the SAME full triple set (collective); each
+ * rank keeps only its vertex range when the LSpM is built. */
 gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s, const uint32_t* p,
                                   const uint32_t* o, uint64_t n, uint32_t n_entities,
                                   uint32_t n_predicates, uint32_t flags);
@@ -133,7 +164,7 @@ gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s, const uint
  * P:L408 "Read necessary RDF triples where predicates appear in the
  * queries"), de-duplicate, and store CSR (rows = subjects) and/or CSC (rows =
  * objects) as row_ptr[N+1] (uint32), col[M] (uint32) and pred[M] (uint8 when
- * n_predicates <= 255, else uint16), entries sorted by (row, pred, col), so
+ * n_predicates <= 254, else uint16), entries sorted by (row, pred, col), so
  * every (row, predicate) pair is one contiguous range.  Empty rows have
  * row_ptr[i] == row_ptr[i+1] (the paper's Mr/Pr row elimination).
  * formats: GSMART_CSR | GSMART_CSC (execute needs both).  Requires kept

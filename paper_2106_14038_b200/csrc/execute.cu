@@ -36,6 +36,7 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
   TRY(dalloc(ctx, &s.d_ctr, 64, s.st));
   TRY(dalloc(ctx, &s.heavy_cnt, 4, s.st));
   TRY(dalloc(ctx, &s.d_epoch, 1, s.st));
+  TRY(dalloc(ctx, &s.d_bar, 1, s.st));
   CU(cudaMemsetAsync(s.lb_status, 0, (size_t)LB_CAP_TILES * 8, s.st));
   CU(cudaMemsetAsync(s.lb_counters, 0, (size_t)LB_EPOCHS * 4, s.st));
   CU(cudaMemsetAsync(s.heavy_cnt, 0, 16, s.st));
@@ -49,13 +50,21 @@ static gsmart_status slot_init(gsmart_ctx* ctx, Slot& s, bool primary) {
 static void slot_free(gsmart_ctx* ctx, Slot& s) {
   cudaStream_t st = s.st;
   for (auto& b : s.lv) {
-    dfree(st, b.bind); dfree(st, b.parent); dfree(st, b.seg_beg); dfree(st, b.off); dfree(st, b.newidx);
-    dfree(st, b.alive);
+    dfree(ctx, st, b.bind); dfree(ctx, st, b.parent); dfree(ctx, st, b.seg_beg); dfree(ctx, st, b.off); dfree(ctx, st, b.newidx);
+    dfree(ctx, st, b.alive);
   }
-  for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(st, s.list[k]);
-  dfree(st, s.lb_status); dfree(st, s.lb_counters); dfree(st, s.tile_start); dfree(st, s.d_sz); dfree(st, s.d_ctr);
-  dfree(st, s.heavy_rows); dfree(st, s.heavy_chunks); dfree(st, s.heavy_sat); dfree(st, s.heavy_cnt);
-  dfree(st, s.frows); dfree(st, s.sat); dfree(st, s.cand); dfree(st, s.d_epoch); dfree(st, s.p2); dfree(st, s.d_tab);
+  for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(ctx, st, s.list[k]);
+  dfree(ctx, st, s.lb_status); dfree(ctx, st, s.lb_counters); dfree(ctx, st, s.tile_start); dfree(ctx, st, s.d_sz); dfree(ctx, st, s.d_ctr);
+  dfree(ctx, st, s.heavy_rows); dfree(ctx, st, s.heavy_chunks); dfree(ctx, st, s.heavy_sat); dfree(ctx, st, s.heavy_cnt);
+  dfree(ctx, st, s.frows); dfree(ctx, st, s.sat); dfree(ctx, st, s.d_epoch); dfree(ctx, st, s.p2); dfree(ctx, st, s.d_tab);
+  dfree(ctx, st, s.d_bar);
+  if (s.sym.va) {
+    cudaStreamSynchronize(st);
+    sym_free(ctx, &s.sym);
+  } else {
+    dfree(ctx, st, s.cand);
+  }
+  if (s.gath.va) sym_free(ctx, &s.gath);
   for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second.exec);
   s.graphs.clear();
   cudaStreamSynchronize(st);
@@ -83,7 +92,7 @@ static gsmart_status ensure_slots(gsmart_ctx* ctx, uint32_t n) {
 // heavy-row buffers sized from the LSpM's heavy-row statistics
 static gsmart_status slot_heavy(gsmart_ctx* ctx, Slot& s) {
   if (s.heavy_gen == ctx->lspm_gen) return GSMART_OK;
-  dfree(s.st, s.heavy_rows); dfree(s.st, s.heavy_chunks); dfree(s.st, s.heavy_sat);
+  dfree(ctx, s.st, s.heavy_rows); dfree(ctx, s.st, s.heavy_chunks); dfree(ctx, s.st, s.heavy_sat);
   const uint64_t rows = std::max<uint64_t>(ctx->f[0].heavy_rows + ctx->f[1].heavy_rows, 1);
   const uint64_t chunks = std::max<uint64_t>(ctx->f[0].heavy_chunks + ctx->f[1].heavy_chunks, 1);
   TRY(dalloc(ctx, &s.heavy_rows, rows, s.st));
@@ -109,13 +118,20 @@ static gsmart_status begin_seq(gsmart_ctx* ctx, Slot& s) {
   }
   s.seq_base = s.epoch_next;
   s.seq_off = 0;
-  // the sequence's first kernel (k_init_cands) copies it to s.d_epoch; the slot is
-  // idle here (every execute drains its stream before the next one begins)
+  s.bar_base = s.bar_next;
+  s.bar_off = 0;
+  // the sequence's first kernel (k_init_cands) copies them to s.d_epoch / s.d_bar;
+  // the slot is idle here (every execute drains its stream before the next one begins)
   reinterpret_cast<volatile uint32_t*>(s.h_pin + H_EPOCH)[0] = s.seq_base;
+  reinterpret_cast<volatile unsigned long long*>(s.h_pin)[H_BAR] = s.bar_base;
   return GSMART_OK;
 }
 
-static void end_seq(Slot& s) { s.epoch_next = s.seq_base + std::min(s.seq_off, SEQ_MAX); }
+// barrier generations only grow (ranks compare flags with >=), look-back epochs wrap
+static void end_seq(Slot& s) {
+  s.epoch_next = s.seq_base + std::min(s.seq_off, SEQ_MAX);
+  s.bar_next = s.bar_base + s.bar_off + 1;
+}
 
 // the next look-back launch of the current sequence
 static LBArgs next_lb(Slot& s) {
@@ -133,8 +149,8 @@ static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t n
   if (b.bind && b.cap >= need) return GSMART_OK;
   uint64_t cap = std::max<uint64_t>(need, std::max<uint64_t>(2 * b.cap, 1u << 16));
   cap = (cap + 1023) / 1024 * 1024;
-  dfree(s.st, b.bind); dfree(s.st, b.parent); dfree(s.st, b.seg_beg); dfree(s.st, b.off); dfree(s.st, b.newidx);
-  dfree(s.st, b.alive);
+  dfree(ctx, s.st, b.bind); dfree(ctx, s.st, b.parent); dfree(ctx, s.st, b.seg_beg); dfree(ctx, s.st, b.off); dfree(ctx, s.st, b.newidx);
+  dfree(ctx, s.st, b.alive);
   b = Slot::LvBuf();
   TRY(dalloc(ctx, &b.bind, cap, s.st));
   TRY(dalloc(ctx, &b.parent, cap, s.st));
@@ -151,7 +167,7 @@ static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t n
 template <typename T>
 static gsmart_status slot_buf(gsmart_ctx* ctx, Slot& s, T** p, uint64_t* cap, uint64_t need) {
   if (*p && *cap >= need) return GSMART_OK;
-  dfree(s.st, *p);
+  dfree(ctx, s.st, *p);
   *p = nullptr;
   TRY(dalloc(ctx, p, need, s.st));
   *cap = need;
@@ -222,7 +238,7 @@ struct Exec {
   bool seq_open = false;        // a look-back launch sequence was started (end it in finalize)
   bool graph_replayed = false;  // phase 1 came from the plan's cached CUDA graph
   bool ctr_pinned = false;      // counters already copied to sl.h_pin[192..) on the stream
-  uint32_t wlo = 0, whi = 0, slice = 0;  // this rank's bitmap words (1-D vertex-range partition)
+  uint32_t wlo = 0, whi = 0;  // this rank's bitmap words (1-D vertex-range partition)
   bool identity = false;                 // trie order == column order: rows come out sorted
   std::vector<uint64_t> F;
   std::chrono::steady_clock::time_point t0;
@@ -235,6 +251,33 @@ struct Exec {
   // candidate bitmaps live in the slot (stable addresses for graph replay);
   // GSMART_KEEP_CANDIDATES copies them into the result at the end
   uint32_t* cand(uint32_t vertex) { return sl.cand + (uint64_t)slot[vertex] * Wpad; }
+
+  // world > 1 with the peer exchange: bitmaps and change words are symmetric,
+  // filters update every rank's copy, a device barrier ends each group
+  bool peer_mode() const { return ctx->world > 1 && ctx->exchange == GSMART_XCHG_PEER; }
+  SymDelta peer_delta() const {
+    SymDelta d{};
+    if (peer_mode()) d = sl.sym.delta(ctx->world);
+    return d;
+  }
+  uint32_t peer_world() const { return peer_mode() ? (uint32_t)ctx->world : 1u; }
+  uint32_t* chg_words() {
+    return peer_mode() ? sl.cand + sl.sym_cand_words : reinterpret_cast<uint32_t*>(sl.d_ctr + 16);
+  }
+  gsmart_status rank_barrier() {
+    unsigned long long* flags = reinterpret_cast<unsigned long long*>(sl.cand + sl.sym_cand_words + 32);
+    prof.begin(K_COLLECTIVE);
+    CU(launch_rank_barrier(flags, peer_delta(), (uint32_t)ctx->rank, (uint32_t)ctx->world, sl.d_bar, ++sl.bar_off,
+                           sl.st));
+    prof.end();
+    launches[K_COLLECTIVE]++;
+    return GSMART_OK;
+  }
+  // label-major list of an edge's center side (world > 1: OUT -> this rank's
+  // subjects, IN -> this rank's objects stored as (o, s))
+  const LabelMajor& lm_for(const GroupEdge& e) const {
+    return (ctx->world > 1 && e.dir == IN) ? ctx->lm_in : ctx->lm;
+  }
 
   gsmart_status alloc_result(void** p, uint64_t bytes) {
     TRY(dalloc(ctx, (char**)p, bytes, sl.st));
@@ -263,6 +306,12 @@ struct Exec {
       x.zero2 = sl.d_sz;  // expansion sizes
       x.n_zero2 = 128;
       x.ovf = sl.d_ovf;
+      x.h_bar = reinterpret_cast<const volatile unsigned long long*>(sl.h_pin + H_BAR);
+      x.d_bar = sl.d_bar;
+      if (peer_mode()) {
+        x.zero32 = chg_words();
+        x.n_zero32 = 32;
+      }
       prof.begin(K_BITMAP);
       CU(launch_init_cands(sl.cand, (uint32_t)plan->vars.size(), Wpad, N, ones, x, sl.st));
       launches[K_BITMAP]++;
@@ -335,16 +384,19 @@ struct Exec {
     }
     // cheapest (and most selective) label first: later edges only mark rows that
     // passed the earlier ones, and stop at once when none did
-    std::stable_sort(push.begin(), push.end(), [&](const GroupEdge* x, const GroupEdge* y) {
-      return ctx->lm.off[x->label + 1] - ctx->lm.off[x->label] < ctx->lm.off[y->label + 1] - ctx->lm.off[y->label];
-    });
+    auto lm_size = [&](const GroupEdge* e) {
+      const LabelMajor& L = lm_for(*e);
+      return L.off[e->label + 1] - L.off[e->label];
+    };
+    std::stable_sort(push.begin(), push.end(),
+                     [&](const GroupEdge* x, const GroupEdge* y) { return lm_size(x) < lm_size(y); });
     // change tracking (SkipIf): a re-evaluation is skipped on the device when no
     // neighbour bitmap changed since this group's previous evaluation (world == 1)
     const uint32_t seq = ++filter_seq;
     SkipIf sk;
-    sk.chg = reinterpret_cast<uint32_t*>(sl.d_ctr + 16);
+    sk.chg = chg_words();
     const uint32_t prev = gi < group_seq.size() ? group_seq[gi] : 0u;
-    if (prev && ctx->world == 1) {
+    if (prev && (ctx->world == 1 || peer_mode())) {
       sk.prev = prev;
       for (auto& e : GE)
         if (!(e.nbr & 0x80000000u) && e.nbr != g.center) sk.nbr_mask |= 1u << slot[e.nbr];
@@ -353,11 +405,12 @@ struct Exec {
     if (!push.empty()) {
       // push form (label-major streaming) of the chosen edges: each marks the rows
       // that also passed the previous one, the last mark set is AND-ed into cand_x
-      const LabelMajor& lm = ctx->lm;
       const uint32_t* prev_sat = nullptr;
       prof.begin(K_FILTER);
       for (size_t i = 0; i < push.size(); i++) {
         const GroupEdge* e = push[i];
+        const LabelMajor& lm = lm_for(*e);
+        const bool center_first = e->dir == OUT || ctx->world > 1;  // lm_in stores (o, s)
         uint32_t* out = sl.sat + (i & 1) * (uint64_t)Wpad;
         unsigned long long* cnt = sl.d_ctr + 32 + (i & 1);
         CU(cudaMemsetAsync(out, 0, (size_t)W * 4, sl.st));
@@ -368,7 +421,7 @@ struct Exec {
         pa.o = lm.o;
         pa.beg = lm.off[e->label];
         pa.end = lm.off[e->label + 1];
-        pa.out = e->dir == OUT ? 1u : 0u;
+        pa.out = center_first ? 1u : 0u;
         pa.cand = cand(g.center);
         pa.sat_in = prev_sat;
         pa.sat_out = out;
@@ -389,12 +442,21 @@ struct Exec {
         launches[K_FILTER]++;
         prev_sat = out;
       }
-      CU(launch_and_tracked(cand(g.center), prev_sat, W, sk, (uint32_t)slot[g.center], seq, sl.st, ctx->sm_count));
+      PeerSet ps;
+      ps.world = peer_world();
+      ps.peers = peer_delta();
+      CU(launch_and_tracked(cand(g.center) + wlo, prev_sat + wlo, whi - wlo, sk, (uint32_t)slot[g.center], seq, ps,
+                            sl.st, ctx->sm_count));
       launches[K_FILTER]++;
       push_and++;
       prof.end();
-      if (by[0].empty() && by[1].empty()) return GSMART_OK;
     }
+    if (!by[0].empty() || !by[1].empty()) TRY(eval_pull(g, by, sk, seq));
+    return exchange_center(g);
+  }
+
+  // pull form of a group's remaining edges (row filter over the center's candidate rows)
+  gsmart_status eval_pull(const Group& g, std::vector<const GroupEdge*> (&by)[2], const SkipIf& sk, uint32_t seq) {
     size_t done[2] = {0, 0};
     // row-list path: compact the center's candidate rows of this rank once per group
     const bool rowlist = (ctx->filter_variant & 4) != 0;
@@ -442,6 +504,8 @@ struct Exec {
       a.skip = sk;
       a.center_slot = (uint32_t)slot[g.center];
       a.seq = seq;
+      a.world = peer_world();
+      a.peers = peer_delta();
       if (rowlist) {
         a.rows = sl.frows;
         a.d_nrows = d_nrows;
@@ -451,13 +515,24 @@ struct Exec {
       prof.end();
       filter_main++;
     }
-    if (ctx->world > 1) {  // every rank needs the whole candidate bitmap of the center
-      prof.begin(K_COLLECTIVE);
-      TRY(coll_allgather(ctx, sl.st, cand(g.center), (size_t)slice * 4));
-      prof.end();
-      launches[K_COLLECTIVE]++;
-      R->stats.allgather_bytes += (uint64_t)(ctx->world - 1) * slice * 4;
-    }
+    return GSMART_OK;
+  }
+
+  // world > 1: every rank needs the whole candidate bitmap of the center.  Peer
+  // exchange: the filter already cleared the bits on every rank's copy; a device
+  // barrier orders them before anyone reads.  NCCL / in-process copies (the
+  // baseline): an all-gather of the ranks' slices (variable sizes).
+  gsmart_status exchange_center(const Group& g) {
+    if (ctx->world == 1 && !ctx->comm) return GSMART_OK;
+    uint64_t other = 0;
+    for (int q = 0; q < ctx->world; q++)
+      if (q != ctx->rank) other += part_word_hi(ctx, q) - part_word_lo(ctx, q);
+    if (ctx->world > 1) R->stats.allgather_bytes += 4 * other;
+    if (peer_mode()) return rank_barrier();
+    prof.begin(K_COLLECTIVE);
+    TRY(coll_allgatherv(ctx, sl.st, cand(g.center)));
+    prof.end();
+    launches[K_COLLECTIVE]++;
     return GSMART_OK;
   }
 
@@ -550,7 +625,8 @@ struct Exec {
   gsmart_status decide_push() {
     push_dec.clear();
     const int v = ctx->filter_variant;
-    if (!ctx->lm.built || ctx->world > 1 || (v & 16) || plan->groups.empty()) return GSMART_OK;
+    if (!ctx->lm.built || (ctx->world > 1 && !ctx->lm_in.built) || (v & 16) || plan->groups.empty())
+      return GSMART_OK;
     auto it = ctx->push_cache.find(plan->uid);
     if (it != ctx->push_cache.end() && it->second.first == ctx->lspm_gen) {
       push_dec = it->second.second;
@@ -580,7 +656,8 @@ struct Exec {
       for (size_t ei = 0; ei < ord.size(); ei++) ord[ei] = ei;
       auto M_of = [&](size_t ei) {
         const uint32_t l = GE[ei].label;
-        return l + 1 < ctx->lm.off.size() ? ctx->lm.off[l + 1] - ctx->lm.off[l] : 0ull;
+        const LabelMajor& Lm = lm_for(GE[ei]);
+        return l + 1 < Lm.off.size() ? Lm.off[l + 1] - Lm.off[l] : 0ull;
       };
       std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return M_of(x) < M_of(y); });
       uint64_t bound = est[g.center];
@@ -600,9 +677,31 @@ struct Exec {
   gsmart_status ensure_workspace() {
     const uint64_t nvar = plan->vars.size();
     TRY(slot_heavy(ctx, sl));
-    TRY(slot_buf(ctx, sl, &sl.cand, &sl.cand_words, std::max<uint64_t>((uint64_t)Wpad * nvar, 1)));
+    if (peer_mode()) {
+      // symmetric: [bitmaps (Wpad words per variable)][32 change words][barrier flags, u64 per rank]
+      const uint64_t need = std::max<uint64_t>((uint64_t)Wpad * nvar, 32);
+      if (!sl.sym.va || sl.sym_cand_words < need) {  // collective: every rank runs the same plans
+        CU(cudaStreamSynchronize(sl.st));
+        const uint64_t words = need + 32 + 2 * MAX_WORLD;
+        const uint64_t g = sym_granularity(ctx);
+        const uint64_t bytes = (words * 4 + g - 1) / g * g;
+        SymRegion R2;
+        TRY(sym_alloc(ctx, (uint64_t)ctx->rank * bytes, bytes, &R2));
+        CU(cudaMemsetAsync(R2.local(), 0, bytes, sl.st));
+        CU(cudaStreamSynchronize(sl.st));
+        if (sl.sym.va) sym_free(ctx, &sl.sym);
+        TRY(host_barrier(ctx));  // every rank's flags are zero before any barrier kernel runs
+        sl.sym = R2;
+        sl.cand = (uint32_t*)R2.local();
+        sl.sym_cand_words = need;
+        sl.bar_next = 1;
+        sl.ws_gen++;
+      }
+    } else {
+      TRY(slot_buf(ctx, sl, &sl.cand, &sl.cand_words, std::max<uint64_t>((uint64_t)Wpad * nvar, 1)));
+    }
     if (ctx->filter_variant & 4) TRY(slot_buf(ctx, sl, &sl.frows, &sl.frows_cap, (uint64_t)W * 32));
-    if (ctx->lm.built && ctx->world == 1) TRY(slot_buf(ctx, sl, &sl.sat, &sl.sat_cap, 2ull * Wpad));
+    if (ctx->lm.built) TRY(slot_buf(ctx, sl, &sl.sat, &sl.sat_cap, 2ull * Wpad));
     for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
@@ -615,6 +714,9 @@ struct Exec {
     group_seq.assign(plan->groups.size(), 0);
     filter_seq = 0;
     TRY(seeds_and_guards());
+    // peers clear bits in this rank's bitmaps from the first group on: not before
+    // this rank initialised and seeded them
+    if (peer_mode()) TRY(rank_barrier());
     for (size_t i = 0; i < plan->groups.size(); i++) TRY(eval_group(plan->groups[i], i));
     if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
       for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i], i));
@@ -627,14 +729,16 @@ struct Exec {
   // valid only if the body starts at the same offset as when it was captured.
   template <typename Body>
   gsmart_status run_cached(uint64_t key, uint32_t key_flags, Body&& body) {
-    const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && ctx->world == 1;
+    const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && (ctx->world == 1 || peer_mode()) &&
+                           !ctx->comm;
     if (!graphable) return body();
     auto it = sl.graphs.find(key);
     if (it != sl.graphs.end() && it->second.ws_gen == sl.ws_gen && it->second.lspm_gen == ctx->lspm_gen &&
         it->second.flags == key_flags) {
-      if (it->second.off0 != sl.seq_off) return body();  // e.g. after an expansion re-run
+      if (it->second.off0 != sl.seq_off || it->second.bar0 != sl.bar_off) return body();  // e.g. after a re-run
       CU(cudaGraphLaunch(it->second.exec, sl.st));
       sl.seq_off += it->second.n_lb;
+      sl.bar_off += it->second.n_bar;
       graph_replayed = true;
       for (int i = 0; i < GSMART_NKERNELS; i++) launches[i] += it->second.launches[i];
       filter_main += it->second.filter_main;
@@ -645,7 +749,10 @@ struct Exec {
       cudaGraphExecDestroy(it->second.exec);
       sl.graphs.erase(it);
     }
-    const uint32_t off0 = sl.seq_off;
+    // capture on the second use: a plan executed once (a cold query) pays no
+    // capture/instantiation; a repeated plan replays from then on
+    if (sl.seen.insert(key).second) return body();
+    const uint32_t off0 = sl.seq_off, bar0 = sl.bar_off;
     const std::vector<int> l0(launches, launches + GSMART_NKERNELS);
     const uint64_t fm0 = filter_main, pa0 = push_and;
     CU(cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal));
@@ -668,6 +775,8 @@ struct Exec {
     ge.flags = key_flags;
     ge.off0 = off0;
     ge.n_lb = sl.seq_off - off0;
+    ge.bar0 = bar0;
+    ge.n_bar = sl.bar_off - bar0;
     ge.launches.resize(GSMART_NKERNELS);
     for (int i = 0; i < GSMART_NKERNELS; i++) ge.launches[i] = launches[i] - l0[i];
     ge.filter_main = filter_main - fm0;
@@ -693,11 +802,9 @@ struct Exec {
     Wpad = (W + 31) / 32 * 32;
     wlo = 0;
     whi = W;
-    if (ctx->world > 1) {
-      slice = partition_slice(W, ctx->world);
-      wlo = std::min<uint32_t>((uint32_t)ctx->rank * slice, W);
-      whi = std::min<uint32_t>(wlo + slice, W);
-      Wpad = std::max<uint32_t>(Wpad, slice * (uint32_t)ctx->world);  // all-gather needs world equal slices
+    if (ctx->world > 1) {  // this rank's vertex range (partition split points are multiples of 2^19)
+      wlo = part_word_lo(ctx, ctx->rank);
+      whi = part_word_hi(ctx, ctx->rank);
     }
     L = (uint32_t)plan->levels.size();
     identity = true;
@@ -762,7 +869,7 @@ struct Exec {
   // the guess and, on a mismatch, redoes phase 2 the ordinary way.
   bool spec = false, spec_pending = false;
   bool can_speculate() const {
-    if (ctx->world > 1 || (flags & GSMART_NO_SPECULATE)) return false;
+    if ((ctx->world > 1 && !peer_mode()) || (flags & GSMART_NO_SPECULATE)) return false;
     auto it = ctx->p2_guess.find(plan->uid);
     if (it == ctx->p2_guess.end() || it->second.gen != ctx->lspm_gen || it->second.flags != flags ||
         it->second.F.size() != L)
@@ -796,7 +903,7 @@ struct Exec {
     R->stats.spec_redo = 1;
     // the speculative outputs (arena, candidate copy) are dead: free them before
     // the redo allocates its own (the stream is drained)
-    for (size_t i = spec_owned0; i < R->owned.size(); i++) dfree(sl.st, R->owned[i]);
+    for (size_t i = spec_owned0; i < R->owned.size(); i++) dfree(ctx, sl.st, R->owned[i]);
     R->owned.resize(spec_owned0);
     R->d_cand = nullptr;
     R->levels.clear();
@@ -893,7 +1000,7 @@ struct Exec {
         tb = mode == M_SORT_SMALL ? SORT_SMALL_MAXN * 4 : sort_rows_tmp_bytes(n_rows, nc);
         const uint64_t need = al(n_rows * nc * 4) + al(tb);
         if (need > sl.p2_cap) {
-          dfree(sl.st, sl.p2);
+          dfree(ctx, sl.st, sl.p2);
           sl.p2 = nullptr;
           sl.p2_cap = 0;
           TRY(dalloc(ctx, &sl.p2, need + need / 4, sl.st));
@@ -977,7 +1084,8 @@ struct Exec {
       uint32_t* all = nullptr;
       if (ctx->rank == 0) TRY(alloc_result((void**)&all, total * nc * 4));
       prof.begin(K_COLLECTIVE);
-      TRY(coll_gather_root(ctx, sl.st, R->d_rows, all, bytes));
+      if (peer_mode()) TRY(gather_peer(R->d_rows, all, bytes));
+      else TRY(coll_gather_root(ctx, sl.st, R->d_rows, all, bytes));
       prof.end();
       launches[K_COLLECTIVE]++;
       if (ctx->rank == 0 && !identity) {
@@ -994,6 +1102,36 @@ struct Exec {
     }
     R->n_rows = total;
     return GSMART_OK;
+  }
+
+  // peer exchange: every rank puts its rows into its chunk of a symmetric gather
+  // buffer; rank 0 copies the chunks (NVLink reads) in rank order
+  gsmart_status gather_peer(const uint32_t* mine, uint32_t* all, const std::vector<unsigned long long>& bytes) {
+    unsigned long long need = 0;
+    for (auto b : bytes) need = std::max(need, b);
+    if (need > sl.gath_cap) {  // collective: every rank sees the same byte counts
+      const uint64_t g = sym_granularity(ctx);
+      const uint64_t cap = std::max<uint64_t>((need + need / 4 + g - 1) / g * g, g);
+      if (sl.gath.va) sym_free(ctx, &sl.gath);
+      sl.gath_cap = 0;
+      TRY(sym_alloc(ctx, (uint64_t)ctx->rank * cap, cap, &sl.gath));
+      sl.gath_cap = cap;
+    }
+    const int me = ctx->rank;
+    if (bytes[me]) CU(cudaMemcpyAsync(sl.gath.local(), mine, bytes[me], cudaMemcpyDeviceToDevice, sl.st));
+    CU(cudaStreamSynchronize(sl.st));
+    TRY(host_barrier(ctx));
+    if (me == 0) {
+      uint64_t off = 0;
+      for (int q = 0; q < ctx->world; q++) {
+        if (bytes[q])
+          CU(cudaMemcpyAsync((char*)all + off, (const char*)(sl.gath.va + sl.gath.off[q]), bytes[q],
+                             cudaMemcpyDeviceToDevice, sl.st));
+        off += bytes[q];
+      }
+      CU(cudaStreamSynchronize(sl.st));
+    }
+    return host_barrier(ctx);  // no rank rewrites its chunk before rank 0 has read it
   }
 
   gsmart_status finalize() {
@@ -1153,7 +1291,7 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
         const bool reached_p2 = ex[i]->state == Exec::S_PHASE2;
         if (st[i] == GSMART_OK) st[i] = ex[i]->finalize();
         else ex[i]->prof.flush();
-        if (st[i] == GSMART_OK && reached_p2 && ctx->world == 1) {
+        if (st[i] == GSMART_OK && reached_p2 && (ctx->world == 1 || ctx->exchange == GSMART_XCHG_PEER)) {
           auto& g = ctx->p2_guess[plans[base + i]->uid];
           g.gen = ctx->lspm_gen;
           g.flags = flags;

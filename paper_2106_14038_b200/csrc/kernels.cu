@@ -87,38 +87,71 @@ cudaError_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint64_t n, un
 // a1 — LSpM build (§6.2): key pack -> radix sort -> unique -> unpack + row counts
 // key = row << sh_row | pred << sh_pred | col ; bit drop_bit set = filtered out
 // =====================================================================================
+// rows outside [rlo, rhi) (another rank's vertex range, world > 1) are dropped like
+// filtered predicates
 __global__ void k_pack_keys(const uint32_t* __restrict__ rowv, const uint32_t* __restrict__ p,
                             const uint32_t* __restrict__ colv, uint64_t n, const uint8_t* __restrict__ keep,
-                            int sh_row, int sh_pred, int drop_bit, uint64_t* __restrict__ keys) {
+                            int sh_row, int sh_pred, int drop_bit, uint32_t rlo, uint32_t rhi,
+                            uint64_t* __restrict__ keys) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t r = __ldg(rowv + i), l = __ldg(p + i), c = __ldg(colv + i);
     uint64_t k = ((uint64_t)r << sh_row) | ((uint64_t)l << sh_pred) | (uint64_t)c;
-    if (!__ldg(keep + l)) k |= 1ull << drop_bit;
+    if (!__ldg(keep + l) || r < rlo || r >= rhi) k |= 1ull << drop_bit;
     keys[i] = k;
   }
 }
 
 cudaError_t launch_pack_keys(const uint32_t* rowv, const uint32_t* p, const uint32_t* colv, uint64_t n,
-                             const uint8_t* keep, int sh_row, int sh_pred, int drop_bit, uint64_t* keys,
-                             cudaStream_t st) {
-  k_pack_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(rowv, p, colv, n, keep, sh_row, sh_pred, drop_bit, keys);
+                             const uint8_t* keep, int sh_row, int sh_pred, int drop_bit, uint32_t rlo, uint32_t rhi,
+                             uint64_t* keys, cudaStream_t st) {
+  k_pack_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(rowv, p, colv, n, keep, sh_row, sh_pred, drop_bit, rlo, rhi,
+                                                          keys);
   return cudaGetLastError();
 }
 
 __global__ void k_pack_pso(const uint32_t* __restrict__ s, const uint32_t* __restrict__ p,
                            const uint32_t* __restrict__ o, uint64_t n, const uint8_t* __restrict__ keep, int nb,
-                           int drop_bit, uint64_t* __restrict__ keys) {
+                           int drop_bit, uint32_t rlo, uint32_t rhi, uint64_t* __restrict__ keys) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t l = __ldg(p + i);
-    uint64_t k = ((uint64_t)l << (2 * nb)) | ((uint64_t)__ldg(s + i) << nb) | (uint64_t)__ldg(o + i);
-    if (!__ldg(keep + l)) k |= 1ull << drop_bit;
+    const uint32_t l = __ldg(p + i), a = __ldg(s + i);
+    uint64_t k = ((uint64_t)l << (2 * nb)) | ((uint64_t)a << nb) | (uint64_t)__ldg(o + i);
+    if (!__ldg(keep + l) || a < rlo || a >= rhi) k |= 1ull << drop_bit;
     keys[i] = k;
   }
 }
 
 cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n, const uint8_t* keep,
-                            int nb, int drop_bit, uint64_t* keys, cudaStream_t st) {
-  k_pack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(s, p, o, n, keep, nb, drop_bit, keys);
+                            int nb, int drop_bit, uint32_t rlo, uint32_t rhi, uint64_t* keys, cudaStream_t st) {
+  k_pack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(s, p, o, n, keep, nb, drop_bit, rlo, rhi, keys);
+  return cudaGetLastError();
+}
+
+// world > 1: out+in entries per 2^shift-vertex bucket (partition split points)
+__global__ void k_bucket_degree(const uint32_t* __restrict__ s, const uint32_t* __restrict__ p,
+                                const uint32_t* __restrict__ o, uint64_t n, const uint8_t* __restrict__ keep, int shift,
+                                unsigned long long* __restrict__ hist) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!__ldg(keep + __ldg(p + i))) continue;
+    atomicAdd(hist + (__ldg(s + i) >> shift), 1ull);
+    atomicAdd(hist + (__ldg(o + i) >> shift), 1ull);
+  }
+}
+
+cudaError_t launch_bucket_degree(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n,
+                                 const uint8_t* keep, int shift, unsigned long long* hist, cudaStream_t st) {
+  k_bucket_degree<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(s, p, o, n, keep, shift, hist);
+  return cudaGetLastError();
+}
+
+// dst[i] = src[i] + add (row pointers of a rank's chunk -> global entry indices)
+__global__ void k_add_copy(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint64_t n, uint32_t add) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] + add;
+}
+
+cudaError_t launch_add_copy(uint32_t* dst, const uint32_t* src, uint64_t n, uint32_t add, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  k_add_copy<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(dst, src, n, add);
   return cudaGetLastError();
 }
 
@@ -212,20 +245,23 @@ cudaError_t launch_unpack(const uint64_t* keys, uint64_t n, const uint32_t* pos,
 // mode 0 (LSpM format): hi = a << sh | pred; mode 1 (label-major): hi = pred << sh | a; lo = b
 __global__ void k_pack_keys2(const uint32_t* __restrict__ a, const uint32_t* __restrict__ p,
                              const uint32_t* __restrict__ b, uint64_t n, const uint8_t* __restrict__ keep, int mode,
-                             int sh, int drop_hi, uint64_t* __restrict__ hi, uint32_t* __restrict__ lo) {
+                             int sh, int drop_hi, uint32_t rlo, uint32_t rhi, uint64_t* __restrict__ hi,
+                             uint32_t* __restrict__ lo) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t l = __ldg(p + i);
-    const uint64_t x = __ldg(a + i);
+    const uint32_t x32 = __ldg(a + i);
+    const uint64_t x = x32;
     uint64_t h = mode == 0 ? ((x << sh) | (uint64_t)l) : (((uint64_t)l << sh) | x);
-    if (!__ldg(keep + l)) h |= 1ull << drop_hi;
+    if (!__ldg(keep + l) || x32 < rlo || x32 >= rhi) h |= 1ull << drop_hi;
     hi[i] = h;
     lo[i] = __ldg(b + i);
   }
 }
 
 cudaError_t launch_pack_keys2(const uint32_t* a, const uint32_t* p, const uint32_t* b, uint64_t n, const uint8_t* keep,
-                              int mode, int sh, int drop_hi, uint64_t* hi, uint32_t* lo, cudaStream_t st) {
-  k_pack_keys2<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(a, p, b, n, keep, mode, sh, drop_hi, hi, lo);
+                              int mode, int sh, int drop_hi, uint32_t rlo, uint32_t rhi, uint64_t* hi, uint32_t* lo,
+                              cudaStream_t st) {
+  k_pack_keys2<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(a, p, b, n, keep, mode, sh, drop_hi, rlo, rhi, hi, lo);
   return cudaGetLastError();
 }
 
@@ -370,9 +406,11 @@ __global__ void k_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride, 
   // the execute's counters and size words (no memset nodes)
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0 && x.d_epoch) *x.d_epoch = *x.h_epoch;
+    if (threadIdx.x == 0 && x.d_bar) *x.d_bar = *x.h_bar;
     if (threadIdx.x == 0 && x.ovf) *x.ovf = 0;
     for (uint32_t i = threadIdx.x; i < x.n_zero; i += blockDim.x) x.zero[i] = 0;
     for (uint32_t i = threadIdx.x; i < x.n_zero2; i += blockDim.x) x.zero2[i] = 0;
+    for (uint32_t i = threadIdx.x; i < x.n_zero32; i += blockDim.x) x.zero32[i] = 0;
   }
   const uint64_t total = (uint64_t)n_slots * stride;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -554,7 +592,24 @@ struct FilterArgsT {
   LBArgs claim;
   SkipIf skip;
   uint32_t center_slot, seq;
+  uint32_t world;
+  SymDelta peers;
 };
+
+// world > 1 (peer exchange): a bit cleared / a change word raised on this rank is
+// applied to every rank's copy of the symmetric buffer (NVLink atomics)
+__device__ __forceinline__ uint32_t and_all_ranks(uint32_t* p, uint32_t mask, uint32_t world, const SymDelta& d) {
+  const uint32_t old = atomicAnd(p, mask);
+  for (uint32_t q = 0; q < world; q++)
+    if (d.words[q]) atomicAnd(p + d.words[q], mask);
+  return old;
+}
+
+__device__ __forceinline__ void max_all_ranks(uint32_t* p, uint32_t v, uint32_t world, const SymDelta& d) {
+  atomicMax(p, v);
+  for (uint32_t q = 0; q < world; q++)
+    if (d.words[q]) atomicMax(p + d.words[q], v);
+}
 
 template <typename PT>
 __device__ __forceinline__ uint32_t match_entry(const FilterArgsT<PT>& a, int d, uint32_t l, uint32_t c,
@@ -680,7 +735,43 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
         }
         sat = need;
       } else if (len > SHORT_ROW) {
-        medium = true;
+        // medium row, lane-private: per group label, a binary search for its first
+        // entry, then its range probed 4 entries per step until a probe hits; all
+        // 32 lanes search in parallel (latency overlapped across rows).  A label
+        // range longer than MED_SCAN without a hit goes to the warp-cooperative
+        // scan below (rare: long runs of non-candidate neighbours).
+        for (int j = 0; j < MAXG; j++) {
+          if (j >= (int)a.ne[d]) break;
+          if ((sat >> j) & 1u) continue;
+          const uint32_t lab = a.e[d][j].label;
+          uint32_t lo = b, hi = e;
+          while (lo < hi) {
+            const uint32_t m = (lo + hi) >> 1;
+            if ((uint32_t)__ldg(a.f[d].pred + m) < lab) lo = m + 1; else hi = m;
+          }
+          const uint32_t kcap = min(e, lo + MED_SCAN);
+          const uint32_t mode = a.e[d][j].mode;
+          bool hit = false, done = false;  // done: the label's range ended inside the window
+          for (uint32_t k = lo; k < kcap && !hit && !done; k += 4) {
+            uint32_t l4[4], c4[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) l4[t] = k + t < kcap ? (uint32_t)__ldg(a.f[d].pred + k + t) : lab;
+#pragma unroll
+            for (int t = 0; t < 4; t++) c4[t] = (k + t < kcap && l4[t] == lab) ? __ldg(a.f[d].col + k + t) : 0u;
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+              if (hit || done || k + t >= kcap) break;
+              if (l4[t] != lab) { done = true; break; }
+              n_scanned++;
+              n_matched++;
+              hit = mode == GE_PROBE ? (bit_of(a.e[d][j].nbr, c4[t]) != 0)
+                                     : (c4[t] == (mode == GE_SELF ? row : a.e[d][j].cval));
+            }
+          }
+          if (hit) sat |= 1u << j;
+          else if (!done && kcap < e && (uint32_t)__ldg(a.f[d].pred + kcap) == lab) medium = true;  // range goes on
+          else break;  // this label has no satisfying entry: the row fails
+        }
       } else if constexpr (SIMD) {
         sat = short_row_u8(a, d, row, b, e, need, n_scanned, n_matched);
       } else {
@@ -735,20 +826,23 @@ __device__ __forceinline__ bool eval_rows(const FilterArgsT<PT>& a, const uint32
 }
 
 // clear the candidate bits of failed rows (one atomicAnd per distinct word per
-// warp); `changed` notes whether a bit actually went from 1 to 0
-__device__ __forceinline__ void clear_failed(uint32_t* cand, const uint32_t row, const bool fail, const uint32_t lane,
-                                             bool& changed) {
+// warp, on every rank's copy when world > 1); `changed` notes whether a bit
+// actually went from 1 to 0
+template <typename PT>
+__device__ __forceinline__ void clear_failed(const FilterArgsT<PT>& a, const uint32_t row, const bool fail,
+                                             const uint32_t lane, bool& changed) {
   const uint32_t word = fail ? (row >> 5) : 0xffffffffu;
   const uint32_t peers = __match_any_sync(GSM_FULL, word);
   const uint32_t bits = __reduce_or_sync(peers, fail ? (1u << (row & 31)) : 0u);
-  if (fail && (int)lane == __ffs(peers) - 1) changed |= (atomicAnd(cand + word, ~bits) & bits) != 0;
+  if (fail && (int)lane == __ffs(peers) - 1)
+    changed |= (and_all_ranks(a.cand + word, ~bits, a.world, a.peers) & bits) != 0;
 }
 
 // end of a filter launch: publish "the center's bitmap changed at this sequence"
 template <typename PT>
 __device__ __forceinline__ void note_change(const FilterArgsT<PT>& a, const bool changed) {
   if (__any_sync(GSM_FULL, changed) && (threadIdx.x & 31) == 0 && a.skip.chg)
-    atomicMax(a.skip.chg + a.center_slot, a.seq);
+    max_all_ranks(a.skip.chg + a.center_slot, a.seq, a.world, a.peers);
 }
 
 template <typename PT, bool SIMD>
@@ -815,7 +909,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
         qn -= 32;
         __syncwarp();
         const bool ok = eval_rows<PT, SIMD>(a, row, true, lane, n_rows, n_scanned, n_matched, n_masked);
-        clear_failed(a.cand, row, !ok, lane, changed);
+        clear_failed(a, row, !ok, lane, changed);
       }
     }
   }
@@ -823,7 +917,7 @@ __global__ void __launch_bounds__(256) k_group_filter(FilterArgsT<PT> a) {
     const bool has = lane < qn;
     const uint32_t row = has ? q[lane] : 0u;
     const bool ok = eval_rows<PT, SIMD>(a, row, has, lane, n_rows, n_scanned, n_matched, n_masked);
-    clear_failed(a.cand, row, has && !ok, lane, changed);
+    clear_failed(a, row, has && !ok, lane, changed);
   }
   // one atomic per warp per counter
   note_change(a, changed);
@@ -887,7 +981,7 @@ __global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterA
         if (j == (uint32_t)t) r = row[t];
       const bool has = (hasm >> j) & 1u;
       const bool ok = eval_rows<PT, SIMD, true>(a, r, (pass >> j) & 1u, lane, n_rows, n_scanned, n_matched, n_masked);
-      clear_failed(a.cand, r, has && !ok, lane, changed);
+      clear_failed(a, r, has && !ok, lane, changed);
     }
   }
   note_change(a, changed);
@@ -951,7 +1045,8 @@ __global__ void k_filter_finalize(FilterArgsT<PT> a) {
     const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
     if (a.heavy_sat[i] != need) {
       const uint32_t b = 1u << (row & 31);
-      if ((atomicAnd(a.cand + (row >> 5), ~b) & b) && a.skip.chg) atomicMax(a.skip.chg + a.center_slot, a.seq);
+      if ((and_all_ranks(a.cand + (row >> 5), ~b, a.world, a.peers) & b) && a.skip.chg)
+        max_all_ranks(a.skip.chg + a.center_slot, a.seq, a.world, a.peers);
     }
     a.heavy_sat[i] = 0;
   }
@@ -983,6 +1078,7 @@ static FilterArgsT<PT> to_t(const FilterArgs& a) {
   t.heavy_rows = a.heavy_rows; t.heavy_chunks = a.heavy_chunks; t.heavy_sat = a.heavy_sat;
   t.heavy_count = a.heavy_count; t.ctr = a.ctr; t.variant = a.variant; t.word_lo = a.word_lo; t.claim = a.claim;
   t.skip = a.skip; t.center_slot = a.center_slot; t.seq = a.seq;
+  t.world = a.world < 1 ? 1u : a.world; t.peers = a.peers;
   return t;
 }
 
@@ -1102,9 +1198,11 @@ cudaError_t launch_push_edge(const PushArgs& a, int sm_count, cudaStream_t st) {
   return pdl_launch(k_push_edge, g, 256, st, a);
 }
 
+// cand[0, n_words) &= sat — this rank's word range; world > 1: the new words are
+// stored into every rank's copy (only this rank writes these words)
 __global__ void __launch_bounds__(256) k_and_tracked(uint32_t* __restrict__ cand, const uint32_t* __restrict__ sat,
                                                     uint32_t n_words, SkipIf skip, uint32_t center_slot,
-                                                    uint32_t seq) {
+                                                    uint32_t seq, PeerSet ps) {
   GSM_PDL_ENTRY();
   if (skip.skip()) return;
   bool changed = false;
@@ -1112,16 +1210,21 @@ __global__ void __launch_bounds__(256) k_and_tracked(uint32_t* __restrict__ cand
     const uint32_t c = cand[w], v = c & __ldcs(sat + w);
     if (v != c) {
       cand[w] = v;
+      for (uint32_t q = 0; q < ps.world; q++)
+        if (ps.peers.words[q]) cand[w + ps.peers.words[q]] = v;
       changed = true;
     }
   }
-  if (__any_sync(GSM_FULL, changed) && (threadIdx.x & 31) == 0 && skip.chg) atomicMax(skip.chg + center_slot, seq);
+  if (__any_sync(GSM_FULL, changed) && (threadIdx.x & 31) == 0 && skip.chg)
+    max_all_ranks(skip.chg + center_slot, seq, ps.world, ps.peers);
 }
 
 cudaError_t launch_and_tracked(uint32_t* cand, const uint32_t* sat, uint32_t n_words, SkipIf skip,
-                               uint32_t center_slot, uint32_t seq, cudaStream_t st, int sm_count) {
+                               uint32_t center_slot, uint32_t seq, const PeerSet& ps, cudaStream_t st, int sm_count) {
   const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_words + 255) / 256, (uint64_t)sm_count * 8));
-  return pdl_launch(k_and_tracked, g, 256, st, cand, sat, n_words, skip, center_slot, seq);
+  PeerSet p = ps;
+  if (p.world < 1) p.world = 1;
+  return pdl_launch(k_and_tracked, g, 256, st, cand, sat, n_words, skip, center_slot, seq, p);
 }
 
 cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_count, cudaStream_t st,

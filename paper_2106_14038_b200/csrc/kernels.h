@@ -36,9 +36,13 @@ cudaError_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint64_t n,
                                int* launches);
 
 // ----------------------------------------------------------------- a1 LSpM build
+// rows outside [rlo, rhi) are dropped (world > 1: another rank's range)
 cudaError_t launch_pack_keys(const uint32_t* rowv, const uint32_t* p, const uint32_t* colv, uint64_t n,
-                             const uint8_t* keep, int sh_row, int sh_pred, int drop_bit,
+                             const uint8_t* keep, int sh_row, int sh_pred, int drop_bit, uint32_t rlo, uint32_t rhi,
                              uint64_t* keys, cudaStream_t st);
+cudaError_t launch_bucket_degree(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n,
+                                 const uint8_t* keep, int shift, unsigned long long* hist, cudaStream_t st);
+cudaError_t launch_add_copy(uint32_t* dst, const uint32_t* src, uint64_t n, uint32_t add, cudaStream_t st);
 // hand-written onesweep LSD radix sort (radix.cu): sorts by key bits [b0, b1);
 // (k0, v0) hold the input, (k1, v1) are same-sized ping-pong buffers; on
 // return *in_second says which pair holds the sorted output.  Stable.
@@ -58,7 +62,8 @@ cudaError_t launch_unique_flags(const uint64_t* keys, uint64_t n, int drop_bit, 
 // keys wider than 63 bits (+ drop flag at drop_hi), lo = b:
 // mode 0 (LSpM format): hi = a << sh | pred; mode 1 (label-major): hi = pred << sh | a
 cudaError_t launch_pack_keys2(const uint32_t* a, const uint32_t* p, const uint32_t* b, uint64_t n, const uint8_t* keep,
-                              int mode, int sh, int drop_hi, uint64_t* hi, uint32_t* lo, cudaStream_t st);
+                              int mode, int sh, int drop_hi, uint32_t rlo, uint32_t rhi, uint64_t* hi, uint32_t* lo,
+                              cudaStream_t st);
 cudaError_t launch_unique_flags2(const uint64_t* hi, const uint32_t* lo, uint64_t n, int drop_hi, uint32_t* flags,
                                  cudaStream_t st);
 // mode 0: a_out = col, pred, counts per row (sh = pb); mode 1: a_out = s, b_out = o,
@@ -75,7 +80,7 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // (p << 2nb | s << nb | o), sorted and de-duplicated like the CSR keys, unpacked
 // into s/o arrays grouped by label; counts[p] += entries of label p
 cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n, const uint8_t* keep,
-                            int nb, int drop_bit, uint64_t* keys, cudaStream_t st);
+                            int nb, int drop_bit, uint32_t rlo, uint32_t rhi, uint64_t* keys, cudaStream_t st);
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
                               uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st);
 // per-row label signature (Fmt::lmask) from row_ptr + pred
@@ -143,6 +148,15 @@ struct LBArgs {
   __device__ __forceinline__ uint32_t* counter() const { return counters + epoch(); }
 #endif
 };
+// world > 1: distance in 32-bit words from this rank's copy of a symmetric
+// buffer to rank q's copy (peer address = local + words[q]); world ranks used
+constexpr int MAX_WORLD = 8;
+struct SymDelta {
+  long long words[MAX_WORLD];
+};
+cudaError_t launch_rank_barrier(unsigned long long* flags_local, const SymDelta& d, uint32_t rank, uint32_t world,
+                                const unsigned long long* gen_base, uint32_t gen_off, cudaStream_t st);
+
 // a3: the first seed of every seeded variable in one launch (blockIdx.y = seed)
 constexpr uint32_t MAX_SEEDS = 16;
 struct SeedBatch {
@@ -185,6 +199,8 @@ struct FilterArgs {
   SkipIf skip;              // re-evaluation guard
   uint32_t center_slot;     // chg[center_slot] = seq when this launch clears a bit
   uint32_t seq;
+  uint32_t world;           // world > 1 (peer exchange): cleared bits and change words go to every rank's copy
+  SymDelta peers;           // (cand and chg live in one symmetric region: one delta per rank)
 };
 // a4, push form of one incident edge (x, l, w, dir): stream the label-major
 // entries of l, mark sat_out(x) for every entry whose center row x is a
@@ -205,10 +221,15 @@ struct PushArgs {
   SkipIf skip;
   unsigned long long* ctr;
 };
+// world > 1 peers for k_and_tracked (the group's push marks AND-ed into cand on every rank)
+struct PeerSet {
+  uint32_t world;
+  SymDelta peers;
+};
 cudaError_t launch_push_edge(const PushArgs& a, int sm_count, cudaStream_t st);
 // cand[0, n_words) &= sat (the group's push edges), change-tracked and skippable like the filter
 cudaError_t launch_and_tracked(uint32_t* cand, const uint32_t* sat, uint32_t n_words, SkipIf skip,
-                               uint32_t center_slot, uint32_t seq, cudaStream_t st, int sm_count);
+                               uint32_t center_slot, uint32_t seq, const PeerSet& ps, cudaStream_t st, int sm_count);
 
 // extra work of the first kernel of an execute (all optional)
 struct InitExtra {
@@ -218,6 +239,10 @@ struct InitExtra {
   uint32_t n_zero = 0;
   unsigned long long* zero2 = nullptr;
   uint32_t n_zero2 = 0;
+  uint32_t* zero32 = nullptr;                      // world > 1: change words in the symmetric region
+  uint32_t n_zero32 = 0;
+  const volatile unsigned long long* h_bar = nullptr;  // pinned: rank-barrier generation base
+  unsigned long long* d_bar = nullptr;
   int* ovf = nullptr;
 };
 cudaError_t launch_init_cands(uint32_t* cand, uint32_t n_slots, uint32_t stride_words, uint32_t n_bits,

@@ -24,6 +24,7 @@ const NcclApi* nccl_api() {
     LOAD(Send, "ncclSend");
     LOAD(Recv, "ncclRecv");
     LOAD(AllReduce, "ncclAllReduce");
+    LOAD(Broadcast, "ncclBroadcast");
     LOAD(GroupStart, "ncclGroupStart");
     LOAD(GroupEnd, "ncclGroupEnd");
     LOAD(GetErrorString, "ncclGetErrorString");

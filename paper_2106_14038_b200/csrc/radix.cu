@@ -202,7 +202,8 @@ static cudaError_t radix_sort_t(K* k0, K* k1, V* v0, V* v1, uint64_t n, int b0, 
   for (int g0 = 0; g0 < npass_total; g0 += RS_MAX_PASSES) {
     const int np = std::min(RS_MAX_PASSES, npass_total - g0);
     const int gb = b0 + 8 * g0;
-    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)RS_MAX_PASSES * 256 * 8 + 64 * 4, st);
+    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)RS_MAX_PASSES * 256 * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, 64 * 4, st);  // tile tickets of every pass
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(status, 0, tiles * 256 * 8, st);
     if (e != cudaSuccess) return e;

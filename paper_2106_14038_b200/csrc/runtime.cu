@@ -139,16 +139,35 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   }
   ctx->rank = cfg->rank;
   ctx->world = cfg->world;
-  if (cfg->world > 1 && cfg->local_comm) {
+  ctx->exchange = cfg->exchange;
+  if (cfg->world > gsm::MAX_WORLD || cfg->exchange > GSMART_XCHG_NCCL || (!cfg->alloc != !cfg->free)) {
+    g_static_err = "world > 8, unknown exchange mode, or only one of alloc/free given";
+    return GSMART_E_INVALID_ARG;
+  }
+  if (cfg->world > 1 && cfg->local_comm) {  // ranks = threads of this process
     if (cfg->local_comm->world != cfg->world) {
       g_static_err = "local_comm world differs from cfg.world";
       return GSMART_E_INVALID_ARG;
     }
     ctx->lcomm = cfg->local_comm;
-  } else if (cfg->world > 1) {
+  } else if (cfg->world > 1) {  // ranks = processes: socket rendezvous named by the unique id
+    if (!cfg->nccl_unique_id) {
+      g_static_err = "world > 1 across processes needs the 128-byte unique id (gsmart_get_nccl_id)";
+      return GSMART_E_INVALID_ARG;
+    }
+    ctx->chan = std::make_unique<gsm::SockChan>();
+    std::string err;
+    if (!ctx->chan->open(cfg->nccl_unique_id, cfg->rank, cfg->world, &err)) {
+      g_static_err = err;
+      return GSMART_E_NCCL;
+    }
+  }
+  // NCCL communicator: the NCCL exchange across processes, or (world == 1 with an
+  // id) a one-rank communicator that runs the same collective calls
+  if (!ctx->lcomm && cfg->nccl_unique_id && (cfg->world == 1 || cfg->exchange == GSMART_XCHG_NCCL)) {
     const NcclApi* api = nccl_api();
-    if (!api || !cfg->nccl_unique_id) {
-      g_static_err = "world > 1 needs NCCL and a unique id (or a local_comm)";
+    if (!api) {
+      g_static_err = "NCCL library (libnccl.so.2) not loadable";
       return GSMART_E_NCCL;
     }
     ncclUniqueId id;
@@ -168,15 +187,25 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
 
 static void free_lspm(gsmart_ctx* ctx) {
   for (auto& f : ctx->f) {
-    dfree(ctx, f.rp);
-    dfree(ctx, f.col);
-    dfree(ctx, f.pred);
-    dfree(ctx, f.lmask);
+    if (f.sym) {
+      cudaStreamSynchronize(ctx->st);
+      sym_free(ctx, &f.s_rp);
+      sym_free(ctx, &f.s_col);
+      sym_free(ctx, &f.s_pred);
+      sym_free(ctx, &f.s_lmask);
+    } else {
+      dfree(ctx, f.rp);
+      dfree(ctx, f.col);
+      dfree(ctx, f.pred);
+      dfree(ctx, f.lmask);
+    }
     f = Lspm();
   }
-  dfree(ctx, ctx->lm.s);
-  dfree(ctx, ctx->lm.o);
-  ctx->lm = LabelMajor();
+  for (LabelMajor* L : {&ctx->lm, &ctx->lm_in}) {
+    dfree(ctx, L->s);
+    dfree(ctx, L->o);
+    *L = LabelMajor();
+  }
   ctx->lspm_gen++;
 }
 
@@ -220,7 +249,7 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
   if (ctx->poisoned) return GSMART_E_CUDA;
   if (n && (!s || !p || !o)) FAIL(GSMART_E_INVALID_ARG, "null triple arrays");
   if (n_entities == 0 || n_entities >= 0x80000000u) FAIL(GSMART_E_INVALID_ARG, "n_entities must be in [1, 2^31)");
-  if (n_predicates == 0 || n_predicates > 65535) FAIL(GSMART_E_INVALID_ARG, "n_predicates must be in [1, 65535]");
+  if (n_predicates == 0 || n_predicates > 65534) FAIL(GSMART_E_INVALID_ARG, "n_predicates must be in [1, 65534]");
   if (n >= 0xffffffffull) FAIL(GSMART_E_INVALID_ARG, "n must be < 2^32 - 1");
   if (flags != GSMART_PTR_HOST && flags != GSMART_PTR_DEVICE) FAIL(GSMART_E_INVALID_ARG, "flags must be PTR_HOST or PTR_DEVICE");
   CU(cudaSetDevice(ctx->cfg.device));
@@ -255,7 +284,7 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
   ctx->n_triples = n;
   ctx->N = n_entities;
   ctx->P = n_predicates;
-  ctx->pred_bytes = n_predicates <= 255 ? 1 : 2;
+  ctx->pred_bytes = n_predicates <= 254 ? 1 : 2;  // 0xff / 0xffff: sentinel label (partitioned LSpM)
   CU(cudaStreamSynchronize(ctx->st));  // caller may free / reuse its buffers after return
   return GSMART_OK;
 }
@@ -279,7 +308,8 @@ struct SortedKeys {
 };
 
 static gsmart_status sort_triple_keys(gsmart_ctx* ctx, Scratch& sc, const uint32_t* a, const uint32_t* b, int mode,
-                                      const uint8_t* d_keep, SortedKeys* out) {
+                                      const uint8_t* d_keep, SortedKeys* out, uint32_t rlo = 0,
+                                      uint32_t rhi = 0xffffffffu) {
   const uint64_t n = ctx->n_triples;
   const int nb = bits_for(ctx->N - 1), pb = bits_for(ctx->P);
   unsigned long long* tot = ctx->d_ctr + 40;
@@ -299,8 +329,8 @@ static gsmart_status sort_triple_keys(gsmart_ctx* ctx, Scratch& sc, const uint32
     TRY(sc.get(&k0, n));
     TRY(sc.get(&k1, n));
     out->drop = 2 * nb + pb;
-    if (mode == 0) CU(launch_pack_keys(a, ctx->d_p, b, n, d_keep, nb + pb, nb, out->drop, k0, ctx->st));
-    else CU(launch_pack_pso(a, ctx->d_p, b, n, d_keep, nb, out->drop, k0, ctx->st));
+    if (mode == 0) CU(launch_pack_keys(a, ctx->d_p, b, n, d_keep, nb + pb, nb, out->drop, rlo, rhi, k0, ctx->st));
+    else CU(launch_pack_pso(a, ctx->d_p, b, n, d_keep, nb, out->drop, rlo, rhi, k0, ctx->st));
     CU(radix_sort_keys_u64(k0, k1, n, 0, out->drop + 1, rtmp, rb, ctx->st, &second, nullptr, true));
     out->k = second ? k1 : k0;
     CU(launch_unique_flags(out->k, n, out->drop, out->pos, ctx->st));
@@ -312,7 +342,7 @@ static gsmart_status sort_triple_keys(gsmart_ctx* ctx, Scratch& sc, const uint32
     TRY(sc.get(&l0, n));
     TRY(sc.get(&l1, n));
     out->drop = nb + pb;
-    CU(launch_pack_keys2(a, ctx->d_p, b, n, d_keep, mode, mode == 0 ? pb : nb, out->drop, h0, l0, ctx->st));
+    CU(launch_pack_keys2(a, ctx->d_p, b, n, d_keep, mode, mode == 0 ? pb : nb, out->drop, rlo, rhi, h0, l0, ctx->st));
     // LSD: the low word first (hi as payload), then the high word (lo as payload)
     CU(radix_sort_pairs_u32_u64(l0, l1, h0, h1, n, 0, nb, rtmp, rb, ctx->st, &second, nullptr, true));
     uint64_t *hc = second ? h1 : h0, *ho = second ? h0 : h1;
@@ -329,7 +359,122 @@ static gsmart_status sort_triple_keys(gsmart_ctx* ctx, Scratch& sc, const uint32
   return GSMART_OK;
 }
 
+// ---- world > 1: the partitioned LSpM.  Rank r stores the rows
+// [v_r, v_r+1) of a format in its own chunks of four symmetric regions (row
+// pointers, columns, labels, row label signatures); every rank maps every chunk,
+// so the kernels read any row through one pointer (peer loads over NVLink).
+// Entry space: rank r's entries start at G_r, a multiple of 2^21 entries (so the
+// column/label chunks start on a mapping granule), with room for M_r + 64;
+// the gap before G_r+1 is filled with sentinel entries (label 0xff.. > any
+// label, column 0xffffffff >= N) that end the rank's last row: rows stay
+// sorted by (label, col) and no label search ever reaches them.
+constexpr uint64_t PART_ALIGN_ENTRIES = 1ull << 21;
+
+static gsmart_status compute_partition(gsmart_ctx* ctx, const uint8_t* d_keep) {
+  const int W = ctx->world;
+  const uint32_t N = ctx->N;
+  const uint32_t nbk = (N + PART_ALIGN_ROWS - 1) / PART_ALIGN_ROWS;
+  Scratch sc(ctx);
+  unsigned long long* hist = nullptr;
+  TRY(sc.get(&hist, nbk));
+  CU(cudaMemsetAsync(hist, 0, (size_t)nbk * 8, ctx->st));
+  if (ctx->n_triples)
+    CU(launch_bucket_degree(ctx->d_s, ctx->d_p, ctx->d_o, ctx->n_triples, d_keep, 19, hist, ctx->st));
+  std::vector<unsigned long long> h(nbk);
+  CU(cudaMemcpyAsync(h.data(), hist, (size_t)nbk * 8, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  ctx->part.v.assign(W + 1, 0);
+  if (gsmart_partition_split((const uint64_t*)h.data(), nbk, N, W, ctx->part.v.data()) != GSMART_OK)
+    FAIL(GSMART_E_INVALID_ARG, "partition split failed");
+  // every rank must have passed the same triples: the same split points
+  std::vector<uint32_t> all((size_t)W * (W + 1));
+  TRY(host_allgather(ctx, ctx->part.v.data(), (W + 1) * 4, all.data()));
+  for (int q = 0; q < W; q++)
+    if (memcmp(all.data() + (size_t)q * (W + 1), ctx->part.v.data(), (W + 1) * 4) != 0)
+      FAIL(GSMART_E_INVALID_ARG, "world > 1: every rank must load the same triple set");
+  return GSMART_OK;
+}
+
+// offset of a chunk of `bytes` for rows [lo, hi): at lo*elt when the range is
+// non-empty, else parked past every real chunk (never read)
+static uint64_t row_chunk_off(gsmart_ctx* ctx, uint32_t lo, uint32_t hi, uint64_t elt) {
+  const uint64_t g = sym_granularity(ctx);
+  if (hi > lo) return (uint64_t)lo * elt;
+  const uint64_t end = ((uint64_t)ctx->N + 1) * elt;
+  return (end + g - 1) / g * g + (uint64_t)ctx->rank * g;
+}
+
+static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
+  Lspm& L = ctx->f[fmt];
+  const uint64_t n = ctx->n_triples;
+  const int W = ctx->world, me = ctx->rank, pbytes = ctx->pred_bytes;
+  const uint32_t N = ctx->N;
+  const int nb = bits_for(N - 1), pb = bits_for(ctx->P);
+  const uint32_t rlo = ctx->part.v[me], rhi = ctx->part.v[me + 1], nloc = rhi - rlo;
+  int last_rank = 0;  // the rank holding row N - 1 also stores row_ptr[N]
+  for (int q = 0; q < W; q++)
+    if (ctx->part.v[q] < ctx->part.v[q + 1]) last_rank = q;
+  const bool last = me == last_rank;
+  Scratch sc(ctx);
+  const uint32_t* rowv = fmt == 0 ? ctx->d_s : ctx->d_o;
+  const uint32_t* colv = fmt == 0 ? ctx->d_o : ctx->d_s;
+  unsigned long long* tot = ctx->d_ctr + 40;
+  SortedKeys sk;
+  TRY(sort_triple_keys(ctx, sc, rowv, colv, 0, d_keep, &sk, rlo, rhi));
+  std::vector<unsigned long long> Ms(W);
+  TRY(host_allgather(ctx, &sk.M, 8, Ms.data()));
+  std::vector<uint64_t> G(W + 1, 0);
+  for (int q = 0; q < W; q++)
+    G[q + 1] = G[q] + (Ms[q] + 64 + PART_ALIGN_ENTRIES - 1) / PART_ALIGN_ENTRIES * PART_ALIGN_ENTRIES;
+  if (G[W] >= 0xffffffffull) FAIL(GSMART_E_UNSUPPORTED, "more than 2^32 padded entries in one LSpM format");
+  const uint64_t span = G[me + 1] - G[me];
+  TRY(sym_alloc(ctx, G[me] * 4, span * 4, &L.s_col));
+  TRY(sym_alloc(ctx, G[me] * pbytes, span * pbytes, &L.s_pred));
+  TRY(sym_alloc(ctx, row_chunk_off(ctx, rlo, rhi, 4), ((uint64_t)nloc + (last ? 1 : 0)) * 4, &L.s_rp));
+  TRY(sym_alloc(ctx, row_chunk_off(ctx, rlo, rhi, 4), (uint64_t)nloc * 4, &L.s_lmask));
+  uint32_t* col_l = (uint32_t*)L.s_col.local();
+  void* pred_l = L.s_pred.local();
+  // sentinel entries past this rank's last real one (see above)
+  CU(cudaMemsetAsync(col_l + sk.M, 0xff, (span - sk.M) * 4, ctx->st));
+  CU(cudaMemsetAsync((char*)pred_l + sk.M * pbytes, 0xff, (span - sk.M) * pbytes, ctx->st));
+  uint32_t* cnt = nullptr;
+  TRY(sc.get(&cnt, (uint64_t)nloc + 1));
+  CU(cudaMemsetAsync(cnt, 0, ((uint64_t)nloc + 1) * 4, ctx->st));
+  uint32_t* cnt_rows = cnt - rlo;  // indexed by global row
+  if (n && !sk.wide)
+    CU(launch_unpack(sk.k, n, sk.pos, sk.drop, nb + pb, nb, col_l, pred_l, pbytes, cnt_rows, ctx->st));
+  else if (n)
+    CU(launch_unpack2(sk.k, sk.lo, n, sk.pos, sk.drop, pb, 0, col_l, pred_l, pbytes, nullptr, cnt_rows, ctx->st));
+  {
+    void* stmp = nullptr;
+    TRY(sc.get((char**)&stmp, scan_tmp_bytes((uint64_t)nloc + 1)));
+    CU(scan_exclusive_u32(cnt, cnt, (uint64_t)nloc + 1, tot, stmp, ctx->st, nullptr));
+  }
+  if (nloc || last)
+    CU(launch_add_copy((uint32_t*)L.s_rp.local(), cnt, (uint64_t)nloc + (last ? 1 : 0), (uint32_t)G[me], ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  TRY(host_barrier(ctx));  // every rank's row pointers are in place (the last row reads the next chunk)
+  L.rp = (uint32_t*)L.s_rp.va;
+  L.col = (uint32_t*)L.s_col.va;
+  L.pred = (void*)L.s_pred.va;
+  L.lmask = (uint32_t*)L.s_lmask.va;
+  if (nloc) CU(launch_label_mask(L.rp + rlo, L.pred, pbytes, nloc, L.lmask + rlo, ctx->st));
+  CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
+  if (nloc) CU(launch_heavy_stats(L.rp + rlo, nloc, ctx->d_ctr + 42, ctx->st));
+  unsigned long long hv[2];
+  TRY(readback(ctx, ctx->d_ctr + 42, 2, hv));
+  L.heavy_rows = hv[0];
+  L.heavy_chunks = hv[1];
+  L.nnz = 0;
+  for (int q = 0; q < W; q++) L.nnz += Ms[q];
+  L.sym = true;
+  L.built = true;
+  TRY(host_barrier(ctx));
+  return GSMART_OK;
+}
+
 static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
+  if (ctx->world > 1) return build_format_part(ctx, fmt, d_keep);
   Lspm& L = ctx->f[fmt];
   const uint64_t n = ctx->n_triples;
   const uint32_t N = ctx->N;
@@ -368,9 +513,12 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
   return GSMART_OK;
 }
 
-// label-major lists: the kept, de-duplicated triples sorted by (p, s, o)
-static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep) {
-  LabelMajor& L = ctx->lm;
+// label-major lists: the kept, de-duplicated triples sorted by (p, s, o).
+// world > 1 (in_side = false): only this rank's subjects; in_side = true: this
+// rank's objects, sorted by (p, o, s) and stored as (o, s) — the center of an
+// IN edge comes first, like the subject of an OUT edge.
+static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, bool in_side = false) {
+  LabelMajor& L = in_side ? ctx->lm_in : ctx->lm;
   const uint64_t n = ctx->n_triples;
   const int nb = bits_for(ctx->N - 1);
   Scratch sc(ctx);
@@ -378,7 +526,10 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep) {
   TRY(sc.get(&cnt, (uint64_t)ctx->P + 2));
   CU(cudaMemsetAsync(cnt, 0, ((size_t)ctx->P + 2) * 4, ctx->st));
   SortedKeys sk;
-  TRY(sort_triple_keys(ctx, sc, ctx->d_s, ctx->d_o, 1, d_keep, &sk));
+  const uint32_t rlo = ctx->world > 1 ? ctx->part.v[ctx->rank] : 0u;
+  const uint32_t rhi = ctx->world > 1 ? ctx->part.v[ctx->rank + 1] : 0xffffffffu;
+  TRY(sort_triple_keys(ctx, sc, in_side ? ctx->d_o : ctx->d_s, in_side ? ctx->d_s : ctx->d_o, 1, d_keep, &sk, rlo,
+                       rhi));
   const unsigned long long M = sk.M;
   TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
   TRY(dalloc(ctx, &L.o, M + 4));
@@ -413,9 +564,26 @@ extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep
   uint8_t* d_keep = nullptr;
   TRY(sc.get(&d_keep, keep.size()));
   CU(cudaMemcpyAsync(d_keep, keep.data(), keep.size(), cudaMemcpyHostToDevice, ctx->st));
-  for (int fmt = 0; fmt < 2; fmt++)
+  static const bool trace = getenv("GSMART_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(ctx->st);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gsmart] build %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  if (ctx->world > 1) TRY(compute_partition(ctx, d_keep));
+  lap("partition");
+  for (int fmt = 0; fmt < 2; fmt++) {
     if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_keep));
-  if (formats == (GSMART_CSR | GSMART_CSC)) TRY(build_label_major(ctx, d_keep));
+    lap(fmt == 0 ? "csr" : "csc");
+  }
+  if (formats == (GSMART_CSR | GSMART_CSC)) {
+    TRY(build_label_major(ctx, d_keep));
+    if (ctx->world > 1) TRY(build_label_major(ctx, d_keep, true));
+    lap("label-major");
+  }
   CU(cudaStreamSynchronize(ctx->st));
   return GSMART_OK;
 }
@@ -475,8 +643,13 @@ extern "C" void gsmart_plan_free(gsmart_plan_t* plan) {
       ctx->p2_guess.erase(uid);
       ctx->plan_cost.erase(uid);
       bool any = false;
-      for (auto& sp : ctx->slots)
+      for (auto& sp : ctx->slots) {
         for (auto& kv : sp->graphs) any = any || (kv.first >> 3) == uid;
+        for (auto it = sp->seen.begin(); it != sp->seen.end();) {
+          if ((*it >> 3) == uid) it = sp->seen.erase(it);
+          else ++it;
+        }
+      }
       if (!any) continue;
       if (dev0 < 0) cudaGetDevice(&dev0);
       cudaSetDevice(ctx->cfg.device);
@@ -556,7 +729,7 @@ extern "C" void gsmart_result_free(gsmart_result* r) {
   if (r->ctx) {
     cudaSetDevice(r->ctx->cfg.device);
     cudaStream_t st = r->st ? r->st : r->ctx->st;
-    for (void* p : r->owned) cudaFreeAsync(p, st);
+    for (void* p : r->owned) dfree(r->ctx, st, p);
     if (r->h_rows) r->ctx->pinned.put(r->h_rows, r->h_cls);
   }
   delete r;

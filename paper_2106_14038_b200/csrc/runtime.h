@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -27,6 +28,22 @@ enum Kid {
 };
 extern const char* kKernelNames[GSMART_NKERNELS];
 
+// One symmetric region (symheap.cu): rank q's chunk is mapped at va + off[q] on
+// every rank; this rank's own chunk is local().
+struct SymRegion {
+  uint64_t va = 0, total = 0;
+  std::vector<uint64_t> off, bytes;
+  std::vector<unsigned long long> handles;  // CUmemGenericAllocationHandle per rank
+  bool own_only = false;                    // handles shared in-process: release only our own
+  int rank = 0;
+  char* local() const { return va ? (char*)(va + off[rank]) : nullptr; }
+  SymDelta delta(int world) const {         // word (4-byte) distance from our chunk to rank q's
+    SymDelta d{};
+    for (int q = 0; q < world && q < MAX_WORLD; q++) d.words[q] = ((long long)off[q] - (long long)off[rank]) / 4;
+    return d;
+  }
+};
+
 struct Lspm {
   uint32_t* rp = nullptr;
   uint32_t* col = nullptr;
@@ -35,6 +52,10 @@ struct Lspm {
   uint64_t nnz = 0;
   bool built = false;
   unsigned long long heavy_rows = 0, heavy_chunks = 0;
+  // world > 1: rp/col/pred/lmask point into symmetric regions (global view of
+  // every rank's rows); this rank stores rows [row_lo, row_hi) only
+  bool sym = false;
+  SymRegion s_rp, s_col, s_pred, s_lmask;
 };
 
 // Label-major entry lists: the kept, de-duplicated triples grouped by predicate,
@@ -48,6 +69,27 @@ struct LabelMajor {
   bool built = false;
 };
 
+// 1-D vertex-range partition (world > 1): rank q owns rows [v[q], v[q+1]) of
+// both formats; split points balance out+in entries, aligned to 2^19 vertices
+// (2 MiB of row pointers: the granularity of a symmetric chunk)
+constexpr uint32_t PART_ALIGN_ROWS = 1u << 19;
+struct Partition {
+  std::vector<uint32_t> v;  // world + 1 split points
+};
+
+// host side of the ranks-as-processes rendezvous (symheap.cu): a star of
+// abstract Unix sockets through rank 0, for small all-gathers and SCM_RIGHTS
+// file-descriptor exchange of symmetric chunks
+struct SockChan {
+  int rank = 0, world = 1;
+  int listen_fd = -1;
+  std::vector<int> peers;  // rank 0: one socket per peer; others: [0] = socket to rank 0
+  ~SockChan();
+  bool open(const void* id128, int rank, int world, std::string* err);
+  bool allgather(const void* mine, size_t n, void* all);
+  bool allgather_fds(int my_fd, std::vector<int>* fds);
+};
+
 inline int bits_for(uint64_t v) {  // bits to represent values in [0, v]
   int b = 1;
   while (b < 64 && (v >> b) != 0) b++;
@@ -58,6 +100,7 @@ constexpr uint32_t LB_CAP_TILES = 1u << 22;  // 4M tiles x 1024 entries = the 2^
 constexpr uint32_t LB_EPOCHS = 65536;
 constexpr uint32_t MAX_SLOTS = 16;
 constexpr uint32_t H_EPOCH = 255;  // h_pin slot: look-back epoch base of the running execute
+constexpr uint32_t H_BAR = 254;    // h_pin slot: rank-barrier generation base (world > 1)
 
 // One concurrent execution lane: a stream plus everything an in-flight
 // execute writes (workspace, look-back state, counters, pinned readback).
@@ -95,15 +138,25 @@ struct Slot {
   uint64_t p2_cap = 0;
   uint32_t* d_epoch = nullptr;         // device base epoch of the current launch sequence
   uint32_t epoch_next = 1, seq_base = 1, seq_off = 0;
+  // world > 1 (peer exchange): candidate bitmaps, change words and barrier flags
+  // in a symmetric region; barrier generations base + off (device-resident base)
+  SymRegion sym;
+  uint64_t sym_cand_words = 0;
+  SymRegion gath;                      // world > 1: rows of every rank, read by rank 0
+  uint64_t gath_cap = 0;               // bytes per rank
+  unsigned long long* d_bar = nullptr;  // device copy of the barrier generation base
+  uint64_t bar_next = 1, bar_base = 1;
+  uint32_t bar_off = 0;
   uint64_t ws_gen = 0;                 // bumped whenever a workspace buffer moves
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     uint64_t ws_gen = 0, lspm_gen = 0;
-    uint32_t flags = 0, n_lb = 0, off0 = 0;
+    uint32_t flags = 0, n_lb = 0, off0 = 0, n_bar = 0, bar0 = 0;
     std::vector<int> launches;  // kernel launches inside the graph, per kernel class
     uint64_t filter_main = 0, push_and = 0;
   };
   std::unordered_map<uint64_t, GraphEntry> graphs;  // (plan uid << 3 | phase tag) -> captured work
+  std::unordered_set<uint64_t> seen;                // keys run once without capture
 };
 
 // Small persistent host thread pool (hostio.cu): run(f) calls f(i) on every
@@ -160,6 +213,7 @@ struct gsmart_comm {
   std::vector<const void*> ptr;
   std::vector<int> dev;
   std::vector<unsigned long long> val;
+  std::vector<std::string> blob;  // host all-gather of byte strings
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     uint64_t g = gen;
@@ -186,6 +240,10 @@ struct gsmart_ctx {
   int pred_bytes = 1;
   gsm::Lspm f[2];
   gsm::LabelMajor lm;
+  gsm::LabelMajor lm_in;     // world > 1: label-major entries whose OBJECT is this rank's (stored as (o, s))
+  gsm::Partition part;       // world > 1: vertex ranges of the ranks
+  std::unique_ptr<gsm::SockChan> chan;  // world > 1, ranks are processes
+  uint32_t exchange = GSMART_XCHG_PEER;
   // push/pull choice per plan (uid -> lspm_gen, per group per edge), DESIGN.md §5
   std::unordered_map<uint64_t, std::pair<uint64_t, std::vector<std::vector<uint8_t>>>> push_cache;
   std::unordered_map<uint64_t, unsigned long long> plan_cost;  // uid -> work of its last execute (batch start order)
@@ -250,11 +308,21 @@ gsmart_status cuda_fail(gsmart_ctx* ctx, cudaError_t e, const char* what, int li
     if (s_ != GSMART_OK) return s_; \
   } while (0)
 
+// Device memory: the caller's allocator hooks (gsmart_config.alloc/free) when
+// given, else the stream-ordered allocator of the device's default pool.
 template <typename T>
 gsmart_status dalloc(gsmart_ctx* ctx, T** p, uint64_t count, cudaStream_t st) {
   *p = nullptr;
   size_t bytes = std::max<uint64_t>(count, 1) * sizeof(T);
   bytes = (bytes + 255) / 256 * 256;
+  if (ctx->cfg.alloc) {
+    *p = (T*)ctx->cfg.alloc(bytes, (void*)st, ctx->cfg.alloc_user);
+    if (!*p) {
+      ctx->err = "allocator hook returned NULL";
+      return GSMART_E_OOM;
+    }
+    return GSMART_OK;
+  }
   cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocAsync", __LINE__);
   return GSMART_OK;
@@ -264,10 +332,12 @@ gsmart_status dalloc(gsmart_ctx* ctx, T** p, uint64_t count) {
   return dalloc(ctx, p, count, ctx->st);
 }
 
-inline void dfree(cudaStream_t st, void* p) {
-  if (p) cudaFreeAsync(p, st);
+inline void dfree(gsmart_ctx* ctx, cudaStream_t st, void* p) {
+  if (!p) return;
+  if (ctx->cfg.free) ctx->cfg.free(p, (void*)st, ctx->cfg.alloc_user);
+  else cudaFreeAsync(p, st);
 }
-inline void dfree(gsmart_ctx* ctx, void* p) { dfree(ctx->st, p); }
+inline void dfree(gsmart_ctx* ctx, void* p) { dfree(ctx, ctx->st, p); }
 
 // stream-ordered scratch freed at scope exit
 struct Scratch {
@@ -277,7 +347,7 @@ struct Scratch {
   Scratch(gsmart_ctx* c, cudaStream_t s) : ctx(c), st(s) {}
   explicit Scratch(gsmart_ctx* c) : ctx(c), st(c->st) {}
   ~Scratch() {
-    for (void* p : ptrs) dfree(st, p);
+    for (void* p : ptrs) dfree(ctx, st, p);
   }
   template <typename T>
   gsmart_status get(T** p, uint64_t count) {
@@ -292,22 +362,31 @@ gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_p
 
 void slots_free(gsmart_ctx* ctx);
 
+// symheap.cu: host all-gather / barrier over the ranks (in-process comm or
+// sockets), symmetric regions, device barrier across ranks
+gsmart_status host_allgather(gsmart_ctx* ctx, const void* mine, size_t n, void* all);
+gsmart_status host_barrier(gsmart_ctx* ctx);
+size_t sym_granularity(gsmart_ctx* ctx);
+gsmart_status sym_alloc(gsmart_ctx* ctx, uint64_t my_off, uint64_t my_bytes, SymRegion* out);
+void sym_free(gsmart_ctx* ctx, SymRegion* R);
+
 // hostio.cu
 bool host_is_pinned(const void* p);
 gsmart_status h2d_staged(gsmart_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
 void stage_ring_free(gsmart_ctx* ctx);
 gsmart_status rows_to_host(gsmart_ctx* ctx, gsmart_result* r, cudaStream_t st);
 
-// ---- 1-D vertex-range partition of the bitmaps: rank r owns
-// words [r*slice, min((r+1)*slice, n_words)) with slice a multiple of 32 words.
-inline uint32_t partition_slice(uint32_t n_words, int world) {
-  const uint32_t chunks = (n_words + 31) / 32;
-  return ((chunks + world - 1) / world) * 32;
+// bitmap words [lo, hi) of rank q's vertex range (empty range: 0, 0)
+inline uint32_t part_word_lo(const gsmart_ctx* ctx, int q) {
+  return ctx->part.v[q] < ctx->part.v[q + 1] ? ctx->part.v[q] / 32 : 0u;
+}
+inline uint32_t part_word_hi(const gsmart_ctx* ctx, int q) {
+  return ctx->part.v[q] < ctx->part.v[q + 1] ? (ctx->part.v[q + 1] + 31) / 32 : 0u;
 }
 
-// ---- collectives for world > 1 (NCCL or the in-process communicator), comm.cu
-// In-place all-gather: rank r's bytes_per_rank bytes at buf + r*bytes_per_rank.
-gsmart_status coll_allgather(gsmart_ctx* ctx, cudaStream_t st, void* buf, size_t bytes_per_rank);
+// ---- collectives of the baseline exchange (NCCL or the in-process communicator), comm.cu
+// In-place all-gather of the ranks' word ranges of a replicated bitmap.
+gsmart_status coll_allgatherv(gsmart_ctx* ctx, cudaStream_t st, uint32_t* bm);
 // Host values of all ranks (blocking).
 gsmart_status coll_allgather_host(gsmart_ctx* ctx, cudaStream_t st, unsigned long long v,
                                   std::vector<unsigned long long>* out);

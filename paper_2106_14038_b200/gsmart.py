@@ -32,10 +32,17 @@ class GsmartError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+GSMART_XCHG_PEER, GSMART_XCHG_NCCL = 0, 1
+
+
 class gsmart_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("max_result_rows", ctypes.c_uint64), ("local_comm", ctypes.c_void_p)]
+                ("max_result_rows", ctypes.c_uint64), ("local_comm", ctypes.c_void_p),
+                ("exchange", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("alloc_user", ctypes.c_void_p)]
 
 
 class gsmart_lspm_view(ctypes.Structure):
@@ -103,7 +110,9 @@ def _load():
         "gsmart_copy_to_host": (st, [vp, vp, vp, ctypes.c_size_t]),
         "gsmart_comm_create_local": (st, [ctypes.c_int, ctypes.POINTER(vp)]),
         "gsmart_comm_destroy": (None, [vp]),
-        "gsmart_partition_words": (st, [u32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(u32), ctypes.POINTER(u32)]),
+        "gsmart_partition_split": (st, [ctypes.POINTER(u64), u32, u32, ctypes.c_int, ctypes.POINTER(u32)]),
+        "gsmart_partition_get": (st, [vp, ctypes.POINTER(u32)]),
+        "gsmart_rendezvous_check": (st, [vp, ctypes.c_int, ctypes.c_int, u64, ctypes.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -119,7 +128,8 @@ EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gs
             "gsmart_result_shape",
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
             "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host",
-            "gsmart_comm_create_local", "gsmart_comm_destroy", "gsmart_partition_words"]
+            "gsmart_comm_create_local", "gsmart_comm_destroy", "gsmart_partition_split", "gsmart_partition_get",
+            "gsmart_rendezvous_check"]
 
 
 def lib():
@@ -147,8 +157,13 @@ def gsmart_get_nccl_id():
     return buf.raw
 
 
-def gsmart_create(device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None):
+def gsmart_create(device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None,
+                  exchange=GSMART_XCHG_PEER, alloc=None, free=None):
+    """alloc/free: optional ALLOC_FN / FREE_FN callbacks (keep them alive while the ctx lives)."""
     cfg = gsmart_config()
+    cfg.exchange = exchange
+    if alloc is not None:
+        cfg.alloc, cfg.free = alloc, free
     cfg.local_comm = local_comm.value if isinstance(local_comm, ctypes.c_void_p) else local_comm
     cfg.device, cfg.rank, cfg.world = device, rank, world
     idbuf = None
@@ -172,10 +187,29 @@ def gsmart_comm_destroy(comm):
     _lib.gsmart_comm_destroy(comm)
 
 
-def gsmart_partition_words(n_entities, world, rank):
-    lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
-    _check(_lib.gsmart_partition_words(n_entities, world, rank, ctypes.byref(lo), ctypes.byref(hi)))
-    return lo.value, hi.value
+PART_ALIGN_ROWS = 1 << 19
+
+
+def gsmart_partition_split(bucket_counts, n_entities, world):
+    """Split points v[0..world] of the nnz-balanced vertex-range partition."""
+    b = np.ascontiguousarray(np.asarray(bucket_counts, dtype=np.uint64))
+    v = (ctypes.c_uint32 * (world + 1))()
+    _check(_lib.gsmart_partition_split(b.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) if len(b) else None,
+                                       len(b), int(n_entities), world, v))
+    return [v[i] for i in range(world + 1)]
+
+
+def gsmart_rendezvous_check(id128, rank, world, value):
+    buf = ctypes.create_string_buffer(bytes(id128), 128)
+    out = (ctypes.c_uint64 * world)()
+    _check(_lib.gsmart_rendezvous_check(buf, rank, world, value, out))
+    return [out[i] for i in range(world)]
+
+
+def gsmart_partition_get(ctx, world):
+    v = (ctypes.c_uint32 * (world + 1))()
+    _check(_lib.gsmart_partition_get(ctx, v), ctx)
+    return [v[i] for i in range(world + 1)]
 
 
 def gsmart_destroy(ctx):
@@ -194,13 +228,13 @@ def _ptr_kind(a):
         if isinstance(a, torch.Tensor):
             if a.dtype not in (torch.int32,) and str(a.dtype) != "torch.uint32":
                 raise TypeError("triple tensors must be int32/uint32")
-            a = a.contiguous()
-            if a.is_cuda:
-                return a.data_ptr(), a, GSMART_PTR_DEVICE
-            a = a.numpy()
+            a = a.contiguous()  # int32 and uint32 share the bit pattern: ids are checked on the device
+            return a.data_ptr(), a, (GSMART_PTR_DEVICE if a.is_cuda else GSMART_PTR_HOST)
     except ImportError:
         pass
-    arr = np.asarray(a)
+    arr = np.ascontiguousarray(np.asarray(a))
+    if arr.dtype == np.int32:
+        return arr.ctypes.data, arr, GSMART_PTR_HOST  # viewed as uint32; negative ids fail the device check
     if arr.size and arr.dtype != np.uint32:
         if arr.dtype.kind not in "iu":
             raise TypeError("triple arrays must hold integers")
@@ -367,8 +401,11 @@ def gsmart_copy_to_host(ctx, dev_ptr, nbytes, dtype=np.uint32):
 class Engine:
     """One context: load -> build -> query.  Thin sugar over the functions above."""
 
-    def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None):
-        self.ctx = gsmart_create(device, rank, world, nccl_id, stream, max_result_rows, local_comm)
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None, max_result_rows=0, local_comm=None,
+                 exchange=GSMART_XCHG_PEER, alloc=None, free=None):
+        self._hooks = (alloc, free)  # the C side holds raw function pointers
+        self.ctx = gsmart_create(device, rank, world, nccl_id, stream, max_result_rows, local_comm, exchange,
+                                 alloc, free)
         self.rank, self.world = rank, world
 
     def load(self, s, p, o, n_entities, n_predicates, keep=None):
