@@ -100,7 +100,7 @@ typedef struct {
    * device buffer the library owns, except the world > 1 symmetric regions
    * (which need the virtual-memory API), comes from alloc(bytes, stream, user)
    * and returns through free(ptr, stream, user), ordered on `stream`.  NULL:
-   * cudaMallocAsync / cudaFreeAsync on the device's default memory pool. */
+   * the stream-ordered allocator on a memory pool of the context's own. */
   void* (*alloc)(size_t bytes, void* stream, void* user);
   void (*free)(void* ptr, void* stream, void* user);
   void* alloc_user;

@@ -10,6 +10,7 @@ namespace gsm {
 constexpr int MAXG = 16;          // max edges per direction in one group evaluation
 constexpr int MAXL = 32;          // max trie levels (= variables)
 constexpr int MAXC = 16;          // max closing edges per level
+constexpr int MAXANC = 4;         // max materialised ancestor-binding columns per trie level
 constexpr uint32_t SHORT_ROW = 32;     // rows <= this: one lane scans it (group filter)
 constexpr uint32_t MED_SCAN = 64;      // longer rows: a lane probes up to this many entries of a label
 constexpr uint32_t HEAVY_ROW = 16384;  // rows > this: split into chunks across CTAs

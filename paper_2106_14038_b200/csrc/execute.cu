@@ -52,6 +52,7 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   for (auto& b : s.lv) {
     dfree(ctx, st, b.bind); dfree(ctx, st, b.parent); dfree(ctx, st, b.seg_beg); dfree(ctx, st, b.off); dfree(ctx, st, b.newidx);
     dfree(ctx, st, b.alive);
+    for (int i = 0; i < MAXANC; i++) dfree(ctx, st, b.anc[i]);
   }
   for (int k = 0; k < GSMART_MAX_LEVELS; k++) dfree(ctx, st, s.list[k]);
   dfree(ctx, st, s.lb_status); dfree(ctx, st, s.lb_counters); dfree(ctx, st, s.tile_start); dfree(ctx, st, s.d_sz); dfree(ctx, st, s.d_ctr);
@@ -144,14 +145,26 @@ static LBArgs next_lb(Slot& s) {
   return a;
 }
 
-static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t need) {
+static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t need, uint32_t n_anc = 0) {
   auto& b = s.lv[k];
-  if (b.bind && b.cap >= need) return GSMART_OK;
+  if (b.bind && b.cap >= need) {
+    for (uint32_t i = 0; i < n_anc; i++)  // ancestor columns this plan needs at level k
+      if (!b.anc[i]) {
+        TRY(dalloc(ctx, &b.anc[i], b.cap, s.st));
+        s.ws_gen++;
+      }
+    return GSMART_OK;
+  }
+  uint32_t keep_anc = n_anc;
+  for (uint32_t i = 0; i < (uint32_t)MAXANC; i++)
+    if (b.anc[i]) keep_anc = std::max(keep_anc, i + 1);
   uint64_t cap = std::max<uint64_t>(need, std::max<uint64_t>(2 * b.cap, 1u << 16));
   cap = (cap + 1023) / 1024 * 1024;
   dfree(ctx, s.st, b.bind); dfree(ctx, s.st, b.parent); dfree(ctx, s.st, b.seg_beg); dfree(ctx, s.st, b.off); dfree(ctx, s.st, b.newidx);
   dfree(ctx, s.st, b.alive);
+  for (uint32_t i = 0; i < (uint32_t)MAXANC; i++) dfree(ctx, s.st, b.anc[i]);
   b = Slot::LvBuf();
+  for (uint32_t i = 0; i < keep_anc; i++) TRY(dalloc(ctx, &b.anc[i], cap, s.st));
   TRY(dalloc(ctx, &b.bind, cap, s.st));
   TRY(dalloc(ctx, &b.parent, cap, s.st));
   TRY(dalloc(ctx, &b.seg_beg, cap, s.st));
@@ -231,6 +244,41 @@ struct Exec {
   uint64_t filter_main = 0;  // main group-filter launches (one bitmap pass each)
   uint32_t filter_seq = 0;             // group evaluations issued so far (SkipIf sequence)
   std::vector<std::vector<GroupEdge>> gedges;  // per group: its edges, then its back edges (Eq. 16)
+  // per trie level k: the older levels (< k) whose bindings deeper levels read
+  // (tree-edge parents, closing-edge targets), carried as columns by level k's
+  // nodes — at most MAXANC, the rest are found by walking parent pointers
+  std::vector<std::vector<uint32_t>> anc_cols;
+  void plan_ancestors() {
+    anc_cols.assign(L, {});
+    std::vector<std::vector<uint32_t>> need(L);
+    for (uint32_t k = 1; k < L; k++) {
+      const Level& Lv = plan->levels[k];
+      if (Lv.tree_edge >= 0) need[k].push_back(Lv.parent_level);
+      for (auto& c : Lv.closing)
+        if (c.other_level != k) need[k].push_back(c.other_level);
+    }
+    for (uint32_t k = 1; k < L; k++) {
+      std::vector<uint32_t> cols;
+      for (uint32_t kk = k + 1; kk < L; kk++)
+        for (uint32_t j : need[kk])
+          if (j < k && std::find(cols.begin(), cols.end(), j) == cols.end()) cols.push_back(j);
+      std::sort(cols.begin(), cols.end());
+      // a column of level k must be derivable from level k-1: its own binding or its column
+      std::vector<uint32_t> ok;
+      for (uint32_t j : cols)
+        if ((j == k - 1 || std::find(anc_cols[k - 1].begin(), anc_cols[k - 1].end(), j) != anc_cols[k - 1].end()) &&
+            ok.size() < (size_t)MAXANC)
+          ok.push_back(j);
+      anc_cols[k] = ok;
+    }
+  }
+  // where expanding level k (parent level k-1) finds the binding of level j
+  int anc_index(uint32_t k, uint32_t j) const {
+    if (j == k - 1) return ANC_BIND;
+    const auto& c = anc_cols[k - 1];
+    auto it = std::find(c.begin(), c.end(), j);
+    return it == c.end() ? ANC_WALK : (int)(it - c.begin());
+  }
   std::vector<std::vector<uint8_t>> push_dec;  // per group, per edge of gedges: push form (label-major)
   uint64_t push_and = 0;               // k_and_tracked launches (bitmap bytes)
   std::vector<uint32_t> group_seq;     // per group: sequence of its last evaluation
@@ -567,11 +615,19 @@ struct Exec {
       a.f[1] = fa[1];
       a.cand = cand(Lv.var);
       for (auto& c : Lv.closing) {
+        a.cl_idx[a.ncl] = c.other_level == k ? ANC_WALK : anc_index(k, c.other_level);
         ClosingDev& d = a.cl[a.ncl++];
         d.label = c.label;
         d.other_level = c.other_level;
         d.dir = c.dir == OUT ? 0 : 1;
         d.self = c.other_level == k ? 1u : 0u;
+      }
+      a.par_idx = a.tree ? anc_index(k, Lv.parent_level) : ANC_WALK;
+      for (size_t i = 0; i < anc_cols[k - 1].size(); i++) a.par_anc[i] = sl.lv[k - 1].anc[i];
+      a.n_anc_out = (uint32_t)anc_cols[k].size();
+      for (uint32_t i = 0; i < a.n_anc_out; i++) {
+        a.anc_src[i] = anc_index(k, anc_cols[k][i]);
+        a.out_anc[i] = sl.lv[k].anc[i];
       }
       if (!a.tree) {
         prof.begin(K_COMPACT);
@@ -702,7 +758,7 @@ struct Exec {
     }
     if (ctx->filter_variant & 4) TRY(slot_buf(ctx, sl, &sl.frows, &sl.frows_cap, (uint64_t)W * 32));
     if (ctx->lm.built) TRY(slot_buf(ctx, sl, &sl.sat, &sl.sat_cap, 2ull * Wpad));
-    for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1));
+    for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1, (uint32_t)anc_cols[k].size()));
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
     return GSMART_OK;
@@ -829,6 +885,7 @@ struct Exec {
       gedges[gi] = plan->groups[gi].edges;
       gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
     }
+    plan_ancestors();
     TRY(decide_push());
     TRY(ensure_workspace());
     TRY(begin_seq(ctx, sl));
@@ -926,7 +983,7 @@ struct Exec {
         FAIL(GSMART_E_RESULT_OVERFLOW, "trie level " + std::to_string(k) + " exceeds max_result_rows");
       }
       if (F[k] > sl.lv[k].cap) {  // later levels are invalid: grow and re-run the expansion
-        TRY(slot_level(ctx, sl, k, F[k]));
+        TRY(slot_level(ctx, sl, k, F[k], (uint32_t)anc_cols[k].size()));
         if (++attempts > 2 * (int)L + 2) FAIL(GSMART_E_CUDA, "expansion capacity did not converge");
         return relaunch_expansion();
       }

@@ -34,6 +34,14 @@ __device__ __forceinline__ uint32_t ancestor(const LevelTab& t, uint32_t k, uint
   return __ldg(t.bind[j] + n);
 }
 
+// binding of level j for node n of level k-1 (the expansion's parent level):
+// its own binding, a materialised ancestor column, or (fallback) a walk
+__device__ __forceinline__ uint32_t anc_binding(const ExpArgs2& a, int idx, uint32_t n, uint32_t j) {
+  if (idx == ANC_BIND) return __ldg(a.tab.bind[a.k - 1] + n);
+  if (idx >= 0) return __ldg(a.par_anc[idx] + n);
+  return ancestor(a.tab, a.k - 1, n, j);
+}
+
 // ------------------------------------------------------------------ bitmap -> ids
 // One launch, no inter-CTA chain.  The range is cut into <= ~4 chunks per SM of
 // whole 2048-word sub-tiles; a CTA takes a ticket (chunks in ticket order, so it
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
       uint32_t b[SS_I];
 #pragma unroll
       for (int j = 0; j < SS_I; j++)
-        b[j] = ((act >> j) & 1u) ? ancestor(a.tab, a.k - 1, (uint32_t)(base + j), a.parent_level) : 0u;
+        b[j] = ((act >> j) & 1u) ? anc_binding(a, a.par_idx, (uint32_t)(base + j), a.parent_level) : 0u;
 #pragma unroll
       for (int j = 0; j < SS_I; j++)
         if ((act >> j) & 1u) {
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
     if (stgt)
       for (uint32_t i = threadIdx.x; i < nr * a.ncl; i += EX_T) {
         const uint32_t p = i / a.ncl, c = i - p * a.ncl;
-        s_tgt[p * TGTC + c] = a.cl[c].self ? 0u : ancestor(a.tab, a.k - 1, nlo + p, a.cl[c].other_level);
+        s_tgt[p * TGTC + c] = a.cl[c].self ? 0u : anc_binding(a, a.cl_idx[c], nlo + p, a.cl[c].other_level);
       }
     __syncthreads();
     // The EX_I entries of a thread go through each stage together, so their
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
       for (int j = 0; j < EX_I; j++) {
         uint32_t tgt = child[j];
         if (!cl.self && ((keepm >> j) & 1u))
-          tgt = stgt ? s_tgt[(node[j] - nlo) * TGTC + q] : ancestor(a.tab, a.k - 1, node[j], cl.other_level);
+          tgt = stgt ? s_tgt[(node[j] - nlo) * TGTC + q] : anc_binding(a, a.cl_idx[q], node[j], cl.other_level);
         row[j] = tgt;  // temporarily the target
       }
 #pragma unroll
@@ -480,6 +488,9 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
       a.out_parent[pos] = node[j];
       a.out_bind[pos] = child[j];
       if (a.out_alive) a.out_alive[pos] = 0;
+      for (uint32_t i = 0; i < a.n_anc_out; i++)  // ancestor columns the deeper levels read
+        a.out_anc[i][pos] = a.anc_src[i] == ANC_BIND ? __ldg(a.tab.bind[a.k - 1] + node[j])
+                                                     : __ldg(a.par_anc[a.anc_src[i]] + node[j]);
       pos++;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) *a.d_nout = pref + tot;

@@ -1000,35 +1000,68 @@ __global__ void __launch_bounds__(256, SIMD ? 4 : 6) k_group_filter_rows(FilterA
   }
 }
 
-// heavy-row chunks: CTA per chunk, OR of satisfied edge bits into heavy_sat[slot]
+// heavy-row chunks: CTA per chunk, OR of satisfied edge bits into heavy_sat[slot].
+// A chunk is skipped once the row's edges are all satisfied (by other chunks); a
+// chunk scans only the entries inside the direction's label window (two warp
+// searches), 4 independent entries per thread per step, and stops as soon as
+// every edge is satisfied.
 template <typename PT>
 __global__ void __launch_bounds__(256) k_filter_heavy(FilterArgsT<PT> a) {
   GSM_PDL_ENTRY();
-  __shared__ uint32_t s_sat;
+  __shared__ uint32_t s_sat, s_lo, s_hi, s_skip;
   const uint32_t nch = a.heavy_count[1];
   for (uint32_t it = blockIdx.x; it < nch; it += gridDim.x) {
     const uint32_t slot = a.heavy_chunks[2 * it], c = a.heavy_chunks[2 * it + 1];
     const uint32_t rec = a.heavy_rows[slot];
     const uint32_t row = rec & 0x7fffffffu;
     const int d = (int)(rec >> 31);
+    const uint32_t need = (a.ne[d] >= 32) ? 0xffffffffu : ((1u << a.ne[d]) - 1u);
     const uint32_t b0 = a.f[d].rp[row], e0 = a.f[d].rp[row + 1];
     const uint32_t b = b0 + c * HEAVY_CHUNK, e = min(e0, b + HEAVY_CHUNK);
-    if (threadIdx.x == 0) s_sat = 0;
+    __syncthreads();  // the previous chunk is done with the shared words
+    if (threadIdx.x < 32) {
+      const uint32_t lo = warp_lower_bound(a.f[d].pred, b, e, a.minl[d]);
+      const uint32_t hi = warp_lower_bound(a.f[d].pred, lo, e, a.maxl[d] + 1);
+      if (threadIdx.x == 0) {
+        s_lo = lo;
+        s_hi = hi;
+        s_sat = 0;
+        // the row is already satisfied by other chunks: nothing to learn here
+        s_skip = *(volatile const uint32_t*)(a.heavy_sat + slot) == need;
+      }
+    }
     __syncthreads();
+    if (s_skip) continue;
+    const uint32_t lo = s_lo, hi = s_hi;
     uint32_t sat = 0, matched = 0;
-    for (uint32_t k = b + threadIdx.x; k < e; k += blockDim.x) {
-      uint32_t l = __ldg(a.f[d].pred + k);
-      if (l >= a.minl[d] && l <= a.maxl[d]) sat |= match_entry(a, d, l, __ldg(a.f[d].col + k), row, 0u, matched);
+    for (uint32_t k0 = lo; k0 < hi; k0 += 4 * blockDim.x) {
+      uint32_t l4[4], c4[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const uint32_t k = k0 + t * blockDim.x + threadIdx.x;
+        l4[t] = k < hi ? (uint32_t)__ldg(a.f[d].pred + k) : 0u;
+        c4[t] = k < hi ? __ldg(a.f[d].col + k) : 0u;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        if (l4[t]) sat |= match_entry(a, d, l4[t], c4[t], row, sat, matched);
+      // every 4 steps: stop when the CTA has satisfied every edge of the row
+      if (((k0 - lo) / (4 * blockDim.x)) % 4 == 3) {
+        if (sat) atomicOr(&s_sat, sat);
+        __syncthreads();
+        const bool all = s_sat == need;
+        __syncthreads();
+        if (all) break;
+      }
     }
     sat = __reduce_or_sync(GSM_FULL, sat);
     if ((threadIdx.x & 31) == 0 && sat) atomicOr(&s_sat, sat);
     __syncthreads();
     if (threadIdx.x == 0) {
       if (s_sat) atomicOr(a.heavy_sat + slot, s_sat);
-      atomicAdd(a.ctr + C_HEAVY, (unsigned long long)(e - b));
-      atomicAdd(a.ctr + C_FILTER_SCANNED, (unsigned long long)(e - b));
+      atomicAdd(a.ctr + C_HEAVY, (unsigned long long)(hi - lo));
+      atomicAdd(a.ctr + C_FILTER_SCANNED, (unsigned long long)(hi - lo));
     }
-    __syncthreads();
   }
 }
 

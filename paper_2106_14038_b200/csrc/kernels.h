@@ -285,7 +285,17 @@ struct ExpArgs2 {
   int* overflow;                           // |= 1 capacity (retry), |= 2 fatal (> 2^32 entries)
   unsigned long long* ctr;
   LBArgs lb;
+  // materialised ancestor bindings (no parent-pointer walks): a node of level
+  // k-1 carries the bindings of the older levels deeper levels still need, in
+  // columns par_anc[i]; ANC_BIND = the parent's own binding, ANC_WALK = walk
+  int par_idx;                             // the tree edge's parent-level binding
+  int cl_idx[MAXC];                        // each closing edge's other-level binding
+  const uint32_t* par_anc[MAXANC];
+  uint32_t n_anc_out;                      // columns level k carries for its children
+  int anc_src[MAXANC];                     // column i of level k: ANC_BIND or an index into par_anc
+  uint32_t* out_anc[MAXANC];
 };
+constexpr int ANC_BIND = -1, ANC_WALK = -2;
 // ids of set bits of bm[0, n_words) plus id_base
 // kernels one launch_bitmap_compact_lb issues (none for an empty range)
 inline int compact_launches(uint32_t n_words) { return n_words ? 1 : 0; }

@@ -126,11 +126,23 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
     }
     ctx->own_stream = true;
   }
-  // keep freed blocks in the pool (the stream-ordered allocator as a caching allocator)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+  // The context's own stream-ordered pool, kept warm (freed blocks stay cached).
+  // Own pool, and no reuse that inserts waits on another stream's frees: ranks
+  // that share a device (threads of one process) must never have an allocation
+  // on one rank's stream wait on a free queued behind another rank's barrier.
+  {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = cfg->device;
+    if (cudaMemPoolCreate(&ctx->pool, &pp) != cudaSuccess) {
+      g_static_err = "cudaMemPoolCreate failed";
+      return GSMART_E_CUDA;
+    }
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    int no = 0;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   if (cudaMalloc(&ctx->d_ctr, 64 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pin, 64 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -185,6 +197,12 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   return GSMART_OK;
 }
 
+gsmart_status gsm::ctx_sync(gsmart_ctx* ctx) {
+  CU(cudaStreamSynchronize(ctx->st));
+  for (auto& sp : ctx->slots) CU(cudaStreamSynchronize(sp->st));
+  return GSMART_OK;
+}
+
 static void free_lspm(gsmart_ctx* ctx) {
   for (auto& f : ctx->f) {
     if (f.sym) {
@@ -231,6 +249,8 @@ extern "C" void gsmart_destroy(gsmart_ctx* ctx) {
   ctx->workers.reset();
   cudaFree(ctx->d_ctr);
   cudaFreeHost(ctx->h_pin);
+  cudaStreamSynchronize(ctx->st);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->own_stream) cudaStreamDestroy(ctx->st);
   delete ctx;
 }
@@ -740,7 +760,8 @@ extern "C" gsmart_status gsmart_copy_to_host(gsmart_ctx* ctx, void* dst, const v
   if (ctx->poisoned) return GSMART_E_CUDA;
   if (!bytes) return GSMART_OK;
   CU(cudaSetDevice(ctx->cfg.device));
-  CU(cudaDeviceSynchronize());  // results may be ordered on any slot stream
-  CU(cudaMemcpy(dst, src_dev, bytes, cudaMemcpyDeviceToHost));
+  TRY(ctx_sync(ctx));  // results may be ordered on any slot stream (never a device-wide sync: ranks may share it)
+  CU(cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
   return GSMART_OK;
 }

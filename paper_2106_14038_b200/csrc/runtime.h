@@ -112,6 +112,7 @@ struct Slot {
     uint64_t cap = 0;
     uint32_t *bind = nullptr, *parent = nullptr, *seg_beg = nullptr, *off = nullptr, *newidx = nullptr;
     uint8_t* alive = nullptr;
+    uint32_t* anc[MAXANC] = {};  // materialised ancestor bindings (allocated on first use)
   };
   LvBuf lv[GSMART_MAX_LEVELS];
   uint32_t* list[GSMART_MAX_LEVELS] = {};
@@ -230,6 +231,7 @@ struct gsmart_comm {
 struct gsmart_ctx {
   gsmart_config cfg{};
   cudaStream_t st = nullptr;
+  cudaMemPool_t pool = nullptr;  // the context's device memory pool (dalloc)
   bool own_stream = false;
   bool poisoned = false;
   std::string err;
@@ -323,8 +325,8 @@ gsmart_status dalloc(gsmart_ctx* ctx, T** p, uint64_t count, cudaStream_t st) {
     }
     return GSMART_OK;
   }
-  cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocAsync", __LINE__);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)p, bytes, ctx->pool, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocFromPoolAsync", __LINE__);
   return GSMART_OK;
 }
 template <typename T>
@@ -361,6 +363,8 @@ gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_p
                        int n, unsigned long long* host);
 
 void slots_free(gsmart_ctx* ctx);
+// wait for every stream of this context (ranks sharing a device never wait on each other's streams)
+gsmart_status ctx_sync(gsmart_ctx* ctx);
 
 // symheap.cu: host all-gather / barrier over the ranks (in-process comm or
 // sockets), symmetric regions, device barrier across ranks

@@ -325,12 +325,11 @@ gsmart_status sym_alloc(gsmart_ctx* ctx, uint64_t my_off, uint64_t my_bytes, Sym
 void sym_free(gsmart_ctx* ctx, SymRegion* R) {
   const VmmApi* api = vmm();
   if (!api || !R->va) return;
-  cudaDeviceSynchronize();
+  ctx_sync(ctx);  // this rank's work on the region is done (peers keep their own mappings)
   for (size_t q = 0; q < R->off.size(); q++) api->MemUnmap(R->va + R->off[q], R->bytes[q]);
   api->MemAddressFree(R->va, R->total);
   for (size_t q = 0; q < R->handles.size(); q++)
     if (!R->own_only || (int)q == R->rank) api->MemRelease(R->handles[q]);
-  (void)ctx;
   *R = SymRegion();
 }
 
@@ -354,9 +353,18 @@ __global__ void k_rank_barrier(unsigned long long* flags_local, SymDelta d, uint
     unsigned long long* dst = flags_local + d.words[q] / 2 + rank;  // rank q's flag array, my slot
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(gen) : "memory");
     unsigned long long v = 0;
+    const long long t0 = clock64();
     do {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags_local + q) : "memory");
-      if (v < gen) __nanosleep(64);
+      if (v < gen) {
+        __nanosleep(256);
+        // a peer that never arrives is a bug (mismatched collective sequence): fail
+        // loudly (~30 s at 2 GHz) instead of hanging the device
+        if (clock64() - t0 > 60000000000ll) {
+          printf("gsmart: rank %u barrier gen %llu timed out waiting for rank %u (flag %llu)\n", rank, gen, q, v);
+          __trap();
+        }
+      }
     } while (v < gen);
   }
   __syncthreads();
