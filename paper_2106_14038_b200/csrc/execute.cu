@@ -312,7 +312,23 @@ struct Exec {
   uint32_t* chg_words() {
     return peer_mode() ? sl.cand + sl.sym_cand_words : reinterpret_cast<uint32_t*>(sl.d_ctr + 16);
   }
+  // Ranks that are threads of one process share one CUDA context, and streams of
+  // one context share a few hardware queues (CUDA_DEVICE_MAX_CONNECTIONS): a
+  // spinning barrier kernel at the head of a queue would block another rank's
+  // kernels queued behind it.  Those ranks synchronise on the host instead (and
+  // run without graphs); ranks that are processes (one context each, the
+  // deployment layout) use the device barrier.
+  bool host_barriers() const { return ctx->world > 1 && ctx->lcomm != nullptr; }
   gsmart_status rank_barrier() {
+    if (host_barriers()) {
+      prof.begin(K_COLLECTIVE);
+      CU(cudaStreamSynchronize(sl.st));
+      TRY(host_barrier(ctx));
+      prof.end();
+      ++sl.bar_off;
+      launches[K_COLLECTIVE]++;
+      return GSMART_OK;
+    }
     unsigned long long* flags = reinterpret_cast<unsigned long long*>(sl.cand + sl.sym_cand_words + 32);
     prof.begin(K_COLLECTIVE);
     CU(launch_rank_barrier(flags, peer_delta(), (uint32_t)ctx->rank, (uint32_t)ctx->world, sl.d_bar, ++sl.bar_off,
@@ -785,8 +801,8 @@ struct Exec {
   // valid only if the body starts at the same offset as when it was captured.
   template <typename Body>
   gsmart_status run_cached(uint64_t key, uint32_t key_flags, Body&& body) {
-    const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && (ctx->world == 1 || peer_mode()) &&
-                           !ctx->comm;
+    const bool graphable = !(flags & (GSMART_PROFILE | GSMART_NO_GRAPH)) && !ctx->comm &&
+                           (ctx->world == 1 || (peer_mode() && !host_barriers()));
     if (!graphable) return body();
     auto it = sl.graphs.find(key);
     if (it != sl.graphs.end() && it->second.ws_gen == sl.ws_gen && it->second.lspm_gen == ctx->lspm_gen &&
@@ -1193,6 +1209,11 @@ struct Exec {
 
   gsmart_status finalize() {
     prof.flush();
+    static const bool trace = getenv("GSMART_TRACE") != nullptr;
+    if (trace && ctx->world > 1)
+      fprintf(stderr, "[gsmart] rank %d plan %llu: barrier gens %llu..%llu, lb epochs %u..%u\n", ctx->rank,
+              (unsigned long long)plan->uid, (unsigned long long)sl.bar_base + 1,
+              (unsigned long long)(sl.bar_base + sl.bar_off), sl.seq_base, sl.seq_base + sl.seq_off);
     if (seq_open) {
       end_seq(sl);
       seq_open = false;

@@ -361,7 +361,8 @@ __global__ void k_rank_barrier(unsigned long long* flags_local, SymDelta d, uint
         // a peer that never arrives is a bug (mismatched collective sequence): fail
         // loudly (~30 s at 2 GHz) instead of hanging the device
         if (clock64() - t0 > 60000000000ll) {
-          printf("gsmart: rank %u barrier gen %llu timed out waiting for rank %u (flag %llu)\n", rank, gen, q, v);
+          printf("gsmart: rank %u barrier gen %llu (base %llu + %u) timed out waiting for rank %u (flag %llu)\n", rank,
+                 gen, *(volatile const unsigned long long*)gen_base, gen_off, q, v);
           __trap();
         }
       }
