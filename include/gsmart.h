@@ -197,7 +197,10 @@ typedef struct {
   uint32_t n_edges; const gsmart_qedge* e;
 } gsmart_query;
 
-/* Plan (host only, microseconds; ctx may be NULL).  Degree-driven traversal
+/* Plan (host only, microseconds; ctx may be NULL; with a ctx whose LSpM is
+ * built and n_predicates < 4096, a group's new neighbours enter the trie in
+ * ascending expected fan-out — entries per row of the label — so functional
+ * patterns precede the fan-out ones; results are identical).  Degree-driven traversal
  * (§6.1.2): constant-incident patterns become seeds (light
  * queries); roots by max unevaluated edges, then max
  * unevaluated out-edges, then lowest index; groups = all unevaluated incident

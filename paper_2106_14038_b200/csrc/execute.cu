@@ -1135,7 +1135,7 @@ struct Exec {
       void* tmp = sl.p2 + al(n_rows * nc * 4);
       prof.begin(K_SORT_ROWS);
       CU(sort_rows(ot.rows, R->d_rows, n_rows, nc, n_key, bits_for(ctx->N - 1), tmp, tb, sl.st,
-                   &launches[K_SORT_ROWS]));
+                   &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50)));
       prof.end();
     }
     return GSMART_OK;

@@ -2,6 +2,7 @@
 // (Product code; nothing here is shared with oracle/.)
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -62,6 +63,9 @@ struct gsmart_plan_s {
 };
 
 namespace gsm {
-gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* out, std::string* err);
+// fanout (optional): expected children per parent of a pattern (label, dir seen
+// from the center) — orders a group's new neighbours in the trie
+gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* out, std::string* err,
+                         const std::function<double(uint32_t, uint32_t)>* fanout = nullptr);
 std::string describe_plan(const gsmart_plan_t& p);
 }  // namespace gsm

@@ -345,20 +345,32 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // One thread per row.  Entries are sorted by label, so a row's label set is
 // walked label by label: short rows linearly, long rows by jumping to the
 // first entry past the current label (binary search) — O(#labels · log len)
-// even for hub rows.
+// even for hub rows.  Optionally counts, per label, the rows holding it
+// (label_rows: a per-CTA shared histogram flushed once; labels < LR_MAX).
+constexpr uint32_t LR_MAX = 4096;
+
 template <typename PT>
 __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restrict__ pred, uint32_t n_rows,
-                             uint32_t* __restrict__ lmask) {
+                             uint32_t* __restrict__ lmask, unsigned long long* __restrict__ label_rows,
+                             uint32_t n_labels) {
+  extern __shared__ uint32_t s_lr[];
+  const bool count = label_rows != nullptr;
+  if (count) {  // [0, n_labels): rows holding the label, [n_labels, 2 n_labels): its entries
+    for (uint32_t i = threadIdx.x; i < 2 * n_labels; i += blockDim.x) s_lr[i] = 0;
+    __syncthreads();
+  }
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
     uint32_t k = rp[r];
     const uint32_t e = rp[r + 1];
     uint32_t m = 0;
-    if (e - k <= 16) {
-      for (; k < e; k++) m |= label_bit(pred[k]);
-    } else {
-      while (k < e) {
-        const uint32_t l = pred[k];
-        m |= label_bit(l);
+    while (k < e) {
+      const uint32_t l = pred[k];
+      const uint32_t k0 = k;
+      m |= label_bit(l);
+      if (e - k <= 16) {  // short remainder: step linearly past this label
+        k++;
+        while (k < e && (uint32_t)pred[k] == l) k++;
+      } else {
         uint32_t lo = k + 1, hi = e;  // first entry with label > l
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
@@ -367,16 +379,29 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
         }
         k = lo;
       }
+      if (count && l < n_labels) {
+        atomicAdd(&s_lr[l], 1u);
+        atomicAdd(&s_lr[n_labels + l], k - k0);
+      }
     }
     lmask[r] = m;
+  }
+  if (count) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2 * n_labels; i += blockDim.x)
+      if (s_lr[i]) atomicAdd(label_rows + i, (unsigned long long)s_lr[i]);
   }
 }
 
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
-                              uint32_t* lmask, cudaStream_t st) {
+                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st) {
   const unsigned g = grid_for(n_rows, 256, 148 * 16);
-  if (pred_bytes == 1) k_label_mask<uint8_t><<<g, 256, 0, st>>>(rp, (const uint8_t*)pred, n_rows, lmask);
-  else k_label_mask<uint16_t><<<g, 256, 0, st>>>(rp, (const uint16_t*)pred, n_rows, lmask);
+  if (n_labels > LR_MAX) label_rows = nullptr;
+  const size_t sm = label_rows ? (size_t)n_labels * 8 : 0;
+  if (pred_bytes == 1)
+    k_label_mask<uint8_t><<<g, 256, sm, st>>>(rp, (const uint8_t*)pred, n_rows, lmask, label_rows, n_labels);
+  else
+    k_label_mask<uint16_t><<<g, 256, sm, st>>>(rp, (const uint16_t*)pred, n_rows, lmask, label_rows, n_labels);
   return cudaGetLastError();
 }
 
@@ -1299,8 +1324,30 @@ cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t
   return cudaGetLastError();
 }
 
-__global__ void k_iota(uint32_t* v, uint64_t n) {
+// Are the rows already lexicographically sorted?  (A trie order that puts
+// functional patterns first yields sorted rows whenever those columns are
+// determined by the earlier ones.)  *sorted starts at 1; any descent clears it
+// and the sort runs; otherwise every sort kernel exits at entry and the rows
+// are copied.
+__global__ void k_rows_sorted(const uint32_t* __restrict__ rows, uint64_t n, uint32_t n_cols, int* sorted) {
   GSM_PDL_ENTRY();
+  bool bad = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* a = rows + i * n_cols;
+    for (uint32_t c = 0; c < n_cols; c++) {
+      const uint32_t x = a[c], y = a[n_cols + c];
+      if (x != y) {
+        bad = bad || x > y;
+        break;
+      }
+    }
+  }
+  if (__any_sync(GSM_FULL, bad) && (threadIdx.x & 31) == 0) *sorted = 0;
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n, const int* skip) {
+  GSM_PDL_ENTRY();
+  if (skip && *skip) return;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     v[i] = (uint32_t)i;
 }
@@ -1308,8 +1355,9 @@ __global__ void k_iota(uint32_t* v, uint64_t n) {
 // key of up to 64 bits: columns [c0, c1) concatenated, most significant first
 __global__ void k_gather_key(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
                              uint32_t n_cols, uint32_t c0, uint32_t c1, int key_bits,
-                             unsigned long long* __restrict__ keys) {
+                             unsigned long long* __restrict__ keys, const int* skip) {
   GSM_PDL_ENTRY();
+  if (skip && *skip) return;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t* r = rows + (uint64_t)perm[i] * n_cols;
     unsigned long long k = 0;
@@ -1319,8 +1367,18 @@ __global__ void k_gather_key(const uint32_t* __restrict__ rows, const uint32_t* 
 }
 
 __global__ void k_gather_rows(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
-                              uint32_t n_cols, uint32_t* __restrict__ out) {
+                              uint32_t n_cols, uint32_t* __restrict__ out, const int* skip) {
   GSM_PDL_ENTRY();
+  const bool ident = skip && *skip;  // already sorted: a straight copy
+  if (ident) {
+    const uint64_t m = n * n_cols;
+    const uint64_t m4 = (reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(out)) & 15 ? 0 : m / 4;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m4; i += (uint64_t)gridDim.x * blockDim.x)
+      reinterpret_cast<uint4*>(out)[i] = __ldcs(reinterpret_cast<const uint4*>(rows) + i);
+    for (uint64_t i = 4 * m4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+      out[i] = rows[i];
+    return;
+  }
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * n_cols;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t r = i / n_cols, c = i - r * n_cols;
@@ -1405,7 +1463,7 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
 // the trie order).  LSD over <= 64-bit keys of packed columns (hand-written radix
 // sort, radix.cu, permutation as payload), least significant chunk first; stable.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
-                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches) {
+                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches, int* sorted_flag) {
   const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
   uint32_t* perm = (uint32_t*)tmp;
   uint32_t* perm2 = (uint32_t*)((char*)tmp + s4);
@@ -1414,20 +1472,29 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
   void* rtmp = (char*)tmp + 2 * s4 + 2 * s8;
   const size_t rbytes = tmp_bytes - 2 * s4 - 2 * s8;
   unsigned g = grid_for(n, 256, 148 * 32);
-  pdl_launch(k_iota, g, 256, st, perm, n);
   int nl = 1;
+  if (sorted_flag) {  // rows often arrive sorted (functional patterns first in the trie): check once
+    cudaError_t e = cudaMemsetAsync(sorted_flag, 0, 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sorted_flag, 1, 1, st);  // little-endian int 1
+    if (e != cudaSuccess) return e;
+    pdl_launch(k_rows_sorted, g, 256, st, rows, n, n_cols, sorted_flag);
+    nl++;
+  }
+  pdl_launch(k_iota, g, 256, st, perm, n, (const int*)sorted_flag);
   const int per = sort_chunk_cols(key_bits);
   for (int c1 = (int)std::min(n_key, n_cols); c1 > 0; c1 -= per) {
     const int c0 = std::max(0, c1 - per);
-    pdl_launch(k_gather_key, g, 256, st, rows, perm, n, n_cols, (uint32_t)c0, (uint32_t)c1, key_bits, keys);
+    pdl_launch(k_gather_key, g, 256, st, rows, perm, n, n_cols, (uint32_t)c0, (uint32_t)c1, key_bits, keys,
+               (const int*)sorted_flag);
     int second = 0;
     cudaError_t e = radix_sort_pairs_u64_u32((uint64_t*)keys, (uint64_t*)keys2, perm, perm2, n, 0,
-                                             (c1 - c0) * key_bits, rtmp, rbytes, st, &second, &nl, false);
+                                             (c1 - c0) * key_bits, rtmp, rbytes, st, &second, &nl, false, sorted_flag);
     if (e != cudaSuccess) return e;
     if (second) std::swap(perm, perm2);
     nl += 1;
   }
-  pdl_launch(k_gather_rows, grid_for(n * n_cols, 256, 148 * 32), 256, st, rows, perm, n, n_cols, rows_out);
+  pdl_launch(k_gather_rows, grid_for(n * n_cols, 256, 148 * 32), 256, st, rows, perm, n, n_cols, rows_out,
+             (const int*)sorted_flag);
   if (launches) *launches += nl + 1;
   return cudaGetLastError();
 }

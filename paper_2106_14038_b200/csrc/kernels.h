@@ -53,7 +53,7 @@ cudaError_t radix_sort_keys_u64(uint64_t* k0, uint64_t* k1, uint64_t n, int b0, 
                                 cudaStream_t st, int* in_second, int* launches, bool skip_trivial);
 cudaError_t radix_sort_pairs_u64_u32(uint64_t* k0, uint64_t* k1, uint32_t* v0, uint32_t* v1, uint64_t n, int b0,
                                      int b1, void* tmp, size_t tmp_bytes, cudaStream_t st, int* in_second,
-                                     int* launches, bool skip_trivial);
+                                     int* launches, bool skip_trivial, const int* skip = nullptr);
 cudaError_t radix_sort_pairs_u32_u64(uint32_t* k0, uint32_t* k1, uint64_t* v0, uint64_t* v1, uint64_t n, int b0,
                                      int b1, void* tmp, size_t tmp_bytes, cudaStream_t st, int* in_second,
                                      int* launches, bool skip_trivial);
@@ -84,8 +84,10 @@ cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
                               uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st);
 // per-row label signature (Fmt::lmask) from row_ptr + pred
+// label_rows (optional, n_labels <= 4096; 2 n_labels words): [l] += rows holding
+// label l, [n_labels + l] += its entries (fan-out statistics for the trie order)
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
-                              uint32_t* lmask, cudaStream_t st);
+                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st);
 
 // ----------------------------------------------------------------- bitmaps
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st);
@@ -344,7 +346,10 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols);
 // (packed-key LSD radix passes).
 // The input must already be ordered on columns [n_key, n_cols) among rows that
 // agree on [0, n_key) (n_key = n_cols: no assumption).
+// sorted_flag (device int, optional): the rows are first checked for order; if
+// already sorted, every sort kernel exits at entry and the rows are copied.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
-                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches);
+                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches,
+                      int* sorted_flag = nullptr);
 
 }  // namespace gsm

@@ -11,7 +11,8 @@
 
 namespace gsm {
 
-gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* P, std::string* err) {
+gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* P, std::string* err,
+                         const std::function<double(uint32_t, uint32_t)>* fanout) {
   if (!q || (q->n_vertices && !q->v) || (q->n_edges && !q->e)) { *err = "null query arrays"; return GSMART_E_INVALID_ARG; }
   if (traversal == GSMART_DIRECTION) { *err = "direction-driven traversal not supported in this version"; return GSMART_E_UNSUPPORTED; }
   if (traversal != GSMART_DEGREE) { *err = "unknown traversal"; return GSMART_E_INVALID_ARG; }
@@ -128,7 +129,20 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
   for (auto& g : P->groups) {
     uint32_t v = g.center;
     if (pos[v] < 0) add_level(v, -1, 0, 0, 0);   // a root
-    for (auto& ge : g.edges) {
+    // With LSpM statistics (gsmart_plan given a built ctx) a group's new
+    // neighbours enter the trie in ascending expected fan-out (entries per row
+    // of the label, from the center's side): functional patterns (one child
+    // per parent) come before the fan-out ones, so the big levels are built
+    // once, at the end, instead of being copied level after level.  The result
+    // is the same for every order (the rows are sorted at the end).
+    std::vector<const GroupEdge*> order;
+    for (auto& ge : g.edges) order.push_back(&ge);
+    if (fanout)
+      std::stable_sort(order.begin(), order.end(), [&](const GroupEdge* a, const GroupEdge* b) {
+        return (*fanout)(a->label, a->dir) < (*fanout)(b->label, b->dir);
+      });
+    for (const GroupEdge* gp : order) {
+      const GroupEdge& ge = *gp;
       uint32_t w = ge.nbr;
       if (w == v) {
         P->levels[pos[v]].closing.push_back({ge.edge, ge.label, (uint32_t)pos[v], OUT});

@@ -36,8 +36,9 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
 // digit counts of every pass; hist[p * 256 + d] (64-bit)
 template <typename K>
 __global__ void __launch_bounds__(256) k_rs_hist(const K* __restrict__ keys, uint64_t n, int b0, int npass,
-                                                 unsigned long long* __restrict__ hist) {
+                                                 unsigned long long* __restrict__ hist, const int* skip) {
   __shared__ uint32_t sh[RS_MAX_PASSES][256];
+  if (skip && *skip) return;
   for (int i = threadIdx.x; i < RS_MAX_PASSES * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -67,7 +68,8 @@ __global__ void __launch_bounds__(RS_T) k_rs_pass(const K* __restrict__ kin, K* 
                                                   const V* __restrict__ vin, V* __restrict__ vout, uint64_t n,
                                                   int shift, const unsigned long long* __restrict__ dbase,
                                                   unsigned long long* __restrict__ status, uint32_t* counter,
-                                                  uint32_t epoch) {
+                                                  uint32_t epoch, const int* skip) {
+  if (skip && *skip) return;  // the caller found the data already in order
   __shared__ uint32_t s_wh[RS_W][256];     // per-warp digit counts -> exclusive warp offsets
   __shared__ uint32_t s_local[256];        // tile-local start of each digit
   __shared__ unsigned long long s_glob[256];  // global start of each digit for this tile
@@ -178,7 +180,8 @@ size_t radix_tmp_bytes(uint64_t n) {
 
 template <typename K, typename V, bool HAS_V>
 static cudaError_t radix_sort_t(K* k0, K* k1, V* v0, V* v1, uint64_t n, int b0, int b1, void* tmp, size_t tmp_bytes,
-                                cudaStream_t st, int* in_second, int* launches, bool skip_trivial) {
+                                cudaStream_t st, int* in_second, int* launches, bool skip_trivial,
+                                const int* skip = nullptr) {
   *in_second = 0;
   if (n <= 1 || b1 <= b0) return cudaSuccess;
   const size_t dyn = sizeof(K) * RS_TILE + (HAS_V ? sizeof(V) * RS_TILE : 0);
@@ -209,7 +212,7 @@ static cudaError_t radix_sort_t(K* k0, K* k1, V* v0, V* v1, uint64_t n, int b0, 
     if (e != cudaSuccess) return e;
     const K* src = cur ? k1 : k0;
     const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
-    k_rs_hist<K><<<g, 256, 0, st>>>(src, n, gb, np, hist);
+    k_rs_hist<K><<<g, 256, 0, st>>>(src, n, gb, np, hist, skip);
     k_rs_scan<<<np, 256, 0, st>>>(hist, base);
     nl += 2;
     std::vector<unsigned long long> h(np * 256, 0);
@@ -227,7 +230,7 @@ static cudaError_t radix_sort_t(K* k0, K* k1, V* v0, V* v1, uint64_t n, int b0, 
       const V* vi = cur ? v1 : v0;
       V* vo = cur ? v0 : v1;
       k_rs_pass<K, V, HAS_V><<<(unsigned)tiles, RS_T, dyn, st>>>(ki, ko, vi, vo, n, gb + 8 * p, base + p * 256, status,
-                                                               counters + p, (uint32_t)(p + 1));
+                                                               counters + p, (uint32_t)(p + 1), skip);
       nl++;
       cur ^= 1;
     }
@@ -245,9 +248,9 @@ cudaError_t radix_sort_keys_u64(uint64_t* k0, uint64_t* k1, uint64_t n, int b0, 
 
 cudaError_t radix_sort_pairs_u64_u32(uint64_t* k0, uint64_t* k1, uint32_t* v0, uint32_t* v1, uint64_t n, int b0,
                                      int b1, void* tmp, size_t tmp_bytes, cudaStream_t st, int* in_second,
-                                     int* launches, bool skip_trivial) {
+                                     int* launches, bool skip_trivial, const int* skip) {
   return radix_sort_t<uint64_t, uint32_t, true>(k0, k1, v0, v1, n, b0, b1, tmp, tmp_bytes, st, in_second, launches,
-                                                skip_trivial);
+                                                skip_trivial, skip);
 }
 
 cudaError_t radix_sort_pairs_u32_u64(uint32_t* k0, uint32_t* k1, uint64_t* v0, uint64_t* v1, uint64_t n, int b0,

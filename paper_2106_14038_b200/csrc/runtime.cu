@@ -424,6 +424,25 @@ static uint64_t row_chunk_off(gsmart_ctx* ctx, uint32_t lo, uint32_t hi, uint64_
   return (end + g - 1) / g * g + (uint64_t)ctx->rank * g;
 }
 
+// rows per label (summed over the ranks when world > 1); none when P > 8192
+static gsmart_status label_rows_readback(gsmart_ctx* ctx, const unsigned long long* d, std::vector<unsigned long long>* out) {
+  out->clear();
+  if (ctx->P + 1 > 4096) return GSMART_OK;
+  std::vector<unsigned long long> h(2 * ((size_t)ctx->P + 1));
+  CU(cudaMemcpyAsync(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  if (ctx->world > 1) {
+    std::vector<unsigned long long> all(h.size() * ctx->world);
+    TRY(host_allgather(ctx, h.data(), h.size() * 8, all.data()));
+    for (size_t i = 0; i < h.size(); i++) {
+      h[i] = 0;
+      for (int q = 0; q < ctx->world; q++) h[i] += all[(size_t)q * h.size() + i];
+    }
+  }
+  *out = h;
+  return GSMART_OK;
+}
+
 static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
   Lspm& L = ctx->f[fmt];
   const uint64_t n = ctx->n_triples;
@@ -478,7 +497,11 @@ static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* 
   L.col = (uint32_t*)L.s_col.va;
   L.pred = (void*)L.s_pred.va;
   L.lmask = (uint32_t*)L.s_lmask.va;
-  if (nloc) CU(launch_label_mask(L.rp + rlo, L.pred, pbytes, nloc, L.lmask + rlo, ctx->st));
+  unsigned long long* lrows = nullptr;
+  TRY(sc.get(&lrows, 2 * ((uint64_t)ctx->P + 1)));
+  CU(cudaMemsetAsync(lrows, 0, ((size_t)ctx->P + 1) * 16, ctx->st));
+  if (nloc) CU(launch_label_mask(L.rp + rlo, L.pred, pbytes, nloc, L.lmask + rlo, lrows, ctx->P + 1, ctx->st));
+  TRY(label_rows_readback(ctx, lrows, &L.label_rows));
   CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
   if (nloc) CU(launch_heavy_stats(L.rp + rlo, nloc, ctx->d_ctr + 42, ctx->st));
   unsigned long long hv[2];
@@ -521,7 +544,11 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
     CU(scan_exclusive_u32(L.rp, L.rp, (uint64_t)N + 1, tot, stmp, ctx->st, nullptr));
   }
   TRY(dalloc(ctx, &L.lmask, (uint64_t)N + 1));
-  CU(launch_label_mask(L.rp, L.pred, ctx->pred_bytes, N, L.lmask, ctx->st));
+  unsigned long long* lrows = nullptr;
+  TRY(sc.get(&lrows, 2 * ((uint64_t)ctx->P + 1)));
+  CU(cudaMemsetAsync(lrows, 0, ((size_t)ctx->P + 1) * 16, ctx->st));
+  CU(launch_label_mask(L.rp, L.pred, ctx->pred_bytes, N, L.lmask, lrows, ctx->P + 1, ctx->st));
+  TRY(label_rows_readback(ctx, lrows, &L.label_rows));
   CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
   CU(launch_heavy_stats(L.rp, N, ctx->d_ctr + 42, ctx->st));
   unsigned long long hv[2];
@@ -631,7 +658,19 @@ extern "C" gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uin
   auto p = std::make_unique<gsmart_plan_t>();
   p->uid = next_uid++;
   std::string err;
-  gsmart_status s = build_plan(q, traversal, p.get(), &err);
+  // trie order by expected fan-out when the ctx has a built LSpM with label statistics
+  std::function<double(uint32_t, uint32_t)> fan;
+  const bool stats = ctx && ctx->f[0].built && ctx->f[1].built &&
+                     ctx->f[0].label_rows.size() == 2 * ((size_t)ctx->P + 1) &&
+                     ctx->f[1].label_rows.size() == 2 * ((size_t)ctx->P + 1);
+  if (stats)
+    fan = [ctx](uint32_t label, uint32_t dir) {
+      const auto& lr = ctx->f[dir == OUT ? 0 : 1].label_rows;
+      if (label > ctx->P) return 0.0;
+      const double rows = (double)lr[label], ent = (double)lr[ctx->P + 1 + label];
+      return rows > 0 ? ent / rows : 0.0;
+    };
+  gsmart_status s = build_plan(q, traversal, p.get(), &err, stats ? &fan : nullptr);
   if (s != GSMART_OK) {
     if (ctx) ctx->err = err; else g_static_err = err;
     return s;

@@ -56,6 +56,9 @@ struct Lspm {
   // every rank's rows); this rank stores rows [row_lo, row_hi) only
   bool sym = false;
   SymRegion s_rp, s_col, s_pred, s_lmask;
+  // [l]: rows holding label l, [P + 1 + l]: its entries (empty when P > 4095);
+  // entries / rows = the expected fan-out of a pattern from this side
+  std::vector<unsigned long long> label_rows;
 };
 
 // Label-major entry lists: the kept, de-duplicated triples grouped by predicate,
