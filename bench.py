@@ -329,6 +329,7 @@ def main():
     step(stats=batch_stats)
     launches_per_step = sum(sum(st["launches"].values()) for st in batch_stats)
     edges_read = sum(st["edges_evaluated"] for st in batch_stats)
+    xchg_bytes = sum(st["allgather_bytes"] for st in batch_stats)  # bitmap words this rank received per step
 
     # ---- profiled pass: the same queries one at a time (GSMART_PROFILE: per-kernel-class
     # CUDA events on the launching stream; sequential so no other stream shares the GPU)
@@ -463,6 +464,13 @@ def main():
                            "definition": "SURVEY §8(d): LSpM entries read whose label matched (seed + filter + "
                                          "push + expansion device counters)"},
             "batch_latency_ms": ms,
+            # SURVEY §8(d) NVLink term: per group, every rank receives the other ranks'
+            # bitmap slices ((P-1)/P * N/8 bytes); against the measured 770 GB/s peer
+            # copy per direction (B200_PROFILING.md).  0 at N = 1.
+            "nvlink": {"bytes_per_step_per_rank": int(xchg_bytes),
+                       "achieved_GBps": xchg_bytes / (ms / 1000) / 1e9, "peak_GBps": 770.0,
+                       "frac": xchg_bytes / (ms / 1000) / 1e9 / 770.0,
+                       "peak_source": "B200_PROFILING.md measured peer copy per direction"},
             "build": {"ms": build_ms, "triples_per_s": len(s_h) / (build_ms / 1000)},
             "kernel_classes": per_class,
             "queries": per_query}

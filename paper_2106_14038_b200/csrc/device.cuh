@@ -122,6 +122,31 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     asm volatile("griddepcontrol.launch_dependents;" :::);     \
   } while (0)
 
+// ---- 1-D TMA bulk copies (cp.async.bulk, completion on a shared-memory
+// mbarrier): global -> shared staging of contiguous tiles without register
+// round trips.  src, dst and bytes must be 16-byte aligned / multiples.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
+  // generic-proxy accesses of dst before this point are ordered before the async write
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(m)),
+      "r"(phase)
+      : "memory");
+}
+
 // Block-wide exclusive scan of one value per thread (blockDim.x <= 1024, multiple of 32).
 template <typename T>
 __device__ __forceinline__ T block_exclusive_scan(T v, T* smem /* >= 32 */, T* total) {

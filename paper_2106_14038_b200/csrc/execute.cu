@@ -168,7 +168,7 @@ static gsmart_status slot_level(gsmart_ctx* ctx, Slot& s, uint32_t k, uint64_t n
   TRY(dalloc(ctx, &b.bind, cap, s.st));
   TRY(dalloc(ctx, &b.parent, cap, s.st));
   TRY(dalloc(ctx, &b.seg_beg, cap, s.st));
-  TRY(dalloc(ctx, &b.off, cap + 1, s.st));
+  TRY(dalloc(ctx, &b.off, cap + 8, s.st));  // + 8: 16-byte TMA spans may round past the end
   TRY(dalloc(ctx, &b.newidx, cap, s.st));
   TRY(dalloc(ctx, &b.alive, cap, s.st));
   b.cap = cap;
@@ -639,6 +639,7 @@ struct Exec {
         d.self = c.other_level == k ? 1u : 0u;
       }
       a.par_idx = a.tree ? anc_index(k, Lv.parent_level) : ANC_WALK;
+      a.use_tma = ctx->use_tma ? 1 : 0;
       for (size_t i = 0; i < anc_cols[k - 1].size(); i++) a.par_anc[i] = sl.lv[k - 1].anc[i];
       a.n_anc_out = (uint32_t)anc_cols[k].size();
       for (uint32_t i = 0; i < a.n_anc_out; i++) {
@@ -774,6 +775,24 @@ struct Exec {
     }
     if (ctx->filter_variant & 4) TRY(slot_buf(ctx, sl, &sl.frows, &sl.frows_cap, (uint64_t)W * 32));
     if (ctx->lm.built) TRY(slot_buf(ctx, sl, &sl.sat, &sl.sat_cap, 2ull * Wpad));
+    if (ctx->l2_persist) {  // A/B: keep the candidate bitmaps (random probes) resident in a persisting L2 window
+      static bool limit_set = false;
+      int dev = ctx->cfg.device, max_persist = 0, max_window = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      if (!limit_set && max_persist > 0) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+        limit_set = true;
+      }
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = sl.cand;
+      v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)Wpad * nvar * 4, (size_t)std::max(max_window, 0));
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(sl.st, cudaStreamAttributeAccessPolicyWindow, &v);
+      cudaGetLastError();
+    }
     for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1, (uint32_t)anc_cols[k].size()));
     for (uint32_t k = 1; k < L; k++)
       if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));

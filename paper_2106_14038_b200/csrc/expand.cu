@@ -339,9 +339,13 @@ constexpr uint32_t OFFCAP = 2048, TGTP = 1024, TGTC = 4;
 template <typename PT>
 __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
   GSM_PDL_ENTRY();
-  __shared__ uint32_t s_off[OFFCAP];
+  __shared__ __align__(16) uint32_t s_offbuf[OFFCAP + 8];
+  __shared__ __align__(8) unsigned long long s_mbar;
   __shared__ uint32_t s_tgt[TGTP * TGTC];
   __shared__ uint32_t s_tile, s_nlo, s_nhi;
+  uint32_t tma_phase = 0;
+  if (a.use_tma && threadIdx.x == 0) mbar_init(&s_mbar, 1);
+  __syncthreads();
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
   const uint64_t F = *a.d_nparent;
@@ -372,15 +376,30 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
     __syncthreads();
     const uint32_t nlo = s_nlo, nr = s_nhi - s_nlo + 1;
     const bool soff = nr + 1 <= OFFCAP;
-    if (soff)
-      for (uint32_t i = threadIdx.x; i <= nr; i += EX_T) s_off[i] = __ldg(a.off + nlo + i);
+    // the tile's parent offsets off[nlo .. nlo + nr] into shared memory: one TMA
+    // bulk copy of the 16-byte-aligned span (issued by one thread, overlapping
+    // the closing-target staging below), else plain loads
+    uint32_t shift = 0;
+    if (soff && a.use_tma) {
+      const uint32_t a0 = nlo & ~3u;
+      shift = nlo - a0;
+      const uint32_t words = (shift + nr + 1 + 3) & ~3u;
+      if (threadIdx.x == 0) tma_load_1d(s_offbuf, a.off + a0, words * 4, &s_mbar);
+    } else if (soff) {
+      for (uint32_t i = threadIdx.x; i <= nr; i += EX_T) s_offbuf[i] = __ldg(a.off + nlo + i);
+    }
     const bool stgt = a.ncl > 0 && a.ncl <= TGTC && nr <= TGTP;
     if (stgt)
       for (uint32_t i = threadIdx.x; i < nr * a.ncl; i += EX_T) {
         const uint32_t p = i / a.ncl, c = i - p * a.ncl;
         s_tgt[p * TGTC + c] = a.cl[c].self ? 0u : anc_binding(a, a.cl_idx[c], nlo + p, a.cl[c].other_level);
       }
+    if (soff && a.use_tma) {
+      mbar_wait(&s_mbar, tma_phase);
+      tma_phase ^= 1u;
+    }
     __syncthreads();
+    const uint32_t* s_off = s_offbuf + shift;
     // The EX_I entries of a thread go through each stage together, so their
     // independent loads (segment begin, column, candidate probe, row bounds,
     // closing-edge search steps) are in flight at the same time.

@@ -345,8 +345,9 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // One thread per row.  Entries are sorted by label, so a row's label set is
 // walked label by label: short rows linearly, long rows by jumping to the
 // first entry past the current label (binary search) — O(#labels · log len)
-// even for hub rows.  Optionally counts, per label, the rows holding it
-// (label_rows: a per-CTA shared histogram flushed once; labels < LR_MAX).
+// even for hub rows.  Optionally samples, per label, the rows holding it and
+// their entries (every 16th row; a per-CTA shared histogram flushed once;
+// labels < LR_MAX): the fan-out statistics of the trie order.
 constexpr uint32_t LR_MAX = 4096;
 
 template <typename PT>
@@ -379,7 +380,7 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
         }
         k = lo;
       }
-      if (count && l < n_labels) {
+      if (count && (r & 15u) == 0 && l < n_labels) {  // a 1-in-16 row sample: the ratio is what matters
         atomicAdd(&s_lr[l], 1u);
         atomicAdd(&s_lr[n_labels + l], k - k0);
       }

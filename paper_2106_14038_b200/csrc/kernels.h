@@ -84,8 +84,8 @@ cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
                               uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st);
 // per-row label signature (Fmt::lmask) from row_ptr + pred
-// label_rows (optional, n_labels <= 4096; 2 n_labels words): [l] += rows holding
-// label l, [n_labels + l] += its entries (fan-out statistics for the trie order)
+// label_rows (optional, n_labels <= 4096; 2 n_labels words): over every 16th row,
+// [l] += rows holding label l, [n_labels + l] += its entries (fan-out statistics)
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
                               uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st);
 
@@ -296,6 +296,7 @@ struct ExpArgs2 {
   uint32_t n_anc_out;                      // columns level k carries for its children
   int anc_src[MAXANC];                     // column i of level k: ANC_BIND or an index into par_anc
   uint32_t* out_anc[MAXANC];
+  int use_tma;                             // stage tile offsets with cp.async.bulk (off[] has >= 8 words of tail)
 };
 constexpr int ANC_BIND = -1, ANC_WALK = -2;
 // ids of set bits of bm[0, n_words) plus id_base

@@ -308,6 +308,7 @@ def test_nccl_world1_communicator():
     for q in qs:
         rows, st = eng.query(q, with_stats=True)
         assert np.array_equal(rows, ix.query(q)), q.name
-        n_groups = len(G.gsmart_plan_describe(eng.plan(q).h)["groups"])
+        with eng.plan(q) as pl:
+            n_groups = len(G.gsmart_plan_describe(pl.h)["groups"])
         assert st["launches"]["collective"] >= n_groups, q.name  # one exchange per group evaluation
     eng.close()
