@@ -693,7 +693,9 @@ struct Exec {
   // center (scattered row_ptr / label / column sectors); push (k_push_edge)
   // streams 8 bytes per entry of the edge's label.  The center's candidate count
   // is bounded by its seed segments (row lengths read once here) or N.
-  static constexpr uint64_t PUSH_MIN = 1ull << 22;  // smaller labels: pull (latency-bound either way)
+  // A small label is cheap to stream (64K entries = 512 KB), while pulling an
+  // unconstrained center touches every row's signature: push below PUSH_RATIO x bound.
+  // (ctx->push_min, default 2^16 entries)
   static constexpr uint64_t PUSH_RATIO = 6;
   gsmart_status decide_push() {
     push_dec.clear();
@@ -736,7 +738,7 @@ struct Exec {
       uint64_t bound = est[g.center];
       for (size_t ei : ord) {
         const uint64_t M = M_of(ei);
-        const bool p = (v & 8) || (M >= PUSH_MIN && M <= PUSH_RATIO * bound);
+        const bool p = (v & 8) || (M >= ctx->push_min && M <= PUSH_RATIO * bound);
         push_dec[gi][ei] = p;
         if (p) bound = std::min(bound, M);
       }
