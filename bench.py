@@ -251,9 +251,12 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     import torch
+    n_dev = max(1, torch.cuda.device_count())
+    oversub = world > n_dev  # more ranks than devices (e.g. checking the N>1 path on one GPU): share devices
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("gloo" if oversub else "nccl", init_method="env://")
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2106_14038_b200 as G
@@ -317,8 +320,8 @@ def main():
             times.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
     ms = statistics.mean(times)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
+    if world > 1:  # max over ranks
+        t = torch.tensor([ms], device="cpu" if oversub else dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.barrier()
         ms = float(t.item())
@@ -448,7 +451,8 @@ def main():
     cfg = config_of(args)
     cfg.update({"triples": int(len(s_h)), "entities": int(N), "predicates": int(P),
                 "queries": [q.name for q in qs], "edges_per_step": int(sum(E)),
-                "parallelism": ("partitioned" if partitioned else "replicas") if world > 1 else "single"})
+                "parallelism": ("partitioned" if partitioned else "replicas") if world > 1 else "single",
+                "devices": n_dev, "oversubscribed": oversub})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",

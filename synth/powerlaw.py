@@ -59,12 +59,15 @@ def queries(d: PowerlawData, n_queries=20, seed=7):
     out of one subject), chains (3-4 hops), triangles when the walk closes,
     with 0-2 vertices replaced by their constant."""
     rng = np.random.default_rng(seed)
-    s = d.s.cpu().numpy().astype(np.int64)
-    p = d.p.cpu().numpy().astype(np.int64)
-    o = d.o.cpu().numpy().astype(np.int64)
-    order = np.argsort(s, kind="stable")
-    ss, pp, oo = s[order], p[order], o[order]
-    starts = np.searchsorted(ss, np.arange(d.n_entities + 1))
+    s = d.s.cpu().numpy()
+    # subject-grouped copies for the walks: a stable sort by subject (on the
+    # data's device — the full 500M-triple set sorts in seconds on a GPU)
+    order = torch.sort(d.s, stable=True).indices
+    ss = d.s[order]
+    pp = d.p[order].cpu().numpy()
+    oo = d.o[order].cpu().numpy()
+    starts = torch.searchsorted(ss, torch.arange(d.n_entities + 1, device=ss.device, dtype=ss.dtype)).cpu().numpy()
+    del order, ss
 
     def out_edges(x):
         a, b = starts[x], starts[x + 1]
