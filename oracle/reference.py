@@ -413,6 +413,93 @@ def plan_degree(q):
             "pi": pi, "tree": tree, "closing": closing, "paths": paths}
 
 
+def plan_direction(q):
+    """Direction-driven traversal, P:L365-L379 (§6.1.1), with the cyclic
+    variant of step 2: roots are unvisited vertices without
+    unevaluated incoming edges (max unevaluated outgoing edges first; cyclic:
+    else the unvisited vertex with the most unevaluated outgoing edges); a
+    popped vertex evaluates all its unevaluated OUTGOING edges (one group, all
+    `OUT`, rows of the CSR LSpM only); newly visited targets are pushed in
+    ascending (unevaluated outgoing edges, index) order so the largest pops
+    first.  Ties beyond the paper's keys: lowest vertex index (R16).  A query
+    with constants is planned degree-driven, so it is refused here
+    (ValueError).  Returns the plan_degree dict shape; no back edges (the
+    groups read CSR rows only), trie order / tree / closing edges derived the
+    same way as for degree-driven plans, a later root joining through its
+    first edge to a visited vertex."""
+    n = q.n_vertices
+    E = q.edges
+    if any(q.is_const(i) for i in range(n)):
+        raise ValueError("direction-driven plans take variable-only queries (P:L381)")
+    F, W = set(), set()
+
+    def unev_in(v):
+        return sum(1 for k, (a, _, b) in enumerate(E) if k not in F and b == v)
+
+    def unev_out(v):
+        return sum(1 for k, (a, _, b) in enumerate(E) if k not in F and a == v)
+
+    groups, roots, glevel, depth = [], [], [], {}
+    while len(F) < len(E):
+        cands = [v for v in range(n) if v not in W and unev_in(v) == 0 and unev_out(v) > 0]
+        if not cands:  # cyclic: P:L377
+            cands = [v for v in range(n) if v not in W and unev_out(v) > 0]
+        if not cands:  # every remaining edge starts at a visited vertex (cannot happen: popped ones are drained)
+            cands = [v for v in range(n) if unev_out(v) > 0]
+        root = max(cands, key=lambda v: (unev_out(v), -v))
+        roots.append(root)
+        W.add(root)
+        depth[root] = 0
+        S = [root]
+        while S:
+            v = S.pop()
+            grp = [(k, OUT, b) for k, (a, _, b) in enumerate(E) if k not in F and a == v]
+            for k, _, _ in grp:
+                F.add(k)
+            new = []
+            for _, _, w in grp:
+                if w not in W:
+                    W.add(w)
+                    depth[w] = depth[v] + 1
+                    new.append(w)
+            new.sort(key=lambda w: (unev_out(w), w))
+            S.extend(new)
+            if grp:
+                groups.append((v, grp))
+                glevel.append(depth[v])
+    pi, tree, closing, pos = [], {}, {}, {}
+
+    def add(v):
+        pos[v] = len(pi)
+        pi.append(v)
+        closing.setdefault(v, [])
+    for v, grp in groups:
+        if v not in pos:
+            add(v)
+            # a later root joins the trie through its first edge to a visited vertex
+            for k, d, w in grp:
+                if w != v and w in pos:
+                    tree[v] = (k, w, IN)
+                    break
+        for k, d, w in grp:
+            if w == v:
+                closing[v].append((k, v, d))
+            elif w not in pos:
+                add(w)
+                tree[w] = (k, v, d)
+            elif tree.get(v, (None,))[0] == k:
+                continue  # the edge that joined v to the trie
+            else:
+                later, other = (w, v) if pos[w] > pos[v] else (v, w)
+                a, _, b = E[k]
+                closing[later].append((k, other, OUT if a == later else IN))
+    for v in q.variables:
+        if v not in pos:
+            add(v)
+    return {"seeds": [], "roots": roots, "groups": groups, "back": [[] for _ in groups], "level": glevel,
+            "pi": pi, "tree": tree, "closing": closing, "paths": {}}
+
+
 # --------------------------------------------------------------------------
 # Filter schedule: seeds (light edges, P:L279/P:L397), then every group center
 # in plan order is "revised" against all its incident patterns (§5 Eqs. 17/21
@@ -432,8 +519,10 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
          pattern: a guard (R13); a false guard makes the conjunction
          unsatisfiable, so every candidate set is emptied;
       3. revise(x) for each group center x in plan order, where
-         revise(x): cand_x &= AND_e y_e over EVERY pattern e incident to x
-         whose other end is a variable (or x itself):
+         revise(x): cand_x &= AND_e y_e over the group's patterns — its
+         unevaluated edges and its back edges; for a degree-driven plan that
+         is EVERY pattern incident to x whose other end is a variable (or x
+         itself), for a direction-driven plan the out-edges of x:
            e = (x, l, w): y_e(i) = OR_j [(i,l,j) in T] ^ cand_w(j)   (Eq. 17)
            e = (w, l, x): y_e(i) = OR_j [(j,l,i) in T] ^ cand_w(j)   (Eq. 21)
            e = (x, l, x): y_e(i) = [(i,l,i) in T]                    (R7)
@@ -472,11 +561,10 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
         for v in cand:
             cand[v][:] = False
 
-    def revise(x):
+    def revise(x, ks):
         y_all = np.ones(N, dtype=bool)
-        for a, l, b in q.edges:
-            if x not in (a, b) or q.vertices[a] is not None or q.vertices[b] is not None:
-                continue
+        for k in ks:
+            a, l, b = q.edges[k]
             y = np.zeros(N, dtype=bool)
             for i in range(N):
                 if not cand[x][i]:
@@ -490,12 +578,15 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
             y_all &= y
         cand[x] &= y_all
 
-    centers = [x for x, _ in plan["groups"]]
-    for x in centers:
-        revise(x)
+    # a group's patterns: its unevaluated edges and its back edges (degree-driven:
+    # every variable pattern incident to the center; direction-driven: the out-edges)
+    back = plan.get("back") or [[] for _ in plan["groups"]]
+    evals = [(x, [k for k, _, _ in grp] + [k for k, _, _ in bk]) for (x, grp), bk in zip(plan["groups"], back)]
+    for x, ks in evals:
+        revise(x, ks)
     if refine:
-        for x in list(reversed(centers))[1:]:
-            revise(x)
+        for x, ks in list(reversed(evals))[1:]:
+            revise(x, ks)
     return cand, ok
 
 

@@ -49,6 +49,7 @@ struct Level {           // trie level = one variable in visitation order pi
 
 struct gsmart_plan_s {
   uint64_t uid = 0;                    // process-unique id (keys cached CUDA graphs)
+  uint32_t traversal = GSMART_DEGREE;  // GSMART_DEGREE or GSMART_DIRECTION
   uint32_t n_vertices = 0;
   std::vector<gsmart_qvertex> vertices;
   std::vector<gsmart_qedge> edges;

@@ -14,8 +14,8 @@ namespace gsm {
 gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* P, std::string* err,
                          const std::function<double(uint32_t, uint32_t)>* fanout) {
   if (!q || (q->n_vertices && !q->v) || (q->n_edges && !q->e)) { *err = "null query arrays"; return GSMART_E_INVALID_ARG; }
-  if (traversal == GSMART_DIRECTION) { *err = "direction-driven traversal not supported in this version"; return GSMART_E_UNSUPPORTED; }
-  if (traversal != GSMART_DEGREE) { *err = "unknown traversal"; return GSMART_E_INVALID_ARG; }
+  if (traversal != GSMART_DEGREE && traversal != GSMART_DIRECTION) { *err = "unknown traversal"; return GSMART_E_INVALID_ARG; }
+  P->traversal = traversal;
   const uint32_t n = q->n_vertices, ne = q->n_edges;
   if (ne > 32) { *err = "more than 32 patterns"; return GSMART_E_INVALID_ARG; }
   P->n_vertices = n;
@@ -61,7 +61,53 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
 
   std::vector<uint32_t> depth(n, 0);
   std::vector<int32_t> first_parent(n, -1);
-  while (n_unev() > 0) {
+  if (traversal == GSMART_DIRECTION) {
+    // Direction-driven traversal (§6.1.1): a query with constants is
+    // planned degree-driven, so it is refused here.
+    if (!P->seeds.empty() || !P->guards.empty()) {
+      *err = "direction-driven plans take variable-only queries (P:L381)";
+      return GSMART_E_UNSUPPORTED;
+    }
+    auto unev_in = [&](uint32_t v) {
+      uint32_t c = 0;
+      for (uint32_t k = 0; k < ne; k++) if (!F[k] && q->e[k].dst == v) c++;
+      return c;
+    };
+    while (n_unev() > 0) {
+      // Step 2: an unvisited vertex without unevaluated incoming edges, max unevaluated
+      // outgoing edges (cyclic variant P:L377: else max unevaluated outgoing), lowest index
+      int32_t best = -1;
+      uint32_t bo = 0;
+      for (int pass = 0; pass < 3 && best < 0; pass++)
+        for (uint32_t v = 0; v < n; v++) {
+          if ((pass < 2 && W[v]) || unev_out(v) == 0) continue;
+          if (pass == 0 && unev_in(v) != 0) continue;
+          const uint32_t o = unev_out(v);
+          if (best < 0 || o > bo) { best = (int32_t)v; bo = o; }
+        }
+      const uint32_t root = (uint32_t)best;
+      P->roots.push_back(root);
+      W[root] = true; depth[root] = 0; first_parent[root] = -1;
+      std::vector<uint32_t> S{root};
+      while (!S.empty()) {                    // Steps 3-4: all unevaluated OUTGOING edges
+        const uint32_t v = S.back(); S.pop_back();
+        Group g; g.center = v; g.level = depth[v];
+        for (uint32_t k = 0; k < ne; k++)
+          if (!F[k] && q->e[k].src == v) g.edges.push_back({k, q->e[k].pred, OUT, q->e[k].dst});
+        for (auto& ge : g.edges) F[ge.edge] = true;
+        std::vector<uint32_t> fresh;
+        for (auto& ge : g.edges)
+          if (!W[ge.nbr]) { W[ge.nbr] = true; depth[ge.nbr] = depth[v] + 1; first_parent[ge.nbr] = (int32_t)v; fresh.push_back(ge.nbr); }
+        std::sort(fresh.begin(), fresh.end(), [&](uint32_t a, uint32_t b) {
+          const uint32_t oa = unev_out(a), ob = unev_out(b);
+          return oa != ob ? oa < ob : a < b;
+        });
+        for (uint32_t w : fresh) S.push_back(w);
+        if (!g.edges.empty()) P->groups.push_back(std::move(g));
+      }
+    }
+  }
+  while (traversal == GSMART_DEGREE && n_unev() > 0) {
     // Step 2: root = max unevaluated edges (among constant neighbours first,
     // P:L398), then max unevaluated out-edges, then lowest index (R16).
     int32_t best = -1; bool best_pref = false; uint32_t bu = 0, bo = 0;
@@ -128,7 +174,20 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
   std::set<uint32_t> root_set(P->roots.begin(), P->roots.end());
   for (auto& g : P->groups) {
     uint32_t v = g.center;
-    if (pos[v] < 0) add_level(v, -1, 0, 0, 0);   // a root
+    int32_t joined = -1;  // the edge through which a later root joins the trie
+    if (pos[v] < 0) {
+      // a root; a later one (direction-driven) joins through its first edge to a
+      // visited vertex, as that vertex's child over the reversed direction
+      for (auto& ge : g.edges)
+        if (ge.nbr != v && pos[ge.nbr] >= 0) { joined = (int32_t)ge.edge; break; }
+      if (joined >= 0) {
+        const auto& e = q->e[joined];
+        const uint32_t w = e.src == v ? e.dst : e.src;
+        add_level(v, joined, w, e.pred, e.src == v ? (uint32_t)IN : (uint32_t)OUT);
+      } else {
+        add_level(v, -1, 0, 0, 0);
+      }
+    }
     // With LSpM statistics (gsmart_plan given a built ctx) a group's new
     // neighbours enter the trie in ascending expected fan-out (entries per row
     // of the label, from the center's side): functional patterns (one child
@@ -143,6 +202,7 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
       });
     for (const GroupEdge* gp : order) {
       const GroupEdge& ge = *gp;
+      if ((int32_t)ge.edge == joined) continue;
       uint32_t w = ge.nbr;
       if (w == v) {
         P->levels[pos[v]].closing.push_back({ge.edge, ge.label, (uint32_t)pos[v], OUT});
@@ -192,7 +252,7 @@ static void jarr(std::ostringstream& o, const std::vector<uint32_t>& v) {
 
 std::string describe_plan(const gsmart_plan_t& p) {
   std::ostringstream o;
-  o << "{\"traversal\":\"degree\",\"roots\":";
+  o << "{\"traversal\":\"" << (p.traversal == GSMART_DIRECTION ? "direction" : "degree") << "\",\"roots\":";
   jarr(o, p.roots);
   o << ",\"seeds\":[";
   for (size_t i = 0; i < p.seeds.size(); i++) {

@@ -412,12 +412,12 @@ class Engine:
         gsmart_load_triples(self.ctx, s, p, o, n_entities, n_predicates)
         gsmart_build_lspm(self.ctx, keep)
 
-    def plan(self, q):
-        return Plan(self, q)
+    def plan(self, q, traversal=GSMART_DEGREE):
+        return Plan(self, q, traversal)
 
-    def query_batch(self, queries, flags=0):
+    def query_batch(self, queries, flags=0, traversal=GSMART_DEGREE):
         """Execute several queries concurrently (gsmart_execute_batch); returns rows per query."""
-        plans = [Plan(self, q) for q in queries]
+        plans = [Plan(self, q, traversal) for q in queries]
         try:
             res = gsmart_execute_batch(self.ctx, [p.h for p in plans], flags)
             out = []
@@ -436,8 +436,8 @@ class Engine:
             for p in plans:
                 p.close()
 
-    def query(self, q, flags=0, with_stats=False):
-        with self.plan(q) as pl:
+    def query(self, q, flags=0, with_stats=False, traversal=GSMART_DEGREE):
+        with self.plan(q, traversal) as pl:
             return pl.run(flags, with_stats)
 
     def close(self):
@@ -459,9 +459,9 @@ class Engine:
 
 
 class Plan:
-    def __init__(self, eng, q):
+    def __init__(self, eng, q, traversal=GSMART_DEGREE):
         self.eng = eng
-        self.h = gsmart_plan(eng.ctx, q)
+        self.h = gsmart_plan(eng.ctx, q, traversal)
 
     def describe(self):
         return gsmart_plan_describe(self.h)

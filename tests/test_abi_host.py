@@ -51,9 +51,9 @@ def test_no_gpu_fails_loudly(G):
     assert ei.value.name == "E_CUDA"
 
 
-def _pydesc(q):
+def _pydesc(q, direction=False):
     """oracle planner -> the describe() JSON shape, for comparison."""
-    pl = R.plan_degree(q)
+    pl = R.plan_direction(q) if direction else R.plan_degree(q)
     D = {0: "out", 1: "in"}
     return {
         "roots": pl["roots"],
@@ -64,12 +64,12 @@ def _pydesc(q):
         "pi": pl["pi"],
         "tree": {v: (k, p, D[d]) for v, (k, p, d) in pl["tree"].items()},
         "closing": {v: sorted((k, o, D[d]) for k, o, d in cl) for v, cl in pl["closing"].items()},
-        "paths": [sorted(map(tuple, pl["paths"][r])) for r in pl["roots"]],
+        "paths": [sorted(map(tuple, pl["paths"][r])) for r in pl["roots"]] if not direction else None,
     }
 
 
-def _cdesc(G, q):
-    h = G.gsmart_plan(None, q)
+def _cdesc(G, q, direction=False):
+    h = G.gsmart_plan(None, q, traversal=G.GSMART_DIRECTION if direction else G.GSMART_DEGREE)
     try:
         d = G.gsmart_plan_describe(h)
     finally:
@@ -118,6 +118,21 @@ def test_plan_parity_with_oracle_planner(G):
             assert c[key] == p[key], (key, q, c[key], p[key])
 
 
+def test_direction_plan_parity_with_oracle_planner(G, golden_fig):
+    """GSMART_DIRECTION (§6.1.1): the C++ planner == the oracle's plan_direction
+    on every field for random variable-only queries (cycles, self-loops,
+    multi-edges, disconnected parts) and Fig. 2 (Ex. 6.1: roots v0, v3)."""
+    qs = [tiny.random_case(s, n_consts=0)[3] for s in range(400)] + [fixtures.fig2_query()]
+    for q in qs:
+        c, d = _cdesc(G, q, direction=True)
+        p = _pydesc(q, direction=True)
+        assert d["traversal"] == "direction"
+        for key in ("roots", "groups", "level", "pi", "tree", "closing"):
+            assert c[key] == p[key], (key, q, c[key], p[key])
+    c, _ = _cdesc(G, fixtures.fig2_query(), direction=True)
+    assert c["roots"] == golden_fig["ex61_roots"]
+
+
 def test_plan_errors(G):
     with pytest.raises(G.GsmartError) as e:
         G.gsmart_plan(None, Query((None,), ((0, 1, 1),)))       # vertex out of range
@@ -125,6 +140,6 @@ def test_plan_errors(G):
     with pytest.raises(G.GsmartError) as e:
         G.gsmart_plan(None, Query((None, None), ((0, 0, 0),)))  # pred 0, var 1 unused
     assert e.value.name == "E_INVALID_ARG"
-    with pytest.raises(G.GsmartError) as e:
-        G.gsmart_plan(None, fixtures.fig2_query(), traversal=G.GSMART_DIRECTION)
+    with pytest.raises(G.GsmartError) as e:  # direction-driven + constants: planned degree-driven
+        G.gsmart_plan(None, Query((None, 3), ((0, 1, 1),)), traversal=G.GSMART_DIRECTION)
     assert e.value.name == "E_UNSUPPORTED"

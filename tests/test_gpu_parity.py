@@ -174,6 +174,58 @@ def test_random_tiny_rows_and_candidates(G, eng, chunk):
                 assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
 
 
+# ------------------------------------------------------------------ direction-driven plans (§6.1.1, f1)
+def test_direction_plans_rows_and_candidates(G, eng, golden_fig):
+    """GSMART_DIRECTION (CSR-side groups, multi-root plans joined in one trie):
+    rows == brute force and every candidate bitmap == filter_schedule under
+    the oracle's plan_direction, refine on and off; Fig. 2 (two roots, Ex. 6.1)."""
+    s, p, o = fixtures.fig1_triples()
+    eng.load(s, p, o, 8, 4)
+    q = fixtures.fig2_query()
+    assert _rows(eng.query(q, traversal=G.GSMART_DIRECTION)) == [tuple(r) for r in golden_fig["solution_rows"]]
+    for seed in range(600):
+        (s, p, o), n, P, q = tiny.random_case(seed, n_consts=0)
+        eng.load(s, p, o, n, P)
+        exp = R.brute_force(s, p, o, n, q)
+        plan = R.plan_direction(q)
+        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+            pl = G.gsmart_plan(eng.ctx, q, G.GSMART_DIRECTION)
+            r = G.gsmart_execute(eng.ctx, pl, flags | G.GSMART_KEEP_CANDIDATES)
+            try:
+                assert _rows(G.gsmart_result_rows(r)) == exp, (seed, q)
+                ref, _ = R.filter_schedule(s, p, o, n, q, plan=plan, refine=refine)
+                for v in q.variables:
+                    ptr, nw = G.gsmart_result_candidates(r, v)
+                    got = _bits_to_set(G.gsmart_copy_to_host(eng.ctx, ptr, nw * 4), n)
+                    assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
+            finally:
+                G.gsmart_result_free(r)
+                G.gsmart_plan_free(pl)
+
+
+def test_direction_plans_watdiv_vs_oracle(G, eng):
+    """The variable-only WatDiv templates (C1, C3) and random-walk power-law
+    queries planned direction-driven == C oracle (same rows as degree-driven)."""
+    from synth import watdiv, powerlaw
+    d = watdiv.generate(0.02)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = [q for q in watdiv.queries(d) if all(v is None for v in q.vertices)]
+    assert len(qs) >= 2
+    for q, got in zip(qs, eng.query_batch(qs, traversal=G.GSMART_DIRECTION)):
+        e = ix.query(q)
+        assert got.shape == e.shape and np.array_equal(got, e), q.name
+    d = powerlaw.generate(400_000, 20_000, 200)
+    s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+    eng.load(s, p, o, d.n_entities, d.n_predicates)
+    ix = OracleIndex(s, p, o)
+    qs = [q for q in powerlaw.queries(d, 15, seed=9) if all(v is None for v in q.vertices)]
+    for q, got in zip(qs, eng.query_batch(qs, traversal=G.GSMART_DIRECTION)):
+        e = ix.query(q)
+        assert got.shape == e.shape and np.array_equal(got, e), q
+
+
 # ------------------------------------------------------------------ larger, skewed graphs
 def _data_queries(rng, s, p, o, n_q):
     """random connected queries whose constants come from the data (non-empty-ish)."""

@@ -190,6 +190,56 @@ def test_ex62_degree_plan(golden_fig):
     assert sorted(pl["paths"][2]) == sorted(golden_fig["paths"])
 
 
+def test_ex61_direction_plan(golden_fig):
+    """Ex. 6.1: the direction-driven traversal of Fig. 2b."""
+    q = fixtures.fig2_query()
+    pl = R.plan_direction(q)
+    assert pl["roots"] == golden_fig["ex61_roots"]
+    got = [[c, [list(q.edges[k]) for k, _, _ in g]] for c, g in pl["groups"]]
+    assert got == golden_fig["ex61_direction_groups"]
+    assert all(d == R.OUT for _, g in pl["groups"] for _, d, _ in g)  # rows of the CSR LSpM only
+
+
+def test_direction_plan_invariants():
+    """Every pattern evaluated exactly once, at its source (OUT); roots have no
+    unevaluated incoming edge unless the rest is cyclic; constants refused."""
+    checked = 0
+    for seed in range(400):
+        (_, _, _), n, P, q = tiny.random_case(seed, n_consts=0)
+        pl = R.plan_direction(q)
+        ks = [k for _, g in pl["groups"] for k, _, _ in g]
+        assert sorted(ks) == list(range(len(q.edges)))
+        for v, g in pl["groups"]:
+            for k, d, w in g:
+                assert q.edges[k][0] == v and q.edges[k][2] == w and d == R.OUT
+        assert sorted(pl["pi"]) == q.variables
+        checked += 1
+    assert checked == 400
+    with pytest.raises(ValueError):
+        R.plan_direction(Query((None, 3), ((0, 1, 1),)))
+
+
+def test_filter_schedule_direction_sound_and_exact():
+    """The schedule under direction-driven plans: sound (⊇ projections) and,
+    for acyclic connected queries whose variable graph is a tree, the first
+    root's set is exact when every pattern points away from it (an
+    out-tree: the backward pass is a bottom-up semijoin)."""
+    exact = 0
+    for seed in range(600):
+        (s, p, o), n, P, q = tiny.random_case(seed, n_consts=0)
+        rows = R.brute_force(s, p, o, n, q)
+        plan = R.plan_direction(q)
+        cand, ok = R.filter_schedule(s, p, o, n, q, plan=plan, refine=True)
+        for ci, v in enumerate(q.variables):
+            assert all(cand[v][r[ci]] for r in rows), (seed, v)
+        if _tree_no_multi(q) and len(plan["roots"]) == 1 and not any(a == b for a, _, b in q.edges):
+            r0 = plan["roots"][0]
+            proj = sorted({row[q.variables.index(r0)] for row in rows})
+            assert cand[r0].nonzero()[0].tolist() == proj, (seed, q)
+            exact += 1
+    assert exact > 50
+
+
 def test_planner_constants_seed_and_root():
     # ?x worksFor <D> . ?x name ?y  : the constant edge is a seed, root = x (P:L397-L398)
     q = Query((None, None, 7), ((0, 6, 2), (0, 2, 1)))
