@@ -1302,6 +1302,11 @@ gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan) {
   if (!plan) FAIL(GSMART_E_INVALID_ARG, "null plan");
   for (auto& e : plan->edges)
     if (e.pred > ctx->P) FAIL(GSMART_E_INVALID_ARG, "query predicate id > n_predicates");
+  if (!ctx->f[1].built) {  // CSR-only LSpM: a direction-driven plan reading subject rows only
+    bool ok = plan->traversal == GSMART_DIRECTION;
+    for (auto& L : plan->levels) ok = ok && (L.tree_edge < 0 || L.dir == OUT);
+    if (!ok) FAIL(GSMART_E_STATE, "this plan needs the CSC LSpM (build CSR|CSC, or plan direction-driven after a CSR-only build)");
+  }
   return GSMART_OK;
 }
 
@@ -1430,7 +1435,7 @@ extern "C" gsmart_status gsmart_execute(gsmart_ctx* ctx, const gsmart_plan_t* pl
   if (!ctx || !plan || !out) return GSMART_E_INVALID_ARG;
   *out = nullptr;
   if (ctx->poisoned) return GSMART_E_CUDA;
-  if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
+  if (!ctx->f[0].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm must be called first");
   CU(cudaSetDevice(ctx->cfg.device));
   return run_batch(ctx, &plan, 1, flags, out);
 }
@@ -1440,7 +1445,7 @@ extern "C" gsmart_status gsmart_execute_batch(gsmart_ctx* ctx, const gsmart_plan
   if (!ctx || (n && (!plans || !out))) return GSMART_E_INVALID_ARG;
   for (uint32_t i = 0; i < n; i++) out[i] = nullptr;
   if (ctx->poisoned) return GSMART_E_CUDA;
-  if (!ctx->f[0].built || !ctx->f[1].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm(CSR|CSC) must be called first");
+  if (!ctx->f[0].built) FAIL(GSMART_E_STATE, "gsmart_build_lspm must be called first");
   CU(cudaSetDevice(ctx->cfg.device));
   gsmart_status s = run_batch(ctx, plans, n, flags, out);
   if (s != GSMART_OK)

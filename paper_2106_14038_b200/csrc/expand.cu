@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
   }
   const Fmt<PT> fsrc = fmt_of<PT>(a.f[a.dir & 1]);
   const Fmt<PT> f0 = fmt_of<PT>(a.f[0]), f1 = fmt_of<PT>(a.f[1]);
+  const bool csr_only = a.f[1].rp == nullptr;
   const uint32_t F1 = (uint32_t)F + 1;
   unsigned long long n_exam = 0, n_close = 0;
   while (true) {
@@ -458,9 +459,12 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
       for (int j = 0; j < EX_I; j++) {
         const uint32_t c = child[j], tgt = row[j];
         const bool on = (keepm >> j) & 1u;
-        const uint32_t c0 = on ? __ldg(fc.rp + c) : 0u, c1 = on ? __ldg(fc.rp + c + 1) : 0u;
-        const uint32_t g0 = on ? __ldg(fo.rp + tgt) : 0u, g1 = on ? __ldg(fo.rp + tgt + 1) : 0u;
-        useo[j] = (g1 - g0) < (c1 - c0);
+        // CSR-only LSpM (direction-driven plans): the pattern's subject row is the
+        // only one stored — the child's when it is the subject, else the target's
+        const bool use_c = on && (!csr_only || cl.dir == 0), use_g = on && (!csr_only || cl.dir == 1);
+        const uint32_t c0 = use_c ? __ldg(fc.rp + c) : 0u, c1 = use_c ? __ldg(fc.rp + c + 1) : 0u;
+        const uint32_t g0 = use_g ? __ldg(fo.rp + tgt) : 0u, g1 = use_g ? __ldg(fo.rp + tgt + 1) : 0u;
+        useo[j] = csr_only ? cl.dir == 1 : (g1 - g0) < (c1 - c0);
         row[j] = useo[j] ? tgt : c;
         key[j] = useo[j] ? c : tgt;
         lo[j] = useo[j] ? g0 : c0;

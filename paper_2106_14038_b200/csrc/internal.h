@@ -66,7 +66,8 @@ struct gsmart_plan_s {
 namespace gsm {
 // fanout (optional): expected children per parent of a pattern (label, dir seen
 // from the center) — orders a group's new neighbours in the trie
+// csr_only: plan for a CSR-only LSpM (direction-driven: later roots are free levels)
 gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* out, std::string* err,
-                         const std::function<double(uint32_t, uint32_t)>* fanout = nullptr);
+                         const std::function<double(uint32_t, uint32_t)>* fanout = nullptr, bool csr_only = false);
 std::string describe_plan(const gsmart_plan_t& p);
 }  // namespace gsm

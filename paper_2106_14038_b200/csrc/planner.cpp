@@ -12,7 +12,7 @@
 namespace gsm {
 
 gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* P, std::string* err,
-                         const std::function<double(uint32_t, uint32_t)>* fanout) {
+                         const std::function<double(uint32_t, uint32_t)>* fanout, bool csr_only) {
   if (!q || (q->n_vertices && !q->v) || (q->n_edges && !q->e)) { *err = "null query arrays"; return GSMART_E_INVALID_ARG; }
   if (traversal != GSMART_DEGREE && traversal != GSMART_DIRECTION) { *err = "unknown traversal"; return GSMART_E_INVALID_ARG; }
   P->traversal = traversal;
@@ -178,8 +178,10 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
     if (pos[v] < 0) {
       // a root; a later one (direction-driven) joins through its first edge to a
       // visited vertex, as that vertex's child over the reversed direction
+      // (not over a CSR-only LSpM: the join reads the visited vertex's CSC row; the
+      // root is then a free level and the edge a closing edge, checked in CSR rows)
       for (auto& ge : g.edges)
-        if (ge.nbr != v && pos[ge.nbr] >= 0) { joined = (int32_t)ge.edge; break; }
+        if (!csr_only && ge.nbr != v && pos[ge.nbr] >= 0) { joined = (int32_t)ge.edge; break; }
       if (joined >= 0) {
         const auto& e = q->e[joined];
         const uint32_t w = e.src == v ? e.dst : e.src;

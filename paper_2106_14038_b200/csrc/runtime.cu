@@ -673,7 +673,8 @@ extern "C" gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uin
       const double rows = (double)lr[label], ent = (double)lr[ctx->P + 1 + label];
       return rows > 0 ? ent / rows : 0.0;
     };
-  gsmart_status s = build_plan(q, traversal, p.get(), &err, stats ? &fan : nullptr);
+  const bool csr_only = ctx && ctx->f[0].built && !ctx->f[1].built;
+  gsmart_status s = build_plan(q, traversal, p.get(), &err, stats ? &fan : nullptr, csr_only);
   if (s != GSMART_OK) {
     if (ctx) ctx->err = err; else g_static_err = err;
     return s;

@@ -203,6 +203,35 @@ def test_direction_plans_rows_and_candidates(G, eng, golden_fig):
                 G.gsmart_plan_free(pl)
 
 
+def test_direction_plans_csr_only(G):
+    """The CSR-only LSpM (the direction-driven storage): direction
+    plans read subject rows only — a later root is a free level joined by a
+    closing edge checked in a CSR row; rows == brute force / C oracle.  A
+    degree-driven plan needs CSC: E_STATE."""
+    e = G.Engine(0)
+    try:
+        for seed in range(300):
+            (s, p, o), n, P, q = tiny.random_case(seed, n_consts=0)
+            G.gsmart_load_triples(e.ctx, s, p, o, n, P)
+            G.gsmart_build_lspm(e.ctx, formats=G.GSMART_CSR)
+            assert _rows(e.query(q, traversal=G.GSMART_DIRECTION)) == R.brute_force(s, p, o, n, q), (seed, q)
+        with pytest.raises(G.GsmartError) as ei:
+            e.query(q)
+        assert ei.value.name == "E_STATE"
+        from synth import watdiv
+        d = watdiv.generate(0.02)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        G.gsmart_load_triples(e.ctx, s, p, o, d.n_entities, d.n_predicates)
+        G.gsmart_build_lspm(e.ctx, formats=G.GSMART_CSR)
+        ix = OracleIndex(s, p, o)
+        for q in [q for q in watdiv.queries(d) if all(v is None for v in q.vertices)]:
+            got = e.query(q, traversal=G.GSMART_DIRECTION)
+            x = ix.query(q)
+            assert got.shape == x.shape and np.array_equal(got, x), q.name
+    finally:
+        e.close()
+
+
 def test_direction_plans_watdiv_vs_oracle(G, eng):
     """The variable-only WatDiv templates (C1, C3) and random-walk power-law
     queries planned direction-driven == C oracle (same rows as degree-driven)."""
