@@ -920,7 +920,8 @@ struct Exec {
     gedges.resize(plan->groups.size());
     for (size_t gi = 0; gi < plan->groups.size(); gi++) {
       gedges[gi] = plan->groups[gi].edges;
-      gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
+      if (!ctx->no_back)  // measurement switch GSMART_NO_BACK=1 (the bitmaps then differ from the schedule)
+        gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
     }
     plan_ancestors();
     TRY(decide_push());
@@ -1245,7 +1246,10 @@ struct Exec {
         R->stats.level_alive[k] = sl.h_pin[128 + k];
       }
     }
-    if (ctx->world > 1 && state == S_PHASE2) TRY(gather_rows());
+    if (ctx->world > 1 && state == S_PHASE2) {
+      TRY(gather_rows());
+      R->host_valid = R->n_rows == 0 && !(flags & GSMART_COUNT_ONLY);  // rank 0's gathered rows are copied on demand
+    }
     unsigned long long c[C_NCTR];
     if (ctr_pinned) memcpy(c, sl.h_pin + 192, C_NCTR * 8);
     else CU(cudaMemcpy(c, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost));

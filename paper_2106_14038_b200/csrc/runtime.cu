@@ -115,6 +115,7 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   if (const char* sv = getenv("GSMART_SPEC_TEST")) ctx->spec_test = atoi(sv) ? 1u : 0u;
   if (const char* tv = getenv("GSMART_NO_TMA")) ctx->use_tma = atoi(tv) == 0;
   if (const char* pv = getenv("GSMART_PUSH_MIN")) ctx->push_min = strtoull(pv, nullptr, 10);
+  if (const char* bv = getenv("GSMART_NO_BACK")) ctx->no_back = atoi(bv) != 0;
   if (const char* lv = getenv("GSMART_L2_PERSIST")) ctx->l2_persist = atoi(lv) != 0;
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     g_static_err = "cudaSetDevice failed";
