@@ -76,6 +76,9 @@ typedef enum {
 #define GSMART_KEEP_CANDIDATES 16u /* keep the candidate bitmaps for gsmart_result_candidates */
 #define GSMART_NO_GRAPH 32u       /* launch kernels one by one instead of replaying the plan's CUDA graph */
 #define GSMART_NO_SPECULATE 64u   /* always wait for the level sizes before pruning/rows (no speculative phase 2) */
+#define GSMART_BACK_EDGES 128u    /* every evaluation of a group also tests the center's already-evaluated patterns
+                                     against the earlier centers' bitmaps (Eq. 16 over Eq. 14 binding vectors,
+                                     DESIGN.md R-back): tighter candidate sets, more work per group */
 
 typedef struct gsmart_ctx gsmart_ctx;
 typedef struct gsmart_plan_s gsmart_plan_t;

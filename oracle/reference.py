@@ -509,7 +509,7 @@ def plan_direction(q):
 # --------------------------------------------------------------------------
 
 
-def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
+def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True, back_edges=False):
     """Candidate sets per variable after the schedule DESIGN.md states:
       1. cand_v = [0, N) for every variable (Eq. 4/5 with no constraint yet);
       2. each seed edge in edge-index order (light edges):
@@ -520,15 +520,15 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
          unsatisfiable, so every candidate set is emptied;
       3. revise(x) for each group center x in plan order, where
          revise(x): cand_x &= AND_e y_e over the group's patterns — its
-         unevaluated edges and its back edges; for a degree-driven plan that
-         is EVERY pattern incident to x whose other end is a variable (or x
-         itself), for a direction-driven plan the out-edges of x:
+         unevaluated edges (§5), and with back_edges (GSMART_BACK_EDGES) also
+         its back edges, so that for a degree-driven plan it is EVERY pattern
+         incident to x whose other end is a variable (or x itself):
            e = (x, l, w): y_e(i) = OR_j [(i,l,j) in T] ^ cand_w(j)   (Eq. 17)
            e = (w, l, x): y_e(i) = OR_j [(j,l,i) in T] ^ cand_w(j)   (Eq. 21)
            e = (x, l, x): y_e(i) = [(i,l,i) in T]                    (R7)
          For the group's unevaluated edges this is §5 (Eqs. 17/21 with the
          neighbours' binding vectors as the diag(.) selections of Eqs.
-         15-16); for edges already evaluated at an earlier center c it is
+         15-16); for back edges (evaluated at an earlier center c) it is
          Eq. 16's restriction of x's rows to c's Eq. 14 binding vector;
       4. if refine: revise(x) for the centers in reverse plan order, the last
          one skipped (nothing it reads changed after it).
@@ -578,9 +578,10 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True):
             y_all &= y
         cand[x] &= y_all
 
-    # a group's patterns: its unevaluated edges and its back edges (degree-driven:
-    # every variable pattern incident to the center; direction-driven: the out-edges)
-    back = plan.get("back") or [[] for _ in plan["groups"]]
+    # a group's patterns: its unevaluated edges, plus (back_edges: GSMART_BACK_EDGES)
+    # its back edges — with them a degree-driven group is every variable pattern
+    # incident to the center (R-back); direction-driven plans have none
+    back = (plan.get("back") if back_edges else None) or [[] for _ in plan["groups"]]
     evals = [(x, [k for k, _, _ in grp] + [k for k, _, _ in bk]) for (x, grp), bk in zip(plan["groups"], back)]
     for x, ks in evals:
         revise(x, ks)

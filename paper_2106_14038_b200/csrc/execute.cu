@@ -702,7 +702,8 @@ struct Exec {
     const int v = ctx->filter_variant;
     if (!ctx->lm.built || (ctx->world > 1 && !ctx->lm_in.built) || (v & 16) || plan->groups.empty())
       return GSMART_OK;
-    auto it = ctx->push_cache.find(plan->uid);
+    const uint64_t pkey = plan->uid * 2 + ((flags & GSMART_BACK_EDGES) ? 1 : 0);  // decisions per edge set
+    auto it = ctx->push_cache.find(pkey);
     if (it != ctx->push_cache.end() && it->second.first == ctx->lspm_gen) {
       push_dec = it->second.second;
       return GSMART_OK;
@@ -743,7 +744,7 @@ struct Exec {
         if (p) bound = std::min(bound, M);
       }
     }
-    ctx->push_cache[plan->uid] = {ctx->lspm_gen, push_dec};
+    ctx->push_cache[pkey] = {ctx->lspm_gen, push_dec};
     return GSMART_OK;
   }
 
@@ -885,7 +886,7 @@ struct Exec {
 
   // phase 1 = seeds + grouped evaluation + expansion (graph key: uid, tag 0)
   gsmart_status run_phase1() {
-    return run_cached(plan->uid << 3, flags & GSMART_NO_REFINE, [&] { return phase1_kernels(); });
+    return run_cached(plan->uid << 3, flags & (GSMART_NO_REFINE | GSMART_BACK_EDGES), [&] { return phase1_kernels(); });
   }
 
   gsmart_status start() {
@@ -920,7 +921,7 @@ struct Exec {
     gedges.resize(plan->groups.size());
     for (size_t gi = 0; gi < plan->groups.size(); gi++) {
       gedges[gi] = plan->groups[gi].edges;
-      if (!ctx->no_back)  // measurement switch GSMART_NO_BACK=1 (the bitmaps then differ from the schedule)
+      if (flags & GSMART_BACK_EDGES)
         gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
     }
     plan_ancestors();

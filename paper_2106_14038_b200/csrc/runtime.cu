@@ -115,7 +115,6 @@ extern "C" gsmart_status gsmart_create(const gsmart_config* cfg, gsmart_ctx** ou
   if (const char* sv = getenv("GSMART_SPEC_TEST")) ctx->spec_test = atoi(sv) ? 1u : 0u;
   if (const char* tv = getenv("GSMART_NO_TMA")) ctx->use_tma = atoi(tv) == 0;
   if (const char* pv = getenv("GSMART_PUSH_MIN")) ctx->push_min = strtoull(pv, nullptr, 10);
-  if (const char* bv = getenv("GSMART_NO_BACK")) ctx->no_back = atoi(bv) != 0;
   if (const char* lv = getenv("GSMART_L2_PERSIST")) ctx->l2_persist = atoi(lv) != 0;
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
     g_static_err = "cudaSetDevice failed";
@@ -703,7 +702,8 @@ extern "C" void gsmart_plan_free(gsmart_plan_t* plan) {
     std::lock_guard<std::mutex> lk(g_live_mu);
     int dev0 = -1;
     for (gsmart_ctx* ctx : g_live) {
-      ctx->push_cache.erase(uid);
+      ctx->push_cache.erase(uid * 2);
+      ctx->push_cache.erase(uid * 2 + 1);
       ctx->p2_guess.erase(uid);
       ctx->plan_cost.erase(uid);
       bool any = false;

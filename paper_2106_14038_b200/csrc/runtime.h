@@ -251,7 +251,6 @@ struct gsmart_ctx {
   uint32_t exchange = GSMART_XCHG_PEER;
   bool use_tma = true;        // GSMART_NO_TMA=1: plain loads instead of cp.async.bulk staging (A/B)
   uint64_t push_min = 1ull << 16;  // smallest label streamed by the push form (GSMART_PUSH_MIN, A/B)
-  bool no_back = false;            // GSMART_NO_BACK=1: groups without back edges (A/B only)
   bool l2_persist = false;    // GSMART_L2_PERSIST=1: persisting L2 window over the candidate bitmaps (A/B)
   // push/pull choice per plan (uid -> lspm_gen, per group per edge), DESIGN.md §5
   std::unordered_map<uint64_t, std::pair<uint64_t, std::vector<std::vector<uint8_t>>>> push_cache;

@@ -22,6 +22,7 @@ GSMART_DEGREE, GSMART_DIRECTION = 0, 1
 GSMART_COUNT_ONLY, GSMART_KEEP_ON_DEVICE, GSMART_NO_REFINE, GSMART_PROFILE = 1, 2, 4, 8
 GSMART_KEEP_CANDIDATES, GSMART_NO_GRAPH = 16, 32
 GSMART_NO_SPECULATE = 64
+GSMART_BACK_EDGES = 128
 NKERNELS, MAX_LEVELS = 16, 32
 
 

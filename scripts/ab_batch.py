@@ -31,6 +31,7 @@ s, p, o, N, P, qs = bench.workload(args.workload, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for var in args.variants.split(";"):
     env = {} if var == "default" else dict(kv.split("=") for kv in var.split(","))
+    xflags = int(env.pop("flags", "0"))  # execute flags, e.g. flags=128 (GSMART_BACK_EDGES)
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -47,7 +48,7 @@ for var in args.variants.split(";"):
     st = torch.cuda.current_stream(dev)
 
     def step():
-        for r in G.gsmart_execute_batch(eng.ctx, plans, G.GSMART_KEEP_ON_DEVICE):
+        for r in G.gsmart_execute_batch(eng.ctx, plans, G.GSMART_KEEP_ON_DEVICE | xflags):
             G.gsmart_result_free(r)
 
     for _ in range(args.warmup):
@@ -69,7 +70,7 @@ for var in args.variants.split(";"):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            G.gsmart_result_free(G.gsmart_execute(eng.ctx, pl, G.GSMART_KEEP_ON_DEVICE))
+            G.gsmart_result_free(G.gsmart_execute(eng.ctx, pl, G.GSMART_KEEP_ON_DEVICE | xflags))
             e1.record(st)
             e1.synchronize()
             xs.append(e0.elapsed_time(e1))

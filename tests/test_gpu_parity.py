@@ -165,13 +165,14 @@ def test_random_tiny_rows_and_candidates(G, eng, chunk):
         (s, p, o), n, P, q = tiny.random_case(seed)
         eng.load(s, p, o, n, P)
         exp = R.brute_force(s, p, o, n, q)
-        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+        for flags, refine, back in ((0, True, False), (G.GSMART_NO_REFINE, False, False),
+                                    (G.GSMART_BACK_EDGES, True, True)):
             rows, cs, _ = _cands(G, eng, q, flags)
             assert _rows(rows) == exp, (seed, q)
-            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine)
+            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=back)
             for v in q.variables:
                 got = _bits_to_set(cs[v], n)
-                assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
+                assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q, flags)
 
 
 # ------------------------------------------------------------------ direction-driven plans (§6.1.1, f1)
@@ -598,10 +599,11 @@ def test_push_form_tiny_rows_and_candidates(G, eng_push):
         (s, p, o), n, P, q = tiny.random_case(seed)
         eng_push.load(s, p, o, n, P)
         exp = R.brute_force(s, p, o, n, q)
-        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+        for flags, refine, back in ((0, True, False), (G.GSMART_NO_REFINE, False, False),
+                                    (G.GSMART_BACK_EDGES, True, True)):
             rows, cs, _ = _cands(G, eng_push, q, flags)
             assert _rows(rows) == exp, (seed, q)
-            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine)
+            ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=back)
             for v in q.variables:
                 assert _bits_to_set(cs[v], n) == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q)
 

@@ -108,21 +108,24 @@ def test_level0_bitmaps_fig1(golden_fig):
     assert R.grouped_eval_in_out(A, D, F).nonzero()[0].tolist() == [1, 4, 5]
 
 
-def test_filter_schedule_fig1_steps(golden_fig):
+@pytest.mark.parametrize("back", [False, True])
+def test_filter_schedule_fig1_steps(golden_fig, back):
     """Every step of the filter schedule on Fig. 1/2 (golden, hand-derived):
-    group 0 -> {1,5} (Ex. 7.2), group 1 -> v0 = {2}, backward -> v2 = {1}."""
+    group 0 -> {1,5} (Ex. 7.2), group 1 -> v0 = {2}, backward -> v2 = {1};
+    with and without the back edges (group 1 then also tests v0 director v2
+    against {1,5}: Product0 still qualifies)."""
     s, p, o = fixtures.fig1_triples()
     q = fixtures.fig2_query()
     plan = R.plan_degree(q)
     g = golden_fig["schedule_fig1"]
-    one = dict(plan, groups=plan["groups"][:1])
-    c1, ok = R.filter_schedule(s, p, o, 8, q, plan=one, refine=False)
+    one = dict(plan, groups=plan["groups"][:1], back=plan["back"][:1])
+    c1, ok = R.filter_schedule(s, p, o, 8, q, plan=one, refine=False, back_edges=back)
     assert ok
     assert c1[2].nonzero()[0].tolist() == g["after_group0_v2"] == golden_fig["level0_candidates"]
-    c2, _ = R.filter_schedule(s, p, o, 8, q, refine=False)
+    c2, _ = R.filter_schedule(s, p, o, 8, q, refine=False, back_edges=back)
     assert c2[0].nonzero()[0].tolist() == g["after_group1_v0"]
     assert c2[2].nonzero()[0].tolist() == g["after_group0_v2"]
-    c3, _ = R.filter_schedule(s, p, o, 8, q, refine=True)
+    c3, _ = R.filter_schedule(s, p, o, 8, q, refine=True, back_edges=back)
     assert c3[2].nonzero()[0].tolist() == g["after_refine_v2"]
     assert c3[0].nonzero()[0].tolist() == g["after_group1_v0"]
     for v in g["never_centers"]:
@@ -150,7 +153,8 @@ def _tree_no_multi(q):
     return len({find(v) for v in q.variables}) == 1
 
 
-def test_filter_schedule_root_exact_acyclic():
+@pytest.mark.parametrize("back", [False, True])
+def test_filter_schedule_root_exact_acyclic(back):
     """Exactness, not just soundness: for a connected query whose variable graph
     is a tree (constants and self-loops allowed), the forward pass followed by
     the backward re-evaluation is a bottom-up semijoin reduction, so the root's
@@ -165,7 +169,7 @@ def test_filter_schedule_root_exact_acyclic():
         if len(plan["roots"]) != 1:
             continue
         rows = R.brute_force(s, p, o, n, q)
-        cand, ok = R.filter_schedule(s, p, o, n, q, plan=plan, refine=True)
+        cand, ok = R.filter_schedule(s, p, o, n, q, plan=plan, refine=True, back_edges=back)
         r = plan["roots"][0]
         proj = sorted({row[q.variables.index(r)] for row in rows})
         assert cand[r].nonzero()[0].tolist() == proj, (seed, q)
@@ -325,12 +329,18 @@ def test_tree_dp_equals_brute_force_random():
 
 def test_filter_schedule_sound_random():
     """Every candidate set contains the projection of the answer (soundness of
-    Eqs. 17/21 pruning), on tree and cyclic queries."""
+    Eqs. 17/21 pruning), on tree and cyclic queries; the back edges only
+    shrink the sets."""
     for seed in range(300):
         (s, p, o), n, P, q = tiny.random_case(seed)
         rows = R.brute_force(s, p, o, n, q)
         for refine in (False, True):
-            cand, ok = R.filter_schedule(s, p, o, n, q, refine=refine)
+            c0, _ = R.filter_schedule(s, p, o, n, q, refine=refine)
+            cb, _ = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=True)
+            for v in q.variables:
+                assert not (cb[v] & ~c0[v]).any(), (seed, v)
+        for refine, back in ((False, False), (True, False), (True, True)):
+            cand, ok = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=back)
             for ci, v in enumerate(q.variables):
                 proj = {r[ci] for r in rows}
                 assert all(cand[v][x] for x in proj), (seed, v)
