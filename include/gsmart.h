@@ -175,6 +175,22 @@ gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s, const uint
 gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep_preds, uint32_t n_keep,
                                 uint32_t formats);
 
+/* Query-dependent LSpM with direction-split keep-sets (§6.2; Ex. 6.4
+ * the CSR keeps the predicates evaluated along their direction,
+ * the CSC those evaluated against it).  keep_csr[n_csr] / keep_csc[n_csc]:
+ * predicate ids (host arrays; an empty set stores no triples in that format).
+ * Builds both formats and the label-major lists (their union).  Executing a
+ * plan that reads a label a format does not hold fails with GSMART_E_STATE
+ * (gsmart_plan_keep_sets gives the sets a batch of plans needs). */
+gsmart_status gsmart_build_lspm_split(gsmart_ctx* ctx, const uint32_t* keep_csr, uint32_t n_csr,
+                                      const uint32_t* keep_csc, uint32_t n_csc);
+/* The predicate ids each format must hold to execute the n plans with the
+ * execute flags `flags` (GSMART_BACK_EDGES adds the back edges): writes at
+ * most cap ids to each of csr_out / csc_out (ascending) and the full counts to
+ * *n_csr / *n_csc.  Closing edges are charged to the CSR (the subject's row). */
+gsmart_status gsmart_plan_keep_sets(const gsmart_plan_t* const* plans, uint32_t n, uint32_t flags, uint32_t* csr_out,
+                                    uint32_t* n_csr, uint32_t* csc_out, uint32_t* n_csc, uint32_t cap);
+
 /* Device view of one built LSpM format (for inspection / parity tests).
  * Pointers are device pointers owned by ctx, valid until the next load/build. */
 typedef struct {

@@ -500,6 +500,43 @@ def plan_direction(q):
             "pi": pi, "tree": tree, "closing": closing, "paths": {}}
 
 
+def keep_sets(q, plan=None, back_edges=False):
+    """Query-dependent LSpM (§6.2, "Read necessary RDF triples where
+    predicates appear in the queries"; Ex. 6.4 P:L436-L448: the CSR keeps the
+    predicates evaluated along their direction, the CSC those evaluated
+    against it): the labels each format must hold for the schedule and the
+    trie of `plan`, as (csr, csc) sorted lists:
+      seed (c -l-> v): c's CSR row; (v -l-> c): c's CSC row; guard: CSR;
+      a variable's 2nd+ seed, tested in v's row: (c -l-> v) CSC, (v -l-> c) CSR;
+      group edge (and back edge): OUT -> CSR, IN -> CSC;
+      trie tree edge: parent's row, OUT -> CSR, IN -> CSC;
+      closing edge: the subject's CSR row."""
+    plan = plan or plan_degree(q)
+    csr, csc = set(), set()
+    is_c = [q.is_const(i) for i in range(q.n_vertices)]
+    seeded = {}
+    for k in plan["seeds"]:
+        a, l, b = q.edges[k]
+        if is_c[a] and is_c[b]:
+            csr.add(l)
+        elif is_c[a]:
+            (csc if b in seeded else csr).add(l)
+            seeded.setdefault(b, k)
+        else:
+            (csr if a in seeded else csc).add(l)
+            seeded.setdefault(a, k)
+    back = plan.get("back") if back_edges else None
+    for gi, (x, grp) in enumerate(plan["groups"]):
+        for k, d, w in list(grp) + (list(back[gi]) if back else []):
+            (csr if d == OUT else csc).add(q.edges[k][1])
+    for v, (k, parent, d) in plan["tree"].items():
+        (csr if d == OUT else csc).add(q.edges[k][1])
+    for v, cl in plan["closing"].items():
+        for k, _, _ in cl:
+            csr.add(q.edges[k][1])
+    return sorted(csr), sorted(csc)
+
+
 # --------------------------------------------------------------------------
 # Filter schedule: seeds (light edges, P:L279/P:L397), then every group center
 # in plan order is "revised" against all its incident patterns (§5 Eqs. 17/21

@@ -281,6 +281,7 @@ struct Exec {
   }
   std::vector<std::vector<uint8_t>> push_dec;  // per group, per edge of gedges: push form (label-major)
   uint64_t push_and = 0;               // k_and_tracked launches (bitmap bytes)
+  uint64_t n_exchanges = 0;            // candidate-bitmap exchanges (world > 1: one per group evaluation)
   std::vector<uint32_t> group_seq;     // per group: sequence of its last evaluation
   int attempts = 0;
   bool seq_open = false;        // a look-back launch sequence was started (end it in finalize)
@@ -588,10 +589,7 @@ struct Exec {
   // baseline): an all-gather of the ranks' slices (variable sizes).
   gsmart_status exchange_center(const Group& g) {
     if (ctx->world == 1 && !ctx->comm) return GSMART_OK;
-    uint64_t other = 0;
-    for (int q = 0; q < ctx->world; q++)
-      if (q != ctx->rank) other += part_word_hi(ctx, q) - part_word_lo(ctx, q);
-    if (ctx->world > 1) R->stats.allgather_bytes += 4 * other;
+    n_exchanges++;
     if (peer_mode()) return rank_barrier();
     prof.begin(K_COLLECTIVE);
     TRY(coll_allgatherv(ctx, sl.st, cand(g.center)));
@@ -639,6 +637,8 @@ struct Exec {
         d.self = c.other_level == k ? 1u : 0u;
       }
       a.par_idx = a.tree ? anc_index(k, Lv.parent_level) : ANC_WALK;
+      // closing checks in the subject's CSR row when the formats hold different labels
+      a.closing_csr = (!ctx->f[1].built || ctx->keep[0] != ctx->keep[1]) ? 1 : 0;
       a.use_tma = ctx->use_tma ? 1 : 0;
       for (size_t i = 0; i < anc_cols[k - 1].size(); i++) a.par_anc[i] = sl.lv[k - 1].anc[i];
       a.n_anc_out = (uint32_t)anc_cols[k].size();
@@ -837,6 +837,7 @@ struct Exec {
       for (int i = 0; i < GSMART_NKERNELS; i++) launches[i] += it->second.launches[i];
       filter_main += it->second.filter_main;
       push_and += it->second.push_and;
+      n_exchanges += it->second.n_exchanges;
       return GSMART_OK;
     }
     if (it != sl.graphs.end()) {
@@ -848,7 +849,7 @@ struct Exec {
     if (sl.seen.insert(key).second) return body();
     const uint32_t off0 = sl.seq_off, bar0 = sl.bar_off;
     const std::vector<int> l0(launches, launches + GSMART_NKERNELS);
-    const uint64_t fm0 = filter_main, pa0 = push_and;
+    const uint64_t fm0 = filter_main, pa0 = push_and, nx0 = n_exchanges;
     CU(cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal));
     gsmart_status s = body();
     cudaGraph_t graph = nullptr;
@@ -875,6 +876,7 @@ struct Exec {
     for (int i = 0; i < GSMART_NKERNELS; i++) ge.launches[i] = launches[i] - l0[i];
     ge.filter_main = filter_main - fm0;
     ge.push_and = push_and - pa0;
+    ge.n_exchanges = n_exchanges - nx0;
     if (sl.graphs.size() >= 512) {  // bounded cache
       for (auto& kv : sl.graphs) cudaGraphExecDestroy(kv.second.exec);
       sl.graphs.clear();
@@ -1260,6 +1262,12 @@ struct Exec {
     st.seed_entries = c[C_SEED];
     st.expand_entries = c[C_EXPAND];
     st.closing_checks = c[C_CLOSING];
+    if (ctx->world > 1) {  // each exchange brings every other rank's slice of the center's bitmap
+      uint64_t other = 0;
+      for (int q = 0; q < ctx->world; q++)
+        if (q != ctx->rank) other += part_word_hi(ctx, q) - part_word_lo(ctx, q);
+      st.allgather_bytes = 4 * other * n_exchanges;
+    }
     st.edges_evaluated = c[C_FILTER_MATCHED] + c[C_SEED] + c[C_EXPAND] + c[C_PUSH];
     const uint64_t pb = (uint64_t)ctx->pred_bytes;
     // algorithmic bytes: what each step must move
@@ -1303,10 +1311,19 @@ struct Exec {
   }
 };
 
-gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan) {
+gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan, uint32_t flags) {
   if (!plan) FAIL(GSMART_E_INVALID_ARG, "null plan");
   for (auto& e : plan->edges)
     if (e.pred > ctx->P) FAIL(GSMART_E_INVALID_ARG, "query predicate id > n_predicates");
+  // every label the plan reads must be held by that format (keep-sets)
+  std::set<uint32_t> acc[2];
+  plan_access(*plan, (flags & GSMART_BACK_EDGES) != 0, &acc[0], &acc[1]);
+  for (int f = 0; f < 2; f++)
+    if (ctx->f[f].built)
+      for (uint32_t l : acc[f])
+        if (l < ctx->keep[f].size() && !ctx->keep[f][l])
+          FAIL(GSMART_E_STATE, std::string("the plan reads predicate ") + std::to_string(l) + " in the " +
+                                   (f ? "CSC" : "CSR") + " LSpM, which the build did not keep");
   if (!ctx->f[1].built) {  // CSR-only LSpM: a direction-driven plan reading subject rows only
     bool ok = plan->traversal == GSMART_DIRECTION;
     for (auto& L : plan->levels) ok = ok && (L.tree_edge < 0 || L.dir == OUT);
@@ -1317,7 +1334,7 @@ gsmart_status check_plan(gsmart_ctx* ctx, const gsmart_plan_t* plan) {
 
 gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint32_t n, uint32_t flags,
                         gsmart_result** out) {
-  for (uint32_t i = 0; i < n; i++) TRY(check_plan(ctx, plans[i]));
+  for (uint32_t i = 0; i < n; i++) TRY(check_plan(ctx, plans[i], flags));
   // world > 1: collectives of one plan complete before the next plan starts (same
   // order on every rank), so a batch runs one plan at a time on slot 0
   const uint32_t ns = ctx->world > 1 ? 1u : std::min<uint32_t>(std::max<uint32_t>(n, 1), MAX_SLOTS);

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
   }
   const Fmt<PT> fsrc = fmt_of<PT>(a.f[a.dir & 1]);
   const Fmt<PT> f0 = fmt_of<PT>(a.f[0]), f1 = fmt_of<PT>(a.f[1]);
-  const bool csr_only = a.f[1].rp == nullptr;
+  const bool csr_only = a.closing_csr != 0 || a.f[1].rp == nullptr;
   const uint32_t F1 = (uint32_t)F + 1;
   unsigned long long n_exam = 0, n_close = 0;
   while (true) {

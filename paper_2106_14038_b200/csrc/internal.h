@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <functional>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -70,4 +71,6 @@ namespace gsm {
 gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_t* out, std::string* err,
                          const std::function<double(uint32_t, uint32_t)>* fanout = nullptr, bool csr_only = false);
 std::string describe_plan(const gsmart_plan_t& p);
+// labels the CSR / CSC LSpM must hold to execute p (query-dependent LSpM)
+void plan_access(const gsmart_plan_t& p, bool back_edges, std::set<uint32_t>* csr, std::set<uint32_t>* csc);
 }  // namespace gsm

@@ -297,6 +297,7 @@ struct ExpArgs2 {
   int anc_src[MAXANC];                     // column i of level k: ANC_BIND or an index into par_anc
   uint32_t* out_anc[MAXANC];
   int use_tma;                             // stage tile offsets with cp.async.bulk (off[] has >= 8 words of tail)
+  int closing_csr;                         // closing checks read the subject's CSR row (CSR-only or split keep-sets)
 };
 constexpr int ANC_BIND = -1, ANC_WALK = -2;
 // ids of set bits of bm[0, n_words) plus id_base

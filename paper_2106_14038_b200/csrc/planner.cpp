@@ -246,6 +246,35 @@ gsmart_status build_plan(const gsmart_query* q, uint32_t traversal, gsmart_plan_
   return GSMART_OK;
 }
 
+// Labels each LSpM format must hold to execute plan p (query-
+// dependent LSpM, P:L408 / Ex. 6.4): seeds read the constant's row (CSR for
+// (c -l-> v), CSC for (v -l-> c)); a variable's later seeds and the group edges
+// read the center's row (OUT: CSR, IN: CSC); tree edges the parent's row;
+// closing edges the subject's CSR row (the executor's choice when the formats
+// keep different labels).
+void plan_access(const gsmart_plan_t& p, bool back_edges, std::set<uint32_t>* csr, std::set<uint32_t>* csc) {
+  std::vector<bool> seeded(p.n_vertices, false);
+  for (const auto& g : p.guards) csr->insert(g.label);
+  std::vector<const Seed*> order;
+  for (const auto& sd : p.seeds) order.push_back(&sd);
+  std::sort(order.begin(), order.end(), [](const Seed* a, const Seed* b) { return a->edge < b->edge; });
+  for (const Seed* sd : order) {
+    const bool first = !seeded[sd->var];
+    seeded[sd->var] = true;
+    if (sd->dir == OUT) (first ? csr : csc)->insert(sd->label);  // c -l-> v
+    else (first ? csc : csr)->insert(sd->label);                 // v -l-> c
+  }
+  for (const auto& g : p.groups) {
+    for (const auto& e : g.edges) (e.dir == OUT ? csr : csc)->insert(e.label);
+    if (back_edges)
+      for (const auto& e : g.back) (e.dir == OUT ? csr : csc)->insert(e.label);
+  }
+  for (const auto& L : p.levels) {
+    if (L.tree_edge >= 0) (L.dir == OUT ? csr : csc)->insert(L.label);
+    for (const auto& c : L.closing) csr->insert(c.label);
+  }
+}
+
 static void jarr(std::ostringstream& o, const std::vector<uint32_t>& v) {
   o << "[";
   for (size_t i = 0; i < v.size(); i++) o << (i ? "," : "") << v[i];

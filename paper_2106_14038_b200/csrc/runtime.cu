@@ -595,6 +595,31 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
   return GSMART_OK;
 }
 
+static gsmart_status keep_mask(gsmart_ctx* ctx, const uint32_t* ids, uint32_t n, bool all, std::vector<uint8_t>* out) {
+  out->assign(ctx->P + 1, all ? 1 : 0);
+  (*out)[0] = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    if (ids[i] == 0 || ids[i] > ctx->P) FAIL(GSMART_E_INVALID_ARG, "keep id out of range");
+    (*out)[ids[i]] = 1;
+  }
+  return GSMART_OK;
+}
+
+static gsmart_status build_lspm_masks(gsmart_ctx* ctx, const std::vector<uint8_t>& kcsr,
+                                      const std::vector<uint8_t>& kcsc, uint32_t formats);
+
+extern "C" gsmart_status gsmart_build_lspm_split(gsmart_ctx* ctx, const uint32_t* keep_csr, uint32_t n_csr,
+                                                 const uint32_t* keep_csc, uint32_t n_csc) {
+  if (!ctx) return GSMART_E_INVALID_ARG;
+  if (ctx->poisoned) return GSMART_E_CUDA;
+  if (ctx->N == 0) FAIL(GSMART_E_STATE, "gsmart_load_triples must be called first");
+  if ((n_csr && !keep_csr) || (n_csc && !keep_csc)) FAIL(GSMART_E_INVALID_ARG, "null keep set");
+  std::vector<uint8_t> kcsr, kcsc;
+  TRY(keep_mask(ctx, keep_csr, n_csr, false, &kcsr));
+  TRY(keep_mask(ctx, keep_csc, n_csc, false, &kcsc));
+  return build_lspm_masks(ctx, kcsr, kcsc, GSMART_CSR | GSMART_CSC);
+}
+
 extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep_preds, uint32_t n_keep,
                                            uint32_t formats) {
   if (!ctx) return GSMART_E_INVALID_ARG;
@@ -602,18 +627,27 @@ extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep
   if (ctx->N == 0) FAIL(GSMART_E_STATE, "gsmart_load_triples must be called first");
   if (formats == 0 || (formats & ~(GSMART_CSR | GSMART_CSC))) FAIL(GSMART_E_INVALID_ARG, "formats must be CSR|CSC");
   if (n_keep && !keep_preds) FAIL(GSMART_E_INVALID_ARG, "null keep_preds");
+  std::vector<uint8_t> keep;
+  TRY(keep_mask(ctx, keep_preds, n_keep, n_keep == 0, &keep));
+  return build_lspm_masks(ctx, keep, keep, formats);
+}
+
+static gsmart_status build_lspm_masks(gsmart_ctx* ctx, const std::vector<uint8_t>& kcsr,
+                                      const std::vector<uint8_t>& kcsc, uint32_t formats) {
   CU(cudaSetDevice(ctx->cfg.device));
-  std::vector<uint8_t> keep(ctx->P + 1, n_keep ? 0 : 1);
-  keep[0] = 0;
-  for (uint32_t i = 0; i < n_keep; i++) {
-    if (keep_preds[i] == 0 || keep_preds[i] > ctx->P) FAIL(GSMART_E_INVALID_ARG, "keep_preds id out of range");
-    keep[keep_preds[i]] = 1;
-  }
+  std::vector<uint8_t> keep(kcsr.size());
+  for (size_t i = 0; i < keep.size(); i++) keep[i] = kcsr[i] | kcsc[i];  // label-major lists, partition
   free_lspm(ctx);
+  ctx->keep[0] = kcsr;
+  ctx->keep[1] = kcsc;
   Scratch sc(ctx);
-  uint8_t* d_keep = nullptr;
+  uint8_t *d_keep = nullptr, *d_kf[2] = {nullptr, nullptr};
   TRY(sc.get(&d_keep, keep.size()));
   CU(cudaMemcpyAsync(d_keep, keep.data(), keep.size(), cudaMemcpyHostToDevice, ctx->st));
+  for (int f = 0; f < 2; f++) {
+    TRY(sc.get(&d_kf[f], keep.size()));
+    CU(cudaMemcpyAsync(d_kf[f], (f ? kcsc : kcsr).data(), keep.size(), cudaMemcpyHostToDevice, ctx->st));
+  }
   static const bool trace = getenv("GSMART_TRACE") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
@@ -626,7 +660,7 @@ extern "C" gsmart_status gsmart_build_lspm(gsmart_ctx* ctx, const uint32_t* keep
   if (ctx->world > 1) TRY(compute_partition(ctx, d_keep));
   lap("partition");
   for (int fmt = 0; fmt < 2; fmt++) {
-    if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_keep));
+    if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_kf[fmt]));
     lap(fmt == 0 ? "csr" : "csc");
   }
   if (formats == (GSMART_CSR | GSMART_CSC)) {
@@ -680,6 +714,24 @@ extern "C" gsmart_status gsmart_plan(gsmart_ctx* ctx, const gsmart_query* q, uin
     return s;
   }
   *out = p.release();
+  return GSMART_OK;
+}
+
+extern "C" gsmart_status gsmart_plan_keep_sets(const gsmart_plan_t* const* plans, uint32_t n, uint32_t flags,
+                                               uint32_t* csr_out, uint32_t* n_csr, uint32_t* csc_out, uint32_t* n_csc,
+                                               uint32_t cap) {
+  if ((n && !plans) || !n_csr || !n_csc || (cap && (!csr_out || !csc_out))) return GSMART_E_INVALID_ARG;
+  std::set<uint32_t> a, b;
+  for (uint32_t i = 0; i < n; i++) {
+    if (!plans[i]) return GSMART_E_INVALID_ARG;
+    plan_access(*plans[i], (flags & GSMART_BACK_EDGES) != 0, &a, &b);
+  }
+  *n_csr = (uint32_t)a.size();
+  *n_csc = (uint32_t)b.size();
+  uint32_t i = 0;
+  for (uint32_t l : a) if (i < cap) csr_out[i++] = l;
+  i = 0;
+  for (uint32_t l : b) if (i < cap) csc_out[i++] = l;
   return GSMART_OK;
 }
 

@@ -157,7 +157,7 @@ struct Slot {
     uint64_t ws_gen = 0, lspm_gen = 0;
     uint32_t flags = 0, n_lb = 0, off0 = 0, n_bar = 0, bar0 = 0;
     std::vector<int> launches;  // kernel launches inside the graph, per kernel class
-    uint64_t filter_main = 0, push_and = 0;
+    uint64_t filter_main = 0, push_and = 0, n_exchanges = 0;
   };
   std::unordered_map<uint64_t, GraphEntry> graphs;  // (plan uid << 3 | phase tag) -> captured work
   std::unordered_set<uint64_t> seen;                // keys run once without capture
@@ -244,6 +244,7 @@ struct gsmart_ctx {
   uint32_t *d_s = nullptr, *d_p = nullptr, *d_o = nullptr;
   int pred_bytes = 1;
   gsm::Lspm f[2];
+  std::vector<uint8_t> keep[2];  // labels each format holds (P + 1 flags) since the last build
   gsm::LabelMajor lm;
   gsm::LabelMajor lm_in;     // world > 1: label-major entries whose OBJECT is this rank's (stored as (o, s))
   gsm::Partition part;       // world > 1: vertex ranges of the ranks

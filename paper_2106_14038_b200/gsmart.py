@@ -93,6 +93,9 @@ def _load():
         "gsmart_last_error": (ctypes.c_char_p, [vp]),
         "gsmart_load_triples": (st, [vp, vp, vp, vp, u64, u32, u32, u32]),
         "gsmart_build_lspm": (st, [vp, vp, u32, u32]),
+        "gsmart_build_lspm_split": (st, [vp, vp, u32, vp, u32]),
+        "gsmart_plan_keep_sets": (st, [ctypes.POINTER(vp), u32, u32, vp, ctypes.POINTER(u32), vp,
+                                       ctypes.POINTER(u32), u32]),
         "gsmart_lspm_get": (st, [vp, u32, ctypes.POINTER(gsmart_lspm_view)]),
         "gsmart_plan": (st, [vp, ctypes.POINTER(gsmart_query), u32, ctypes.POINTER(vp)]),
         "gsmart_plan_describe": (st, [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
@@ -124,7 +127,8 @@ def _load():
 
 _lib = _load()
 EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gsmart_create", "gsmart_destroy",
-            "gsmart_last_error", "gsmart_load_triples", "gsmart_build_lspm", "gsmart_lspm_get", "gsmart_plan",
+            "gsmart_last_error", "gsmart_load_triples", "gsmart_build_lspm", "gsmart_build_lspm_split",
+            "gsmart_plan_keep_sets", "gsmart_lspm_get", "gsmart_plan",
             "gsmart_plan_describe", "gsmart_plan_free", "gsmart_execute", "gsmart_execute_batch",
             "gsmart_result_shape",
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
@@ -259,6 +263,26 @@ def gsmart_build_lspm(ctx, keep=None, formats=GSMART_CSR | GSMART_CSC):
     keep = np.ascontiguousarray(np.asarray([] if keep is None else keep, dtype=np.uint32))
     ptr = keep.ctypes.data if len(keep) else None
     _check(_lib.gsmart_build_lspm(ctx, ptr, len(keep), formats), ctx)
+
+
+def gsmart_build_lspm_split(ctx, keep_csr, keep_csc):
+    """Query-dependent LSpM: the CSR keeps keep_csr, the CSC keep_csc (predicate ids)."""
+    a = np.ascontiguousarray(np.asarray(list(keep_csr), dtype=np.uint32))
+    b = np.ascontiguousarray(np.asarray(list(keep_csc), dtype=np.uint32))
+    _check(_lib.gsmart_build_lspm_split(ctx, a.ctypes.data if len(a) else None, len(a),
+                                        b.ctypes.data if len(b) else None, len(b)), ctx)
+
+
+def gsmart_plan_keep_sets(plans, flags=0):
+    """(csr, csc): the predicate ids each format must keep to execute the plans."""
+    n = len(plans)
+    arr = (ctypes.c_void_p * max(n, 1))(*[p.value if isinstance(p, ctypes.c_void_p) else p for p in plans])
+    cap = 70000
+    a = (ctypes.c_uint32 * cap)()
+    b = (ctypes.c_uint32 * cap)()
+    na, nb = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.gsmart_plan_keep_sets(arr, n, flags, a, ctypes.byref(na), b, ctypes.byref(nb), cap))
+    return [a[i] for i in range(na.value)], [b[i] for i in range(nb.value)]
 
 
 def gsmart_lspm_get(ctx, fmt):

@@ -133,6 +133,29 @@ def test_direction_plan_parity_with_oracle_planner(G, golden_fig):
     assert c["roots"] == golden_fig["ex61_roots"]
 
 
+def test_keep_sets_ex64_and_oracle(G, golden_fig):
+    """Query-dependent LSpM (§6.2, f3): the labels each format must keep for a
+    plan == the oracle's keep_sets; for Fig. 2 they are Ex. 6.4's
+    direction-split keep-sets (CSR {follows, actor}, CSC {director, follows})."""
+    P = fixtures.PREDICATE_IDS
+    h = G.gsmart_plan(None, fixtures.fig2_query())
+    try:
+        csr, csc = G.gsmart_plan_keep_sets([h])
+    finally:
+        G.gsmart_plan_free(h)
+    assert csr == sorted(P[x] for x in golden_fig["ex64_csr"]["keep"])
+    assert csc == sorted(P[x] for x in golden_fig["ex64_csc"]["keep"])
+    for seed in range(300):
+        q = tiny.random_case(seed)[3]
+        for back in (False, True):
+            h = G.gsmart_plan(None, q)
+            try:
+                got = G.gsmart_plan_keep_sets([h], G.GSMART_BACK_EDGES if back else 0)
+            finally:
+                G.gsmart_plan_free(h)
+            assert tuple(got) == R.keep_sets(q, back_edges=back), (seed, q, back)
+
+
 def test_plan_errors(G):
     with pytest.raises(G.GsmartError) as e:
         G.gsmart_plan(None, Query((None,), ((0, 1, 1),)))       # vertex out of range

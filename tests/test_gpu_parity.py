@@ -175,6 +175,47 @@ def test_random_tiny_rows_and_candidates(G, eng, chunk):
                 assert got == set(np.nonzero(ref[v])[0].tolist()), (seed, v, q, flags)
 
 
+# ------------------------------------------------------------------ query-dependent LSpM (f3)
+def test_split_keep_sets(G, golden_fig):
+    """Direction-split keep-sets (§6.2, Ex. 6.4): built with the sets a batch of
+    plans needs, the CSR/CSC hold only their labels (Fig. 1: 6 and 9 entries,
+    R20), rows == oracle on the full triple set; a plan reading a label a
+    format dropped is refused (E_STATE)."""
+    from synth import lubm
+    e = G.Engine(0)
+    try:
+        s, p, o = fixtures.fig1_triples()
+        q = fixtures.fig2_query()
+        G.gsmart_load_triples(e.ctx, s, p, o, 8, 4)
+        h = G.gsmart_plan(None, q)
+        csr, csc = G.gsmart_plan_keep_sets([h])
+        G.gsmart_plan_free(h)
+        G.gsmart_build_lspm_split(e.ctx, csr, csc)
+        assert G.gsmart_lspm_get(e.ctx, G.GSMART_CSR)["nnz"] == golden_fig["ex64_csr"]["nnz"]
+        assert G.gsmart_lspm_get(e.ctx, G.GSMART_CSC)["nnz"] == golden_fig["ex64_csc"]["nnz"]
+        assert _rows(e.query(q)) == [tuple(r) for r in golden_fig["solution_rows"]]
+        d = lubm.generate(5)
+        s, p, o = d.s.numpy(), d.p.numpy(), d.o.numpy()
+        qs = lubm.queries(d)
+        G.gsmart_load_triples(e.ctx, s, p, o, d.n_entities, d.n_predicates)
+        plans = [G.gsmart_plan(None, q) for q in qs]
+        csr, csc = G.gsmart_plan_keep_sets(plans)
+        G.gsmart_build_lspm_split(e.ctx, csr, csc)
+        ix = OracleIndex(s, p, o)
+        for q, r in zip(qs, G.gsmart_execute_batch(e.ctx, plans, 0)):
+            assert np.array_equal(G.gsmart_result_rows(r), ix.query(q)), q.name
+            G.gsmart_result_free(r)
+        for pl in plans:
+            G.gsmart_plan_free(pl)
+        missing = sorted(set(range(1, d.n_predicates + 1)) - set(csr))
+        bad = Query((None, None), ((0, missing[0], 1),))
+        with pytest.raises(G.GsmartError) as ei:
+            e.query(bad)
+        assert ei.value.name == "E_STATE"
+    finally:
+        e.close()
+
+
 # ------------------------------------------------------------------ direction-driven plans (§6.1.1, f1)
 def test_direction_plans_rows_and_candidates(G, eng, golden_fig):
     """GSMART_DIRECTION (CSR-side groups, multi-root plans joined in one trie):
