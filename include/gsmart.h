@@ -308,6 +308,53 @@ void gsmart_result_free(gsmart_result* r);
  * of `bytes` from device memory `src_dev` (on ctx's device) into host `dst`. */
 gsmart_status gsmart_copy_to_host(gsmart_ctx* ctx, void* dst, const void* src_dev, size_t bytes);
 
+/* ------------------------------------------------------------------ f4: ingest
+ * N-Triples read + dictionary encode on the device (§6.2.1 steps 1-2,
+ * "Read ... RDF triples", "Encode RDF strings into numeric ids
+ * ... the index of subject and object is 0-based, the index of predicate is
+ * 1-based").
+ *
+ * Input subset (R24): lines split at '\n'; a line that is empty or
+ * whitespace (' ', '\t', '\r') or whose first non-blank byte is '#' is
+ * skipped; otherwise it holds S P O '.' with terms separated by spaces/tabs
+ * (none needed after an IRI): S = <IRI> | _:blank, P = <IRI>,
+ * O = <IRI> | _:blank | "literal" (backslash escapes) [@lang | ^^<IRI>].
+ * Only ' ', '\t', '\r' may follow the '.'.  A term is its exact bytes.
+ * Ids follow first appearance in file order, subject before object; entities
+ * from 0, predicates from 1 (R24).
+ *
+ * text: `bytes` bytes (flags GSMART_PTR_HOST or GSMART_PTR_DEVICE), not
+ * NUL-terminated; the context copies it (the dictionary's term bytes) and
+ * the caller may free it on return.  Loads the encoded triples exactly like
+ * gsmart_load_triples (replaces earlier data, invalidates the LSpM) and
+ * returns n_triples, n_entities, n_predicates (any out pointer may be NULL).
+ * A document without triples returns GSMART_OK with all three 0 and nothing
+ * loaded.  Errors: GSMART_E_INVALID_ARG "line L: ..." for the first malformed
+ * line L (0-based, counting every '\n'-separated line), nothing loaded;
+ * GSMART_E_UNSUPPORTED for > 2^31 - 1 triples, >= 2^31 entities, > 65534
+ * predicates, or a 64-bit term-hash collision between two distinct terms
+ * (detected exactly by byte comparison; the ids are never silently merged).
+ * world must be 1. */
+gsmart_status gsmart_ingest_ntriples(gsmart_ctx* ctx, const char* text, uint64_t bytes, uint32_t flags,
+                                     uint64_t* n_triples, uint32_t* n_entities, uint32_t* n_predicates);
+
+#define GSMART_DICT_ENTITY 0u
+#define GSMART_DICT_PREDICATE 1u
+/* Id of a term (exact bytes, `len` of them, host memory) in the dictionary of
+ * the last gsmart_ingest_ntriples: *id = entity id (kind ENTITY) or predicate
+ * id >= 1 (kind PREDICATE), or 0xFFFFFFFF when the term does not occur (an
+ * absent entity used as a query constant gives empty results, R12).
+ * GSMART_E_STATE when the loaded data did not come from an ingest. */
+gsmart_status gsmart_dict_lookup(gsmart_ctx* ctx, uint32_t kind, const char* term, uint64_t len, uint32_t* id);
+/* Bytes of term `id` (inverse of gsmart_dict_lookup) copied to host buf (at
+ * most cap bytes); *len = the full term length.  GSMART_E_INVALID_ARG for an
+ * id outside [0, n_entities) / [1, n_predicates]; GSMART_E_STATE as above. */
+gsmart_status gsmart_dict_term(gsmart_ctx* ctx, uint32_t kind, uint32_t id, char* buf, uint64_t cap, uint64_t* len);
+/* Device pointers to the loaded (s, p, o) arrays (n entries each, uint32,
+ * context-owned, valid until the next load/ingest or gsmart_destroy). */
+gsmart_status gsmart_triples_get(const gsmart_ctx* ctx, const uint32_t** s, const uint32_t** p, const uint32_t** o,
+                                 uint64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -206,7 +206,7 @@ gsmart_status gsm::ctx_sync(gsmart_ctx* ctx) {
   return GSMART_OK;
 }
 
-static void free_lspm(gsmart_ctx* ctx) {
+void gsm::free_lspm(gsmart_ctx* ctx) {
   for (auto& f : ctx->f) {
     if (f.sym) {
       cudaStreamSynchronize(ctx->st);
@@ -239,6 +239,7 @@ extern "C" void gsmart_destroy(gsmart_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   slots_free(ctx);
   free_lspm(ctx);
+  dict_free(ctx);
   dfree(ctx, ctx->d_s);
   dfree(ctx, ctx->d_p);
   dfree(ctx, ctx->d_o);
@@ -277,6 +278,7 @@ extern "C" gsmart_status gsmart_load_triples(gsmart_ctx* ctx, const uint32_t* s,
   if (flags != GSMART_PTR_HOST && flags != GSMART_PTR_DEVICE) FAIL(GSMART_E_INVALID_ARG, "flags must be PTR_HOST or PTR_DEVICE");
   CU(cudaSetDevice(ctx->cfg.device));
   free_lspm(ctx);
+  dict_free(ctx);
   dfree(ctx, ctx->d_s);
   dfree(ctx, ctx->d_p);
   dfree(ctx, ctx->d_o);

@@ -76,6 +76,20 @@ struct LabelMajor {
 // both formats; split points balance out+in entries, aligned to 2^19 vertices
 // (2 MiB of row pointers: the granularity of a symmetric chunk)
 constexpr uint32_t PART_ALIGN_ROWS = 1u << 19;
+// f4 dictionary (ingest.cu): term bytes stay resident in `text`; per kind
+// (0 entity, 1 predicate) the (offset, length) of each id's term and the
+// sorted term hashes with their ids (lookups)
+struct Dict {
+  uint8_t* text = nullptr;
+  uint64_t bytes = 0;
+  bool valid = false;
+  uint32_t n[2] = {0, 0};
+  uint64_t* off[2] = {nullptr, nullptr};
+  uint32_t* len[2] = {nullptr, nullptr};
+  uint64_t* hash[2] = {nullptr, nullptr};
+  uint32_t* hid[2] = {nullptr, nullptr};
+};
+
 struct Partition {
   std::vector<uint32_t> v;  // world + 1 split points
 };
@@ -248,6 +262,7 @@ struct gsmart_ctx {
   gsm::LabelMajor lm;
   gsm::LabelMajor lm_in;     // world > 1: label-major entries whose OBJECT is this rank's (stored as (o, s))
   gsm::Partition part;       // world > 1: vertex ranges of the ranks
+  gsm::Dict dict;            // f4: terms of the last gsmart_ingest_ntriples
   std::unique_ptr<gsm::SockChan> chan;  // world > 1, ranks are processes
   uint32_t exchange = GSMART_XCHG_PEER;
   bool use_tma = true;        // GSMART_NO_TMA=1: plain loads instead of cp.async.bulk staging (A/B)
@@ -370,6 +385,10 @@ gsmart_status readback(gsmart_ctx* ctx, cudaStream_t st, unsigned long long* h_p
                        int n, unsigned long long* host);
 
 void slots_free(gsmart_ctx* ctx);
+// ingest.cu: release the dictionary (new data loaded, or destroy)
+void dict_free(gsmart_ctx* ctx);
+// runtime.cu: release both LSpM formats and the label-major lists
+void free_lspm(gsmart_ctx* ctx);
 // wait for every stream of this context (ranks sharing a device never wait on each other's streams)
 gsmart_status ctx_sync(gsmart_ctx* ctx);
 

@@ -36,6 +36,7 @@ class GsmartError(RuntimeError):
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 GSMART_XCHG_PEER, GSMART_XCHG_NCCL = 0, 1
+GSMART_DICT_ENTITY, GSMART_DICT_PREDICATE = 0, 1
 
 
 class gsmart_config(ctypes.Structure):
@@ -117,6 +118,12 @@ def _load():
         "gsmart_partition_split": (st, [ctypes.POINTER(u64), u32, u32, ctypes.c_int, ctypes.POINTER(u32)]),
         "gsmart_partition_get": (st, [vp, ctypes.POINTER(u32)]),
         "gsmart_rendezvous_check": (st, [vp, ctypes.c_int, ctypes.c_int, u64, ctypes.POINTER(u64)]),
+        "gsmart_ingest_ntriples": (st, [vp, vp, u64, u32, ctypes.POINTER(u64), ctypes.POINTER(u32),
+                                        ctypes.POINTER(u32)]),
+        "gsmart_dict_lookup": (st, [vp, u32, ctypes.c_char_p, u64, ctypes.POINTER(u32)]),
+        "gsmart_dict_term": (st, [vp, u32, u32, vp, u64, ctypes.POINTER(u64)]),
+        "gsmart_triples_get": (st, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                    ctypes.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -134,7 +141,8 @@ EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gs
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
             "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host",
             "gsmart_comm_create_local", "gsmart_comm_destroy", "gsmart_partition_split", "gsmart_partition_get",
-            "gsmart_rendezvous_check"]
+            "gsmart_rendezvous_check", "gsmart_ingest_ntriples", "gsmart_dict_lookup", "gsmart_dict_term",
+            "gsmart_triples_get"]
 
 
 def lib():
@@ -420,6 +428,53 @@ def gsmart_copy_to_host(ctx, dev_ptr, nbytes, dtype=np.uint32):
     if nbytes:
         _check(_lib.gsmart_copy_to_host(ctx, out.ctypes.data, dev_ptr, nbytes), ctx)
     return out
+
+
+def gsmart_ingest_ntriples(ctx, text):
+    """Parse + dictionary-encode an N-Triples document on the device and load
+    it (f4).  text: bytes / bytearray / numpy uint8 (host) or a CUDA uint8
+    tensor.  Returns (n_triples, n_entities, n_predicates)."""
+    kind, keep = GSMART_PTR_HOST, None
+    try:
+        import torch
+        if isinstance(text, torch.Tensor):
+            if text.dtype != torch.uint8:
+                raise TypeError("text tensor must be uint8")
+            keep = text.contiguous()
+            ptr, n = keep.data_ptr(), keep.numel()
+            kind = GSMART_PTR_DEVICE if keep.is_cuda else GSMART_PTR_HOST
+    except ImportError:
+        pass
+    if keep is None:
+        keep = np.frombuffer(text, dtype=np.uint8) if isinstance(text, (bytes, bytearray, memoryview)) \
+            else np.ascontiguousarray(text, dtype=np.uint8)
+        ptr, n = (keep.ctypes.data if keep.size else None), keep.size
+    nt, ne, npr = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.gsmart_ingest_ntriples(ctx, ptr, n, kind, ctypes.byref(nt), ctypes.byref(ne), ctypes.byref(npr)), ctx)
+    return nt.value, ne.value, npr.value
+
+
+def gsmart_dict_lookup(ctx, kind, term):
+    """Id of a term (bytes) or 0xFFFFFFFF when absent."""
+    out = ctypes.c_uint32()
+    _check(_lib.gsmart_dict_lookup(ctx, kind, bytes(term), len(term), ctypes.byref(out)), ctx)
+    return out.value
+
+
+def gsmart_dict_term(ctx, kind, term_id):
+    """Bytes of the term with this id."""
+    n = ctypes.c_uint64()
+    _check(_lib.gsmart_dict_term(ctx, kind, term_id, None, 0, ctypes.byref(n)), ctx)
+    buf = ctypes.create_string_buffer(max(n.value, 1))
+    _check(_lib.gsmart_dict_term(ctx, kind, term_id, buf, n.value, ctypes.byref(n)), ctx)
+    return buf.raw[:n.value]
+
+
+def gsmart_triples_get(ctx):
+    """Host copies of the loaded (s, p, o) id arrays."""
+    s, p, o, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+    _check(_lib.gsmart_triples_get(ctx, ctypes.byref(s), ctypes.byref(p), ctypes.byref(o), ctypes.byref(n)), ctx)
+    return tuple(gsmart_copy_to_host(ctx, a.value, 4 * n.value) for a in (s, p, o))
 
 
 # ------------------------------------------------------------------------ convenience
