@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define GSMART_ABI_VERSION 2
+#define GSMART_ABI_VERSION 3
 
 typedef enum {
   GSMART_OK = 0,
@@ -79,6 +79,15 @@ typedef enum {
 #define GSMART_BACK_EDGES 128u    /* every evaluation of a group also tests the center's already-evaluated patterns
                                      against the earlier centers' bitmaps (Eq. 16 over Eq. 14 binding vectors,
                                      DESIGN.md R-back): tighter candidate sets, more work per group */
+#define GSMART_FACTORISED 256u    /* f2: factorised binding trees (§7.1, per-path trees that
+                                     share their DFS prefix) instead of the prefix trie: one level per occurrence of
+                                     a variable, hanging off its tree parent's level; a pattern that closes onto a
+                                     non-parent vertex adds a second occurrence of the variable and Ω pruning
+                                     (§8.1) intersects its bindings per root binding; the rows are
+                                     enumerated from the pruned trees (combination index -> one node per
+                                     occurrence, Ω occurrences equal) and sorted.  COUNT_ONLY without Ω variables
+                                     reads the count off the trees (no enumeration).  Same rows as the trie.
+                                     world > 1: GSMART_E_UNSUPPORTED.  See gsmart_result_tree. */
 
 typedef struct gsmart_ctx gsmart_ctx;
 typedef struct gsmart_plan_s gsmart_plan_t;
@@ -280,6 +289,21 @@ gsmart_status gsmart_result_level(const gsmart_result* r, uint32_t k, uint32_t* 
                                   uint64_t* n, const uint32_t** parent_dev,
                                   const uint32_t** bind_dev);
 
+/* Level k of the result's tree form.  Trie (default): as gsmart_result_level,
+ * *parent_level = k - 1 (-1 for k = 0), *alive_dev = NULL (every node alive).
+ * GSMART_FACTORISED: occurrence k of the factorised binding trees (§7.1,
+ * P:L516) — *parent_level = the occurrence its nodes hang off (-1 for the
+ * root occurrence), parent[i] indexes that occurrence's nodes, children of a
+ * node are contiguous; alive_dev[i] (uint8) = 1 iff node i survived pre-,
+ * bottom-up and Ω pruning; *vertex = the variable (a second occurrence repeats
+ * it).  The solutions are, per alive root node, every choice of one alive
+ * node per occurrence consistent with the parent links and with equal
+ * bindings at every occurrence of a variable.  Device memory owned by the
+ * result. */
+gsmart_status gsmart_result_tree(const gsmart_result* r, uint32_t k, uint32_t* vertex, int32_t* parent_level,
+                                 uint64_t* n, const uint32_t** parent_dev, const uint32_t** bind_dev,
+                                 const uint8_t** alive_dev);
+
 #define GSMART_MAX_LEVELS 32
 #define GSMART_NKERNELS 16
 typedef struct {
@@ -299,6 +323,9 @@ typedef struct {
   uint64_t allgather_bytes;     /* world > 1 */
   uint32_t spec_phase2;         /* 1: phase 2 (prune, rows) was queued speculatively behind phase 1 */
   uint32_t spec_redo;           /* 1: the speculation guessed wrong sizes; phase 2 was redone */
+  uint32_t factorised;          /* 1: GSMART_FACTORISED (levels = occurrences, see gsmart_result_tree) */
+  uint32_t n_omega;             /* factorised: second occurrences (Ω) */
+  uint64_t combinations;        /* factorised: combinations of the pruned trees (= n_rows when n_omega == 0) */
   const char* kernel_names[GSMART_NKERNELS];
 } gsmart_stats;
 gsmart_status gsmart_result_stats(const gsmart_result* r, gsmart_stats* out);

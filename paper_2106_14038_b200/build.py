@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["kernels.cu", "expand.cu", "runtime.cu", "execute.cu", "comm.cu", "planner.cpp", "nccl_shim.cpp", "hostio.cu", "radix.cu", "symheap.cu", "ingest.cu"]
+SOURCES = ["kernels.cu", "expand.cu", "runtime.cu", "execute.cu", "comm.cu", "planner.cpp", "nccl_shim.cpp", "hostio.cu", "radix.cu", "symheap.cu", "ingest.cu", "factorised.cu"]
 
 
 def _needs(src, obj):

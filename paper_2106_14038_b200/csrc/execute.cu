@@ -292,6 +292,91 @@ struct Exec {
   std::vector<uint64_t> F;
   std::chrono::steady_clock::time_point t0;
 
+  // ---- f2: factorised binding trees (GSMART_FACTORISED; §7.1, §8.1).
+  // One level per occurrence of a variable: the trie level's variable hangs off
+  // its tree parent's occurrence (not off the previous trie level), and each
+  // closing pattern onto a non-parent earlier level adds a second occurrence of
+  // the variable under that level (the paper's per-path trees: a variable on
+  // two paths, Ω).  Self-loops and patterns parallel to the tree edge stay
+  // closing checks of the occurrence (target = the parent binding).
+  struct Occ {
+    uint32_t var = 0;
+    int par = -1;       // parent occurrence (-1: root)
+    bool tree = true;   // false: a free level (children = the candidate list), under the root
+    uint32_t label = 0, dir = 0;  // tree edge; dir seen from the parent (OUT: the parent is the subject)
+    std::vector<ClosingDev> cl;
+    std::vector<int> cl_idx;
+    int col = -1;       // output column (first occurrence), -1 for a second occurrence
+    int same = -1;      // second occurrence: the first occurrence of its variable
+  };
+  bool fact = false;
+  std::vector<Occ> occ;
+  uint32_t n_omega = 0;
+  gsmart_status build_occurrences() {
+    const uint32_t LT = (uint32_t)plan->levels.size();
+    std::vector<int> of_var(plan->n_vertices, -1);
+    std::vector<int> center_of(plan->edges.size(), -1);  // the group that evaluated each pattern
+    for (auto& g : plan->groups)
+      for (auto& e : g.edges) center_of[e.edge] = (int)g.center;
+    occ.clear();
+    n_omega = 0;
+    // (center, other variable) -> the patterns between them that close onto a non-parent level
+    std::map<std::pair<uint32_t, uint32_t>, std::vector<uint32_t>> cross;
+    for (uint32_t k = 0; k < LT; k++) {
+      const Level& Lv = plan->levels[k];
+      Occ o;
+      o.var = Lv.var;
+      o.col = plan->col_of[Lv.var];
+      o.tree = k > 0 && Lv.tree_edge >= 0;
+      const uint32_t plev = o.tree ? Lv.parent_level : 0;
+      if (k > 0) {
+        o.par = of_var[plan->levels[plev].var];
+        o.label = Lv.label;
+        o.dir = Lv.dir;
+      }
+      for (auto& c : Lv.closing) {
+        if (c.other_level == k) {
+          if (k > 0) {  // the root level's self-loops are exact in its candidate set
+            o.cl.push_back({c.label, k, c.dir == OUT ? 0u : 1u, 1u});
+            o.cl_idx.push_back(ANC_WALK);
+          }
+        } else if (k > 0 && c.other_level == plev) {
+          o.cl.push_back({c.label, plev, c.dir == OUT ? 0u : 1u, 0u});
+          o.cl_idx.push_back(ANC_BIND);
+        } else {
+          // the path of the pattern's center continues to the other endpoint (P:L516,
+          // Ex. 7.1 "v2 -> v0 -> v1"): a second occurrence of that variable under the center
+          const uint32_t other = plan->levels[c.other_level].var;
+          const int ctr = center_of[c.edge] >= 0 ? center_of[c.edge] : (int)other;
+          const uint32_t dupv = (uint32_t)ctr == Lv.var ? other : Lv.var;
+          cross[{(uint32_t)ctr, dupv}].push_back(c.edge);
+        }
+      }
+      of_var[Lv.var] = (int)occ.size();
+      occ.push_back(o);
+    }
+    for (auto& kv : cross) {
+      const uint32_t ctr = kv.first.first, v = kv.first.second;
+      Occ d;
+      d.var = v;
+      d.par = of_var[ctr];
+      const gsmart_qedge& e0 = plan->edges[kv.second[0]];
+      d.label = e0.pred;
+      d.dir = e0.src == ctr ? (uint32_t)OUT : (uint32_t)IN;  // seen from the center
+      for (size_t i = 1; i < kv.second.size(); i++) {
+        const gsmart_qedge& e = plan->edges[kv.second[i]];
+        d.cl.push_back({e.pred, (uint32_t)d.par, e.src == v ? 0u : 1u, 0u});  // seen from the new child
+        d.cl_idx.push_back(ANC_BIND);
+      }
+      d.same = of_var[v];
+      occ.push_back(d);
+      n_omega++;
+    }
+    if (occ.size() > (size_t)MAXOCC || occ.size() > (size_t)GSMART_MAX_LEVELS)
+      FAIL(GSMART_E_UNSUPPORTED, "GSMART_FACTORISED: more than 32 occurrences");
+    return GSMART_OK;
+  }
+
   Exec(gsmart_ctx* c, Slot& s, const gsmart_plan_t* p, uint32_t fl, gsmart_result* r)
       : ctx(c), sl(s), plan(p), flags(fl), R(r), prof(s.st, &r->stats, (fl & GSMART_PROFILE) != 0), sc(c, s.st) {
     t0 = std::chrono::steady_clock::now();
@@ -601,6 +686,7 @@ struct Exec {
   // ---- a5/a6/a7: one expansion attempt over all levels (async), sizes -> pinned
   // fresh: sizes and overflow flags were zeroed by this execute's k_init_cands
   gsmart_status launch_expansion(bool fresh) {
+    if (fact) return launch_expansion_f(fresh);
     unsigned long long* dsz = sl.d_sz;
     if (!fresh) CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
     if (L > 1) CU(cudaMemsetAsync(sl.lv[0].alive, 0, sl.lv[0].cap, sl.st));
@@ -678,6 +764,294 @@ struct Exec {
       prof.end();
     }
     CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
+    return GSMART_OK;
+  }
+
+  // f2: level 0 as in the trie, then every occurrence from its parent occurrence
+  // (k_seg_scan + k_expand_lb unchanged: the parent level index p is passed as
+  // k - 1, so ANC_BIND reads the parent occurrence's bindings)
+  gsmart_status launch_expansion_f(bool fresh) {
+    unsigned long long* dsz = sl.d_sz;
+    if (!fresh) CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
+    prof.begin(K_COMPACT);
+    CU(launch_bitmap_compact_lb(cand(occ[0].var), W, sl.lv[0].bind, sl.lv[0].cap, dsz + 0, sl.d_ovf, next_lb(sl),
+                                ctx->sm_count, sl.st));
+    launches[K_COMPACT] += compact_launches(W);
+    prof.end();
+    for (uint32_t o = 1; o < L; o++) {
+      const Occ& oc = occ[o];
+      const uint32_t p = (uint32_t)oc.par;
+      ExpArgs2 a;
+      memset(&a, 0, sizeof a);
+      for (uint32_t j = 0; j < o; j++) {
+        a.tab.parent[j] = sl.lv[j].parent;
+        a.tab.bind[j] = sl.lv[j].bind;
+      }
+      a.k = p + 1;
+      a.d_nparent = dsz + p;
+      a.cap_par = sl.lv[p].cap;
+      a.tree = oc.tree ? 1 : 0;
+      a.parent_level = p;
+      a.label = oc.label;
+      a.dir = oc.dir == OUT ? 0 : 1;
+      a.f[0] = fa[0];
+      a.f[1] = fa[1];
+      a.cand = cand(oc.var);
+      for (size_t i = 0; i < oc.cl.size(); i++) {
+        a.cl[a.ncl] = oc.cl[i];
+        a.cl_idx[a.ncl++] = oc.cl_idx[i];
+      }
+      a.par_idx = ANC_BIND;
+      a.closing_csr = (!ctx->f[1].built || ctx->keep[0] != ctx->keep[1]) ? 1 : 0;
+      a.use_tma = ctx->use_tma ? 1 : 0;
+      if (!a.tree) {
+        prof.begin(K_COMPACT);
+        CU(launch_bitmap_compact_lb(cand(oc.var), W, sl.list[o], sl.list_cap[o], dsz + 64 + o, sl.d_ovf,
+                                    next_lb(sl), ctx->sm_count, sl.st));
+        launches[K_COMPACT] += compact_launches(W);
+        prof.end();
+        a.list = sl.list[o];
+        a.d_list_len = dsz + 64 + o;
+      }
+      a.seg_beg = sl.lv[p].seg_beg;
+      a.off = sl.lv[p].off;
+      a.tile_start = sl.tile_start;
+      a.d_T = dsz + 32 + o;
+      a.out_parent = sl.lv[o].parent;
+      a.out_bind = sl.lv[o].bind;
+      a.cap_out = sl.lv[o].cap;
+      a.d_nout = dsz + o;
+      a.overflow = sl.d_ovf;
+      a.ctr = sl.d_ctr;
+      a.lb = next_lb(sl);
+      prof.begin(K_EXPAND_SEG);
+      CU(launch_seg_scan(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      launches[K_EXPAND_SEG]++;
+      prof.end();
+      a.lb = next_lb(sl);
+      prof.begin(K_EXPAND_EMIT);
+      CU(launch_expand_lb(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      launches[K_EXPAND_EMIT]++;
+      prof.end();
+    }
+    CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
+    return GSMART_OK;
+  }
+
+  // f2 phase 2 (host-synchronous; no speculation or graph): a8 on the factorised
+  // trees (a node lives iff every branch below it keeps a child, and its parent
+  // lives), §8.1 Ω pruning per root binding, subtree counts, then a9 rows
+  // enumerated from the trees and sorted.
+  gsmart_status phase2_f() {
+    state = S_PHASE2;
+    TRY(keep_candidates());
+    const int sm = ctx->sm_count;
+    const uint32_t nc = (uint32_t)plan->vars.size();
+    std::vector<std::vector<uint32_t>> kids(L);
+    for (uint32_t o = 1; o < L; o++) kids[occ[o].par].push_back(o);
+    uint64_t maxF = 1;
+    for (uint32_t o = 0; o < L; o++) maxF = std::max<uint64_t>(maxF, F[o]);
+    uint8_t* hc = nullptr;
+    TRY(sc.get(&hc, maxF));
+    auto rootb = [&](uint32_t o) { return o == 0 ? sl.lv[0].bind : sl.lv[o].newidx; };
+    prof.begin(K_PRUNE);
+    for (uint32_t o = 0; o < L; o++) {
+      CU(launch_f_fill(sl.lv[o].alive, F[o], 1, sm, sl.st));
+      launches[K_PRUNE]++;
+    }
+    auto bottom_up = [&]() -> gsmart_status {
+      for (uint32_t o = L - 1; o >= 1; o--) {
+        const uint32_t p = (uint32_t)occ[o].par;
+        if (!F[p]) continue;
+        CU(cudaMemsetAsync(hc, 0, F[p], sl.st));
+        CU(launch_f_mark(sl.lv[o].parent, sl.lv[o].alive, F[o], hc, sm, sl.st));
+        CU(launch_f_and(sl.lv[p].alive, hc, F[p], sm, sl.st));
+        launches[K_PRUNE] += 2;
+      }
+      return GSMART_OK;
+    };
+    auto top_down = [&](bool roots) -> gsmart_status {
+      for (uint32_t o = 1; o < L; o++) {
+        const uint32_t p = (uint32_t)occ[o].par;
+        CU(launch_f_down(sl.lv[o].alive, sl.lv[o].parent, sl.lv[p].alive, roots ? rootb(p) : nullptr,
+                         roots ? rootb(o) : nullptr, F[o], sm, sl.st));
+        launches[K_PRUNE]++;
+      }
+      return GSMART_OK;
+    };
+    TRY(bottom_up());
+    TRY(top_down(n_omega > 0));
+    if (n_omega) {  // §8.1 steps 1-3: per root binding, a variable's bindings must occur at all its occurrences
+      std::map<uint32_t, std::vector<uint32_t>> by_var;
+      for (uint32_t o = 0; o < L; o++) by_var[occ[o].var].push_back(o);
+      // one bit above every live key: dead nodes' keys (all ones) sort strictly last
+      const int kb = std::min(64, 33 + bits_for(ctx->N ? ctx->N - 1 : 0));
+      for (auto& kv : by_var) {
+        const auto& G = kv.second;
+        if (G.size() < 2) continue;
+        std::vector<unsigned long long*> sorted(G.size());
+        for (size_t i = 0; i < G.size(); i++) {
+          const uint32_t X = G[i];
+          unsigned long long *k0 = nullptr, *k1 = nullptr;
+          void* tmp = nullptr;
+          const uint64_t n = std::max<uint64_t>(F[X], 1);
+          TRY(sc.get(&k0, n));
+          TRY(sc.get(&k1, n));
+          const size_t tb = radix_tmp_bytes(n);
+          TRY(sc.get((char**)&tmp, tb));
+          CU(launch_f_keys(rootb(X), sl.lv[X].bind, sl.lv[X].alive, F[X], k0, sm, sl.st));
+          int second = 0;
+          CU(radix_sort_keys_u64(reinterpret_cast<uint64_t*>(k0), reinterpret_cast<uint64_t*>(k1), F[X], 0, kb, tmp,
+                                 tb, sl.st, &second, &launches[K_PRUNE], false));
+          sorted[i] = second ? k1 : k0;
+          launches[K_PRUNE]++;
+        }
+        for (size_t i = 0; i < G.size(); i++) {
+          FProbeArgs pa;
+          memset(&pa, 0, sizeof pa);
+          pa.root = rootb(G[i]);
+          pa.bind = sl.lv[G[i]].bind;
+          pa.alive = sl.lv[G[i]].alive;
+          pa.n = F[G[i]];
+          for (size_t j = 0; j < G.size(); j++)
+            if (j != i) {
+              pa.keys[pa.n_other] = sorted[j];
+              pa.n_keys[pa.n_other++] = F[G[j]];
+            }
+          CU(launch_f_probe(pa, sm, sl.st));
+          launches[K_PRUNE]++;
+        }
+      }
+      TRY(bottom_up());  // step 4: parents left without a child in some branch
+      TRY(top_down(false));
+    }
+    // subtree counts, leaves first: cnt(m) = prod over branches of the children's counts
+    std::vector<unsigned long long*> P(L, nullptr);
+    std::vector<uint32_t*> cb(L, nullptr), ce(L, nullptr);
+    unsigned long long* n_alive = nullptr;
+    TRY(sc.get(&n_alive, 1));
+    for (uint32_t o = 0; o < L; o++) TRY(sc.get(&P[o], F[o] + 1));
+    for (uint32_t o = 1; o < L; o++) {
+      const uint64_t np = std::max<uint64_t>(F[occ[o].par], 1);
+      TRY(sc.get(&cb[o], np));
+      TRY(sc.get(&ce[o], np));
+      CU(cudaMemsetAsync(cb[o], 0, np * 4, sl.st));
+      CU(cudaMemsetAsync(ce[o], 0, np * 4, sl.st));
+      CU(launch_f_ranges(sl.lv[o].parent, F[o], cb[o], ce[o], sm, sl.st));
+      launches[K_PRUNE]++;
+    }
+    for (uint32_t o = L; o-- > 0;) {
+      FCountArgs ca;
+      memset(&ca, 0, sizeof ca);
+      ca.alive = sl.lv[o].alive;
+      ca.n = F[o];
+      for (uint32_t c : kids[o]) {
+        ca.P[ca.nch] = P[c];
+        ca.beg[ca.nch] = cb[c];
+        ca.end[ca.nch++] = ce[c];
+      }
+      ca.out = P[o];
+      ca.lb = next_lb(sl);
+      ca.overflow = sl.d_ovf;
+      CU(launch_f_count_scan(ca, sm, sl.st));
+      launches[K_PRUNE]++;
+    }
+    prof.end();
+    unsigned long long total = 0;
+    int ovf = 0;
+    CU(cudaMemcpyAsync(&total, P[0] + F[0], 8, cudaMemcpyDeviceToHost, sl.st));
+    CU(cudaMemcpyAsync(&ovf, sl.d_ovf, 4, cudaMemcpyDeviceToHost, sl.st));
+    CU(cudaStreamSynchronize(sl.st));
+    if (ovf & 4) FAIL(GSMART_E_RESULT_OVERFLOW, "factorised: more than 2^46 combinations");
+    R->stats.factorised = 1;
+    R->stats.n_omega = n_omega;
+    R->stats.combinations = total;
+    // the trees themselves (gsmart_result_tree): bindings, parent links, alive flags
+    R->levels.clear();
+    {
+      uint64_t bytes = 0;
+      auto al = [](uint64_t b) { return (b + 255) / 256 * 256; };
+      for (uint32_t o = 0; o < L; o++) bytes += al(F[o] * 4) * 2 + al(F[o]);
+      char* arena = nullptr;
+      TRY(alloc_result((void**)&arena, std::max<uint64_t>(bytes, 256)));
+      for (uint32_t o = 0; o < L; o++) {
+        gsmart_result::Lv lv{occ[o].var, F[o], nullptr, nullptr};
+        lv.parent_level = occ[o].par;
+        lv.bind = (uint32_t*)arena;
+        arena += al(F[o] * 4);
+        if (o) {
+          lv.parent = (uint32_t*)arena;
+          CU(cudaMemcpyAsync(lv.parent, sl.lv[o].parent, F[o] * 4, cudaMemcpyDeviceToDevice, sl.st));
+        }
+        arena += al(F[o] * 4);
+        lv.alive = (uint8_t*)arena;
+        arena += al(F[o]);
+        CU(cudaMemcpyAsync(lv.bind, sl.lv[o].bind, F[o] * 4, cudaMemcpyDeviceToDevice, sl.st));
+        CU(cudaMemcpyAsync(lv.alive, sl.lv[o].alive, F[o], cudaMemcpyDeviceToDevice, sl.st));
+        R->levels.push_back(lv);
+      }
+    }
+    const bool filtered = n_omega > 0;
+    const bool want_rows = !(flags & GSMART_COUNT_ONLY);
+    R->count_only = !want_rows;
+    FEnumArgs ea;
+    memset(&ea, 0, sizeof ea);
+    for (uint32_t o = 0; o < L; o++) {
+      FOcc& fo = ea.o[o];
+      fo.bind = sl.lv[o].bind;
+      fo.P = P[o];
+      fo.beg = cb[o];
+      fo.end = ce[o];
+      fo.par = occ[o].par;
+      fo.col = occ[o].col;
+      fo.same = occ[o].same;
+      fo.leaf = kids[o].empty() ? 1 : 0;
+    }
+    ea.n_occ = L;
+    ea.n_root = (uint32_t)F[0];
+    ea.nc = nc;
+    ea.total = total;
+    ea.overflow = sl.d_ovf;
+    ea.filtered = filtered ? 1 : 0;
+    unsigned long long* d_cnt = sl.d_ctr + 60;
+    ea.d_count = d_cnt;
+    uint64_t n_rows = total;
+    if (filtered && total) {  // Ω equality: count the consistent combinations first
+      ea.count_only = 1;
+      CU(cudaMemsetAsync(d_cnt, 0, 8, sl.st));
+      prof.begin(K_ENUMERATE);
+      CU(launch_f_enum(ea, sm, sl.st));
+      prof.end();
+      launches[K_ENUMERATE]++;
+      CU(cudaMemcpyAsync(&n_rows, d_cnt, 8, cudaMemcpyDeviceToHost, sl.st));
+      CU(cudaStreamSynchronize(sl.st));
+    }
+    R->n_rows = n_rows;
+    if (n_rows > ctx->cap()) FAIL(GSMART_E_RESULT_OVERFLOW, "factorised: rows exceed max_result_rows");
+    CU(cudaMemcpyAsync(sl.h_pin + 192, sl.d_ctr, C_NCTR * 8, cudaMemcpyDeviceToHost, sl.st));
+    ctr_pinned = true;
+    if (!want_rows || !n_rows) {
+      R->host_valid = !n_rows && want_rows;
+      return GSMART_OK;
+    }
+    uint32_t* raw = nullptr;
+    TRY(sc.get(&raw, n_rows * nc));
+    TRY(alloc_result((void**)&R->d_rows, n_rows * nc * 4));
+    ea.count_only = 0;
+    ea.rows = raw;
+    ea.cap_rows = n_rows;
+    if (filtered) CU(cudaMemsetAsync(d_cnt, 0, 8, sl.st));
+    prof.begin(K_ENUMERATE);
+    CU(launch_f_enum(ea, sm, sl.st));
+    launches[K_ENUMERATE]++;
+    prof.end();
+    const size_t tb = sort_rows_tmp_bytes(n_rows, nc);
+    void* tmp = nullptr;
+    TRY(sc.get((char**)&tmp, std::max<size_t>(tb, 256)));
+    prof.begin(K_SORT_ROWS);
+    CU(sort_rows(raw, R->d_rows, n_rows, nc, nc, bits_for(ctx->N ? ctx->N - 1 : 0), tmp, tb, sl.st,
+                 &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50)));
+    prof.end();
     return GSMART_OK;
   }
 
@@ -798,7 +1172,8 @@ struct Exec {
     }
     for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1, (uint32_t)anc_cols[k].size()));
     for (uint32_t k = 1; k < L; k++)
-      if (plan->levels[k].tree_edge < 0) TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
+      if (fact ? !occ[k].tree : plan->levels[k].tree_edge < 0)
+        TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));
     return GSMART_OK;
   }
 
@@ -888,7 +1263,8 @@ struct Exec {
 
   // phase 1 = seeds + grouped evaluation + expansion (graph key: uid, tag 0)
   gsmart_status run_phase1() {
-    return run_cached(plan->uid << 3, flags & (GSMART_NO_REFINE | GSMART_BACK_EDGES), [&] { return phase1_kernels(); });
+    return run_cached(plan->uid << 3, flags & (GSMART_NO_REFINE | GSMART_BACK_EDGES | GSMART_FACTORISED),
+                      [&] { return phase1_kernels(); });
   }
 
   gsmart_status start() {
@@ -926,7 +1302,16 @@ struct Exec {
       if (flags & GSMART_BACK_EDGES)
         gedges[gi].insert(gedges[gi].end(), plan->groups[gi].back.begin(), plan->groups[gi].back.end());
     }
-    plan_ancestors();
+    fact = (flags & GSMART_FACTORISED) != 0;
+    if (fact) {
+      if (ctx->world > 1 || ctx->comm) FAIL(GSMART_E_UNSUPPORTED, "GSMART_FACTORISED needs world == 1");
+      TRY(build_occurrences());
+      L = (uint32_t)occ.size();
+      identity = false;
+      anc_cols.assign(L, {});
+    } else {
+      plan_ancestors();
+    }
     TRY(decide_push());
     TRY(ensure_workspace());
     TRY(begin_seq(ctx, sl));
@@ -967,7 +1352,7 @@ struct Exec {
   // the guess and, on a mismatch, redoes phase 2 the ordinary way.
   bool spec = false, spec_pending = false;
   bool can_speculate() const {
-    if ((ctx->world > 1 && !peer_mode()) || (flags & GSMART_NO_SPECULATE)) return false;
+    if ((ctx->world > 1 && !peer_mode()) || (flags & GSMART_NO_SPECULATE) || fact) return false;
     auto it = ctx->p2_guess.find(plan->uid);
     if (it == ctx->p2_guess.end() || it->second.gen != ctx->lspm_gen || it->second.flags != flags ||
         it->second.F.size() != L)
@@ -1046,6 +1431,7 @@ struct Exec {
   // output pointers from the slot's OutTab (filled here per execute, copied to the
   // device inside the work), so it replays from a per-plan graph like phase 1.
   gsmart_status phase2() {
+    if (fact) return phase2_f();
     state = S_PHASE2;
     static_assert(C_NCTR <= 64, "counter readback slots");
     TRY(keep_candidates());
@@ -1243,7 +1629,7 @@ struct Exec {
       end_seq(sl);
       seq_open = false;
     }
-    if (state == S_PHASE2 && R->n_rows) {
+    if (state == S_PHASE2 && R->n_rows && !fact) {
       for (uint32_t k = 0; k < L && k < (uint32_t)R->levels.size(); k++) {
         R->levels[k].n = sl.h_pin[128 + k];
         R->stats.level_alive[k] = sl.h_pin[128 + k];

@@ -354,4 +354,61 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
                       int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches,
                       int* sorted_flag = nullptr);
 
+
+// ----------------------------------------------------------------- f2 factorised trees (factorised.cu)
+constexpr int MAXOCC = 32;  // occurrences of variables in the factorised tree (= GSMART_MAX_LEVELS)
+struct FProbeArgs {         // Ω pruning of one occurrence against the other occurrences of its variable
+  const uint32_t* root;     // root binding of each node
+  const uint32_t* bind;
+  uint8_t* alive;
+  uint64_t n;
+  uint32_t n_other;
+  const unsigned long long* keys[MAXOCC];  // sorted (root, binding) keys of the other occurrences
+  uint64_t n_keys[MAXOCC];
+};
+struct FCountArgs {         // subtree counts of one occurrence from its child occurrences
+  const uint8_t* alive;
+  uint64_t n;
+  uint32_t nch;
+  const unsigned long long* P[MAXOCC];  // child occurrence q: exclusive scan of its counts
+  const uint32_t* beg[MAXOCC];          // child range of each node of this occurrence
+  const uint32_t* end[MAXOCC];
+  unsigned long long* out;              // [n + 1]
+  LBArgs lb;
+  int* overflow;                        // |= 4: a count exceeds 2^46
+};
+struct FOcc {               // one occurrence, as the enumeration reads it
+  const uint32_t* bind;
+  const unsigned long long* P;  // exclusive scan of the counts of its nodes
+  const uint32_t* beg;          // [n of the parent occurrence]: this occurrence's children of a parent node
+  const uint32_t* end;
+  int par;                      // parent occurrence (-1 for the root)
+  int col;                      // output column, -1 for a second occurrence (Ω)
+  int same;                     // Ω: the first occurrence of the same variable, else -1
+  int leaf;                     // no child occurrences: every node counts 0 or 1
+};
+struct FEnumArgs {
+  FOcc o[MAXOCC];
+  uint32_t n_occ, n_root, nc;
+  unsigned long long total;     // combinations of the pruned trees
+  uint32_t* rows;               // [cap_rows x nc]
+  uint64_t cap_rows;
+  unsigned long long* d_count;  // rows kept (filtered)
+  int* overflow;                // |= 8: more rows than cap_rows
+  int count_only, filtered;
+};
+cudaError_t launch_f_fill(uint8_t* a, uint64_t n, uint8_t v, int sm, cudaStream_t st);
+cudaError_t launch_f_mark(const uint32_t* parent, const uint8_t* alive, uint64_t n, uint8_t* hc, int sm,
+                          cudaStream_t st);
+cudaError_t launch_f_and(uint8_t* alive, const uint8_t* hc, uint64_t n, int sm, cudaStream_t st);
+cudaError_t launch_f_down(uint8_t* alive, const uint32_t* parent, const uint8_t* alive_par, const uint32_t* root_par,
+                          uint32_t* root, uint64_t n, int sm, cudaStream_t st);
+cudaError_t launch_f_keys(const uint32_t* root, const uint32_t* bind, const uint8_t* alive, uint64_t n,
+                          unsigned long long* keys, int sm, cudaStream_t st);
+cudaError_t launch_f_probe(const FProbeArgs& a, int sm, cudaStream_t st);
+cudaError_t launch_f_ranges(const uint32_t* parent, uint64_t n, uint32_t* beg, uint32_t* end, int sm,
+                            cudaStream_t st);
+cudaError_t launch_f_count_scan(const FCountArgs& a, int sm, cudaStream_t st);
+cudaError_t launch_f_enum(const FEnumArgs& a, int sm, cudaStream_t st);
+
 }  // namespace gsm

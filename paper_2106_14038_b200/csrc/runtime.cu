@@ -836,6 +836,20 @@ extern "C" gsmart_status gsmart_result_level(const gsmart_result* r, uint32_t k,
   return GSMART_OK;
 }
 
+extern "C" gsmart_status gsmart_result_tree(const gsmart_result* r, uint32_t k, uint32_t* vertex, int32_t* parent_level,
+                                            uint64_t* n, const uint32_t** parent_dev, const uint32_t** bind_dev,
+                                            const uint8_t** alive_dev) {
+  if (!r || k >= r->levels.size()) return GSMART_E_INVALID_ARG;
+  const auto& L = r->levels[k];
+  if (vertex) *vertex = L.var;
+  if (parent_level) *parent_level = L.parent_level == -2 ? (int32_t)k - 1 : L.parent_level;
+  if (n) *n = L.n;
+  if (parent_dev) *parent_dev = L.parent;
+  if (bind_dev) *bind_dev = L.bind;
+  if (alive_dev) *alive_dev = L.alive;
+  return GSMART_OK;
+}
+
 extern "C" gsmart_status gsmart_result_stats(const gsmart_result* r, gsmart_stats* out) {
   if (!r || !out) return GSMART_E_INVALID_ARG;
   *out = r->stats;

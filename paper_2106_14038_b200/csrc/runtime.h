@@ -302,7 +302,7 @@ struct gsmart_result {
   uint32_t* d_cand = nullptr;
   uint32_t n_words = 0, stride_words = 0;
   std::vector<int32_t> cand_slot;  // vertex -> slot or -1
-  struct Lv { uint32_t var; uint64_t n; uint32_t* parent; uint32_t* bind; };
+  struct Lv { uint32_t var; uint64_t n; uint32_t* parent; uint32_t* bind; int32_t parent_level = -2; uint8_t* alive = nullptr; };
   std::vector<Lv> levels;
   std::vector<void*> owned;        // device allocations to free
   gsmart_stats stats{};

@@ -23,6 +23,7 @@ GSMART_COUNT_ONLY, GSMART_KEEP_ON_DEVICE, GSMART_NO_REFINE, GSMART_PROFILE = 1, 
 GSMART_KEEP_CANDIDATES, GSMART_NO_GRAPH = 16, 32
 GSMART_NO_SPECULATE = 64
 GSMART_BACK_EDGES = 128
+GSMART_FACTORISED = 256
 NKERNELS, MAX_LEVELS = 16, 32
 
 
@@ -75,6 +76,7 @@ class gsmart_stats(ctypes.Structure):
                 ("n_levels", ctypes.c_uint32), ("level_nodes", ctypes.c_uint64 * MAX_LEVELS),
                 ("level_alive", ctypes.c_uint64 * MAX_LEVELS), ("allgather_bytes", ctypes.c_uint64),
                 ("spec_phase2", ctypes.c_uint32), ("spec_redo", ctypes.c_uint32),
+                ("factorised", ctypes.c_uint32), ("n_omega", ctypes.c_uint32), ("combinations", ctypes.c_uint64),
                 ("kernel_names", ctypes.c_char_p * NKERNELS)]
 
 
@@ -110,6 +112,8 @@ def _load():
         "gsmart_result_candidates": (st, [vp, u32, ctypes.POINTER(vp), ctypes.POINTER(u32)]),
         "gsmart_result_level": (st, [vp, u32, ctypes.POINTER(u32), ctypes.POINTER(u64), ctypes.POINTER(vp),
                                      ctypes.POINTER(vp)]),
+        "gsmart_result_tree": (st, [vp, u32, ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(u64),
+                                    ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "gsmart_result_stats": (st, [vp, ctypes.POINTER(gsmart_stats)]),
         "gsmart_result_free": (None, [vp]),
         "gsmart_copy_to_host": (st, [vp, vp, vp, ctypes.c_size_t]),
@@ -139,7 +143,7 @@ EXPORTED = ["gsmart_abi_version", "gsmart_build_info", "gsmart_get_nccl_id", "gs
             "gsmart_plan_describe", "gsmart_plan_free", "gsmart_execute", "gsmart_execute_batch",
             "gsmart_result_shape",
             "gsmart_result_rows", "gsmart_result_rows_device", "gsmart_result_candidates",
-            "gsmart_result_level", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host",
+            "gsmart_result_level", "gsmart_result_tree", "gsmart_result_stats", "gsmart_result_free", "gsmart_copy_to_host",
             "gsmart_comm_create_local", "gsmart_comm_destroy", "gsmart_partition_split", "gsmart_partition_get",
             "gsmart_rendezvous_check", "gsmart_ingest_ntriples", "gsmart_dict_lookup", "gsmart_dict_term",
             "gsmart_triples_get"]
@@ -399,6 +403,18 @@ def gsmart_result_level(r, k):
     return v.value, n.value, par.value, bnd.value
 
 
+def gsmart_result_tree(r, k):
+    """(vertex, parent_level, n, parent_dev, bind_dev, alive_dev) of level k of
+    the result's tree form (occurrence k with GSMART_FACTORISED)."""
+    v = ctypes.c_uint32()
+    pl = ctypes.c_int32()
+    n = ctypes.c_uint64()
+    par, bnd, alv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _check(_lib.gsmart_result_tree(r, k, ctypes.byref(v), ctypes.byref(pl), ctypes.byref(n), ctypes.byref(par),
+                                   ctypes.byref(bnd), ctypes.byref(alv)))
+    return v.value, pl.value, n.value, par.value, bnd.value, alv.value
+
+
 def gsmart_result_stats(r):
     s = gsmart_stats()
     _check(_lib.gsmart_result_stats(r, ctypes.byref(s)))
@@ -416,6 +432,7 @@ def gsmart_result_stats(r):
         "level_alive": [int(s.level_alive[i]) for i in range(s.n_levels)],
         "allgather_bytes": int(s.allgather_bytes),
         "spec_phase2": int(s.spec_phase2), "spec_redo": int(s.spec_redo),
+        "factorised": int(s.factorised), "n_omega": int(s.n_omega), "combinations": int(s.combinations),
     }
 
 

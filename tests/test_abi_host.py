@@ -38,7 +38,7 @@ def test_header_symbols_exported(G):
 
 
 def test_abi_version_and_build_info(G):
-    assert G.gsmart_abi_version() == 2
+    assert G.gsmart_abi_version() == 3
     assert "sm_100a" in G.gsmart_build_info()
 
 
