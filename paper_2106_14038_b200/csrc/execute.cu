@@ -59,6 +59,7 @@ static void slot_free(gsmart_ctx* ctx, Slot& s) {
   dfree(ctx, st, s.heavy_rows); dfree(ctx, st, s.heavy_chunks); dfree(ctx, st, s.heavy_sat); dfree(ctx, st, s.heavy_cnt);
   dfree(ctx, st, s.frows); dfree(ctx, st, s.sat); dfree(ctx, st, s.d_epoch); dfree(ctx, st, s.p2); dfree(ctx, st, s.d_tab);
   dfree(ctx, st, s.d_bar);
+  dfree(ctx, st, s.om);
   if (s.sym.va) {
     cudaStreamSynchronize(st);
     sym_free(ctx, &s.sym);
@@ -312,6 +313,24 @@ struct Exec {
   bool fact = false;
   std::vector<Occ> occ;
   uint32_t n_omega = 0;
+  std::vector<uint64_t> om_off, om_mask;  // per occurrence: its key set in sl.om (second occurrences only)
+  // key sets of the first occurrences, one per second occurrence, sized for the
+  // first occurrence's level capacity (load factor <= 1/2)
+  gsmart_status ensure_om() {
+    om_off.assign(L, 0);
+    om_mask.assign(L, 0);
+    uint64_t total = 0;
+    for (uint32_t o = 0; o < L; o++) {
+      if (occ[o].same < 0) continue;
+      uint64_t c = 1024;
+      while (c < 2 * sl.lv[occ[o].same].cap) c <<= 1;
+      om_off[o] = total;
+      om_mask[o] = c - 1;
+      total += c;
+    }
+    if (total) TRY(slot_buf(ctx, sl, &sl.om, &sl.om_cap, total));
+    return GSMART_OK;
+  }
   gsmart_status build_occurrences() {
     const uint32_t LT = (uint32_t)plan->levels.size();
     std::vector<int> of_var(plan->n_vertices, -1);
@@ -322,6 +341,11 @@ struct Exec {
     n_omega = 0;
     // (center, other variable) -> the patterns between them that close onto a non-parent level
     std::map<std::pair<uint32_t, uint32_t>, std::vector<uint32_t>> cross;
+    auto is_anc = [&](int from, int a) {  // occurrence a on the path from `from` up to the root
+      for (int x = from; x >= 0; x = occ[x].par)
+        if (x == a) return true;
+      return false;
+    };
     for (uint32_t k = 0; k < LT; k++) {
       const Level& Lv = plan->levels[k];
       Occ o;
@@ -343,6 +367,11 @@ struct Exec {
         } else if (k > 0 && c.other_level == plev) {
           o.cl.push_back({c.label, plev, c.dir == OUT ? 0u : 1u, 0u});
           o.cl_idx.push_back(ANC_BIND);
+        } else if (k > 0 && is_anc(o.par, of_var[plan->levels[c.other_level].var])) {
+          // onto an older level on this node's own root path: checked during expansion
+          // (a walk up the parent occurrences), no second occurrence needed
+          o.cl.push_back({c.label, (uint32_t)of_var[plan->levels[c.other_level].var], c.dir == OUT ? 0u : 1u, 0u});
+          o.cl_idx.push_back(ANC_WALK);
         } else {
           // the path of the pattern's center continues to the other endpoint (P:L516,
           // Ex. 7.1 "v2 -> v0 -> v1"): a second occurrence of that variable under the center
@@ -703,6 +732,7 @@ struct Exec {
       for (uint32_t j = 0; j < k; j++) {
         a.tab.parent[j] = sl.lv[j].parent;
         a.tab.bind[j] = sl.lv[j].bind;
+        a.tab.up[j] = (uint8_t)(j ? j - 1 : 0);
       }
       a.k = k;
       a.d_nparent = dsz + (k - 1);
@@ -772,7 +802,10 @@ struct Exec {
   // k - 1, so ANC_BIND reads the parent occurrence's bindings)
   gsmart_status launch_expansion_f(bool fresh) {
     unsigned long long* dsz = sl.d_sz;
-    if (!fresh) CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
+    if (!fresh) {
+      CU(cudaMemsetAsync(dsz, 0, 128 * 8, sl.st));
+      TRY(ensure_om());  // a level grew: key sets follow (not inside a capture: re-runs launch directly)
+    }
     prof.begin(K_COMPACT);
     CU(launch_bitmap_compact_lb(cand(occ[0].var), W, sl.lv[0].bind, sl.lv[0].cap, dsz + 0, sl.d_ovf, next_lb(sl),
                                 ctx->sm_count, sl.st));
@@ -786,6 +819,7 @@ struct Exec {
       for (uint32_t j = 0; j < o; j++) {
         a.tab.parent[j] = sl.lv[j].parent;
         a.tab.bind[j] = sl.lv[j].bind;
+        a.tab.up[j] = (uint8_t)(j ? occ[j].par : 0);
       }
       a.k = p + 1;
       a.d_nparent = dsz + p;
@@ -804,6 +838,17 @@ struct Exec {
       a.par_idx = ANC_BIND;
       a.closing_csr = (!ctx->f[1].built || ctx->keep[0] != ctx->keep[1]) ? 1 : 0;
       a.use_tma = ctx->use_tma ? 1 : 0;
+      if (oc.same >= 0) {  // Ω pre-pruning (§7.2.2 applied to §8.1's common variable)
+        unsigned long long* t = sl.om + om_off[o];
+        CU(cudaMemsetAsync(t, 0xff, (om_mask[o] + 1) * 8, sl.st));
+        prof.begin(K_PRUNE);
+        CU(launch_f_hash_build(a.tab, (uint32_t)oc.same, dsz + oc.same, sl.lv[oc.same].cap, t, om_mask[o],
+                               ctx->sm_count, sl.st));
+        launches[K_PRUNE]++;
+        prof.end();
+        a.om_tab = t;
+        a.om_mask = om_mask[o];
+      }
       if (!a.tree) {
         prof.begin(K_COMPACT);
         CU(launch_bitmap_compact_lb(cand(oc.var), W, sl.list[o], sl.list_cap[o], dsz + 64 + o, sl.d_ovf,
@@ -1171,6 +1216,7 @@ struct Exec {
       cudaGetLastError();
     }
     for (uint32_t k = 0; k < L; k++) TRY(slot_level(ctx, sl, k, 1, (uint32_t)anc_cols[k].size()));
+    if (fact) TRY(ensure_om());
     for (uint32_t k = 1; k < L; k++)
       if (fact ? !occ[k].tree : plan->levels[k].tree_edge < 0)
         TRY(slot_buf(ctx, sl, &sl.list[k], &sl.list_cap[k], (uint64_t)W * 32));

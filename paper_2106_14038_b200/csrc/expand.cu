@@ -27,9 +27,9 @@ __device__ __forceinline__ uint32_t ub_global(const uint32_t* __restrict__ a, ui
 }
 
 __device__ __forceinline__ uint32_t ancestor(const LevelTab& t, uint32_t k, uint32_t n, uint32_t j) {
-  while (k > j) {
+  while (k != j) {  // j is an ancestor level of k
     n = __ldg(t.parent[k] + n);
-    k--;
+    k = t.up[k];
   }
   return __ldg(t.bind[j] + n);
 }
@@ -439,6 +439,24 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
 #pragma unroll
     for (int j = 0; j < EX_I; j++)
       if (((actm >> j) & 1u) && !bit_of(a.cand, child[j])) keepm &= ~(1u << j);
+    if (a.om_tab) {  // f2: the child must occur under the same root binding at its first occurrence
+#pragma unroll
+      for (int j = 0; j < EX_I; j++) {
+        if (!((keepm >> j) & 1u)) continue;
+        const uint32_t r = ancestor(a.tab, a.k - 1, node[j], 0);
+        const unsigned long long key = ((unsigned long long)r << 32) | child[j];
+        uint64_t h = f_hash(key) & a.om_mask;
+        while (true) {
+          const unsigned long long v = __ldg(a.om_tab + h);
+          if (v == key) break;
+          if (v == ~0ull) {
+            keepm &= ~(1u << j);
+            break;
+          }
+          h = (h + 1) & a.om_mask;
+        }
+      }
+    }
     n_exam += __popc(actm);
     for (uint32_t q = 0; q < a.ncl && keepm; q++) {
       const ClosingDev cl = a.cl[q];

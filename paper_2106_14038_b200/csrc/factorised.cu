@@ -206,6 +206,27 @@ __global__ void __launch_bounds__(256) k_f_enum(const FEnumArgs a) {
   }
 }
 
+__global__ void k_f_hash_build(const LevelTab tab, uint32_t lev, const unsigned long long* d_n, uint64_t cap,
+                               unsigned long long* __restrict__ keys, uint64_t mask) {
+  GSM_PDL_ENTRY();
+  const uint64_t n = *d_n;
+  if (n > cap) return;  // the level overflowed its capacity: the host grows it and re-runs the expansion
+  for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < n; m += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)m, k = lev;
+    while (k != 0) {  // root node of m
+      x = __ldg(tab.parent[k] + x);
+      k = tab.up[k];
+    }
+    const unsigned long long key = ((unsigned long long)__ldg(tab.bind[0] + x) << 32) | __ldg(tab.bind[lev] + m);
+    uint64_t h = f_hash(key) & mask;
+    while (true) {
+      const unsigned long long prev = atomicCAS(keys + h, ~0ull, key);
+      if (prev == ~0ull || prev == key) break;
+      h = (h + 1) & mask;
+    }
+  }
+}
+
 static unsigned grid_for(uint64_t n, int sm_count) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count * 8));
 }
@@ -247,6 +268,10 @@ cudaError_t launch_f_count_scan(const FCountArgs& a, int sm, cudaStream_t st) {
   const uint64_t tiles = (a.n + FC_TILE - 1) / FC_TILE;
   if (tiles > a.lb.cap_tiles) return cudaErrorInvalidValue;
   return pdl_launch(k_f_count_scan, (unsigned)std::min<uint64_t>(tiles, (uint64_t)sm * 8), FC_T, st, a);
+}
+cudaError_t launch_f_hash_build(const LevelTab& tab, uint32_t lev, const unsigned long long* d_n, uint64_t cap,
+                                unsigned long long* tab_keys, uint64_t mask, int sm, cudaStream_t st) {
+  return pdl_launch(k_f_hash_build, (unsigned)sm * 8, 256, st, tab, lev, d_n, cap, tab_keys, mask);
 }
 cudaError_t launch_f_enum(const FEnumArgs& a, int sm, cudaStream_t st) {
   if (!a.total) return cudaSuccess;

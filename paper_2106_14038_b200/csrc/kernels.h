@@ -256,6 +256,7 @@ cudaError_t launch_group_filter(const FilterArgs& a, int pred_bytes, int sm_coun
 struct LevelTab {
   const uint32_t* parent[MAXL];
   const uint32_t* bind[MAXL];
+  uint8_t up[MAXL];  // the level parent[k] indexes (trie: k - 1; factorised: the parent occurrence)
 };
 struct ClosingDev {
   uint32_t label, other_level, dir, self;
@@ -298,7 +299,24 @@ struct ExpArgs2 {
   uint32_t* out_anc[MAXANC];
   int use_tma;                             // stage tile offsets with cp.async.bulk (off[] has >= 8 words of tail)
   int closing_csr;                         // closing checks read the subject's CSR row (CSR-only or split keep-sets)
+  // f2 Ω pre-pruning of a second occurrence: a child c of a node under root
+  // binding r is kept only if (r, c) is a node of the variable's first
+  // occurrence (open-addressing set of keys r << 32 | c; empty = ~0)
+  const unsigned long long* om_tab;
+  uint64_t om_mask;
 };
+// f2: insert the (root binding, binding) key of every node of a level into an
+// open-addressing set (capacity om_mask + 1, a power of two, cleared to ~0)
+cudaError_t launch_f_hash_build(const LevelTab& tab, uint32_t lev, const unsigned long long* d_n, uint64_t cap,
+                                unsigned long long* tab_keys, uint64_t mask, int sm, cudaStream_t st);
+__host__ __device__ __forceinline__ uint64_t f_hash(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
 constexpr int ANC_BIND = -1, ANC_WALK = -2;
 // ids of set bits of bm[0, n_words) plus id_base
 // kernels one launch_bitmap_compact_lb issues (none for an empty range)

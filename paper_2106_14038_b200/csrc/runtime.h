@@ -137,6 +137,8 @@ struct Slot {
   unsigned long long* lb_status = nullptr;
   uint32_t* lb_counters = nullptr;
   uint32_t* tile_start = nullptr;      // [LB_CAP_TILES] expansion tile -> first parent
+  unsigned long long* om = nullptr;    // f2: (root, binding) key sets of first occurrences with a second one
+  uint64_t om_cap = 0;
   uint32_t epoch = 0;
   unsigned long long* d_sz = nullptr;  // [0,32) F_k, [32,64) T_k, [64,96) list len, [96,128) alive, 127 overflow
   int* d_ovf = nullptr;

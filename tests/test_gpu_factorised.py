@@ -174,8 +174,11 @@ def _check_dataset(G, eng, s, p, o, N, P, qs):
         assert eng.query(q, flags=G.GSMART_FACTORISED | G.GSMART_COUNT_ONLY) == len(exp), q.name
 
 
-def test_lubm_rows(G, eng):
-    d = lubm.generate(2)
+@pytest.mark.parametrize("U", [2, 10])
+def test_lubm_rows(G, eng, U):
+    """U = 10: levels outgrow the first workspace (grow + re-run the expansion,
+    Ω key sets re-sized with them)."""
+    d = lubm.generate(U)
     _check_dataset(G, eng, d.s.numpy(), d.p.numpy(), d.o.numpy(), d.n_entities, d.n_predicates, lubm.queries(d))
 
 
