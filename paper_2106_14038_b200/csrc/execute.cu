@@ -1526,7 +1526,8 @@ struct Exec {
     if (want_rows) {
       R->d_rows = alias_rows ? ot.bind[0] : (uint32_t*)take(n_rows * nc * 4);
       ot.rows = ot.sorted = R->d_rows;
-      if (mode != M_IDENTITY) {  // enumerate into slot scratch, then sort into the result
+      if (mode != M_IDENTITY) {  // small: enumerate into slot scratch, rank-sort into the result;
+                                 // big: enumerate into the result, sort in place (scratch only if unsorted)
         tb = mode == M_SORT_SMALL ? SORT_SMALL_MAXN * 4 : sort_rows_tmp_bytes(n_rows, nc);
         const uint64_t need = al(n_rows * nc * 4) + al(tb);
         if (need > sl.p2_cap) {
@@ -1536,8 +1537,10 @@ struct Exec {
           TRY(dalloc(ctx, &sl.p2, need + need / 4, sl.st));
           sl.p2_cap = need + need / 4;
         }
-        ot.rows = (uint32_t*)sl.p2;
-        if (mode == M_SORT_SMALL) ot.rank = (uint32_t*)(sl.p2 + al(n_rows * nc * 4));
+        if (mode == M_SORT_SMALL) {
+          ot.rows = (uint32_t*)sl.p2;
+          ot.rank = (uint32_t*)(sl.p2 + al(n_rows * nc * 4));
+        }
       }
     } else {
       R->count_only = true;
@@ -1591,8 +1594,8 @@ struct Exec {
       while (n_key > 0 && col_level[n_key - 1] < col_level[n_key]) n_key--;
       void* tmp = sl.p2 + al(n_rows * nc * 4);
       prof.begin(K_SORT_ROWS);
-      CU(sort_rows(ot.rows, R->d_rows, n_rows, nc, n_key, bits_for(ctx->N - 1), tmp, tb, sl.st,
-                   &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50)));
+      CU(sort_rows((const uint32_t*)sl.p2, R->d_rows, n_rows, nc, n_key, bits_for(ctx->N - 1), tmp, tb, sl.st,
+                   &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50), true));
       prof.end();
     }
     return GSMART_OK;

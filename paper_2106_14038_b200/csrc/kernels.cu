@@ -1299,21 +1299,36 @@ struct ColMap {
   uint32_t c[MAXL];
 };
 
-__global__ void k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
-                            const unsigned long long* __restrict__ d_n_last, uint32_t n_cols) {
+// One row per leaf, 256 rows per CTA step: each thread walks its leaf's parent
+// chain into a shared-memory tile (row-major, n_cols words per row), then the
+// CTA writes the tile's contiguous n_cols * 256 words with coalesced stores
+// (a direct store per column would touch n_cols * 32 scattered words per warp).
+constexpr int EN_T = 256;
+__global__ void __launch_bounds__(EN_T) k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
+                                                   const unsigned long long* __restrict__ d_n_last, uint32_t n_cols) {
   GSM_PDL_ENTRY();
   if (!ot->go) return;
+  extern __shared__ uint32_t s_rows[];
   const uint32_t n_last = (uint32_t)*d_n_last;
   uint32_t* __restrict__ rows = ot->rows;
   uint32_t* __restrict__ rank = ot->rank;
-  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n_last; m += gridDim.x * blockDim.x) {
-    uint32_t idx = m;
-    uint32_t* r = rows + (uint64_t)m * n_cols;
-    for (int k = (int)L - 1; k >= 0; k--) {
-      r[cm.c[k]] = __ldg(ot->bind[k] + idx);
-      if (k > 0) idx = __ldg(ot->parent[k] + idx);
+  for (uint64_t base = (uint64_t)blockIdx.x * EN_T; base < n_last; base += (uint64_t)gridDim.x * EN_T) {
+    const uint64_t m = base + threadIdx.x;
+    if (m < n_last) {
+      uint32_t idx = (uint32_t)m;
+      uint32_t* r = s_rows + threadIdx.x * n_cols;
+      for (int k = (int)L - 1; k >= 0; k--) {
+        r[cm.c[k]] = __ldg(ot->bind[k] + idx);
+        if (k > 0) idx = __ldg(ot->parent[k] + idx);
+      }
+      if (rank && m < SORT_SMALL_MAXN) rank[m] = 0;  // the rank sort adds into it
     }
-    if (rank && m < SORT_SMALL_MAXN) rank[m] = 0;  // the rank sort adds into it
+    __syncthreads();
+    const uint64_t nr = min((uint64_t)EN_T, (uint64_t)n_last - base);
+    const uint32_t words = (uint32_t)(nr * n_cols);
+    uint32_t* out = rows + base * n_cols;
+    for (uint32_t i = threadIdx.x; i < words; i += EN_T) __stcs(out + i, s_rows[i]);
+    __syncthreads();
   }
 }
 
@@ -1321,7 +1336,13 @@ cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t
                              const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st) {
   ColMap cm;
   for (uint32_t k = 0; k < MAXL; k++) cm.c[k] = k < n_levels ? col_of_level[k] : 0;
-  pdl_launch(k_enumerate, (unsigned)sm_count * 16, 256, st, ot, n_levels, cm, d_n_last, n_cols);
+  const size_t smem = (size_t)EN_T * n_cols * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_enumerate, cudaFuncAttributeMaxDynamicSharedMemorySize, EN_T * MAXL * 4);
+    attr = true;
+  }
+  pdl_launch_smem(k_enumerate, (unsigned)sm_count * 8, EN_T, smem, st, ot, n_levels, cm, d_n_last, n_cols);
   return cudaGetLastError();
 }
 
@@ -1346,6 +1367,18 @@ __global__ void k_rows_sorted(const uint32_t* __restrict__ rows, uint64_t n, uin
   if (__any_sync(GSM_FULL, bad) && (threadIdx.x & 31) == 0) *sorted = 0;
 }
 
+// in-place sort: the rows move to the sort's scratch only when they are not sorted
+__global__ void k_copy_unless_sorted(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t m,
+                                     const int* sorted) {
+  GSM_PDL_ENTRY();
+  if (*sorted) return;
+  const uint64_t m4 = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15 ? 0 : m / 4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m4; i += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+  for (uint64_t i = 4 * m4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 __global__ void k_iota(uint32_t* v, uint64_t n, const int* skip) {
   GSM_PDL_ENTRY();
   if (skip && *skip) return;
@@ -1368,9 +1401,10 @@ __global__ void k_gather_key(const uint32_t* __restrict__ rows, const uint32_t* 
 }
 
 __global__ void k_gather_rows(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ perm, uint64_t n,
-                              uint32_t n_cols, uint32_t* __restrict__ out, const int* skip) {
+                              uint32_t n_cols, uint32_t* __restrict__ out, const int* skip, int ident_copy) {
   GSM_PDL_ENTRY();
-  const bool ident = skip && *skip;  // already sorted: a straight copy
+  const bool ident = skip && *skip;  // already sorted: a straight copy (in place: nothing to do)
+  if (ident && !ident_copy) return;
   if (ident) {
     const uint64_t m = n * n_cols;
     const uint64_t m4 = (reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(out)) & 15 ? 0 : m / 4;
@@ -1464,7 +1498,8 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
 // the trie order).  LSD over <= 64-bit keys of packed columns (hand-written radix
 // sort, radix.cu, permutation as payload), least significant chunk first; stable.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
-                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches, int* sorted_flag) {
+                      int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches, int* sorted_flag,
+                      bool inplace) {
   const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
   uint32_t* perm = (uint32_t*)tmp;
   uint32_t* perm2 = (uint32_t*)((char*)tmp + s4);
@@ -1474,12 +1509,18 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
   const size_t rbytes = tmp_bytes - 2 * s4 - 2 * s8;
   unsigned g = grid_for(n, 256, 148 * 32);
   int nl = 1;
+  if (inplace && !sorted_flag) return cudaErrorInvalidValue;
   if (sorted_flag) {  // rows often arrive sorted (functional patterns first in the trie): check once
     cudaError_t e = cudaMemsetAsync(sorted_flag, 0, 4, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(sorted_flag, 1, 1, st);  // little-endian int 1
     if (e != cudaSuccess) return e;
-    pdl_launch(k_rows_sorted, g, 256, st, rows, n, n_cols, sorted_flag);
+    pdl_launch(k_rows_sorted, g, 256, st, inplace ? rows_out : rows, n, n_cols, sorted_flag);
     nl++;
+    if (inplace) {  // rows_out holds the input: move it to `rows` (scratch) only if a sort follows
+      pdl_launch(k_copy_unless_sorted, grid_for(n * n_cols / 4 + 1, 256, 148 * 32), 256, st, (const uint32_t*)rows_out,
+                 const_cast<uint32_t*>(rows), n * n_cols, (const int*)sorted_flag);
+      nl++;
+    }
   }
   pdl_launch(k_iota, g, 256, st, perm, n, (const int*)sorted_flag);
   const int per = sort_chunk_cols(key_bits);
@@ -1495,7 +1536,7 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
     nl += 1;
   }
   pdl_launch(k_gather_rows, grid_for(n * n_cols, 256, 148 * 32), 256, st, rows, perm, n, n_cols, rows_out,
-             (const int*)sorted_flag);
+             (const int*)sorted_flag, inplace ? 0 : 1);
   if (launches) *launches += nl + 1;
   return cudaGetLastError();
 }

@@ -26,6 +26,22 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+// the same with dynamic shared memory
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ----------------------------------------------------------------- scans
 // Exclusive scan of n uint32 values (in may alias out).  Writes the 64-bit
@@ -368,9 +384,11 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols);
 // agree on [0, n_key) (n_key = n_cols: no assumption).
 // sorted_flag (device int, optional): the rows are first checked for order; if
 // already sorted, every sort kernel exits at entry and the rows are copied.
+// inplace: the input is in rows_out (rows = scratch of the same size, used only
+// when the rows turn out unsorted); needs sorted_flag.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
                       int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches,
-                      int* sorted_flag = nullptr);
+                      int* sorted_flag = nullptr, bool inplace = false);
 
 
 // ----------------------------------------------------------------- f2 factorised trees (factorised.cu)
