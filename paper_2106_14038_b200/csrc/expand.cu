@@ -12,6 +12,8 @@
 //                look-back prefix, so parent[] stays non-decreasing.
 // Overflow of a capacity is flagged in device memory and handled by the host
 // after the single sync (grow + re-run the expansion).
+#include <cstdlib>
+
 #include "kernels.h"
 #include "lookback.cuh"
 
@@ -222,12 +224,13 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
 }
 
 // ------------------------------------------------------------------ level k: segments + scan
-constexpr int SS_T = 256, SS_I = 4, SS_TILE = SS_T * SS_I;
-constexpr int EX_T = 256, EX_I = 4, EX_TILE = EX_T * EX_I;  // expansion tile (entries)
+constexpr int SS_T = 256;
+constexpr int EX_TILE = 1024;  // expansion tile (entries); EX_T threads x EX_I entries each
 
-template <typename PT>
+template <typename PT, int SS_I>
 __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
   GSM_PDL_ENTRY();
+  constexpr int SS_TILE = SS_T * SS_I;
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_pref;
@@ -336,9 +339,10 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
 // ------------------------------------------------------------------ level k: expansion
 constexpr uint32_t OFFCAP = 2048, TGTP = 1024, TGTC = 4;
 
-template <typename PT>
-__global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
+template <typename PT, int EX_T>
+__global__ void __launch_bounds__(EX_T, 1024 / EX_T) k_expand_lb(ExpArgs2 a) {
   GSM_PDL_ENTRY();
+  constexpr int EX_I = EX_TILE / EX_T;
   __shared__ __align__(16) uint32_t s_offbuf[OFFCAP + 8];
   __shared__ __align__(8) unsigned long long s_mbar;
   __shared__ uint32_t s_tgt[TGTP * TGTC];
@@ -549,15 +553,40 @@ __global__ void __launch_bounds__(EX_T, 4) k_expand_lb(ExpArgs2 a) {
 
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 8;
-  if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t>, g, SS_T, st, a);
-  else pdl_launch(k_seg_scan<uint16_t>, g, SS_T, st, a);
+  const char* ev = getenv("GSMART_SS_I");  // A/B: parents per thread (1: measured best, 4.88 vs 5.07 ms)
+  const int ssi = ev ? atoi(ev) : 1;
+  if (ssi == 8) {
+    if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t, 8>, g, SS_T, st, a);
+    else pdl_launch(k_seg_scan<uint16_t, 8>, g, SS_T, st, a);
+  } else if (ssi == 1) {
+    if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t, 1>, g, SS_T, st, a);
+    else pdl_launch(k_seg_scan<uint16_t, 1>, g, SS_T, st, a);
+  } else if (ssi == 2) {
+    if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t, 2>, g, SS_T, st, a);
+    else pdl_launch(k_seg_scan<uint16_t, 2>, g, SS_T, st, a);
+  } else {
+    if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t, 4>, g, SS_T, st, a);
+    else pdl_launch(k_seg_scan<uint16_t, 4>, g, SS_T, st, a);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 6;
-  if (pred_bytes == 1) pdl_launch(k_expand_lb<uint8_t>, g, EX_T, st, a);
-  else pdl_launch(k_expand_lb<uint16_t>, g, EX_T, st, a);
+  const char* ev = getenv("GSMART_EX_T");  // A/B: threads per 1024-entry tile
+  const int ext = ev ? atoi(ev) : 256;
+  if (ext == 512) {
+    g = (unsigned)sm_count * 3;
+    if (pred_bytes == 1) pdl_launch(k_expand_lb<uint8_t, 512>, g, 512, st, a);
+    else pdl_launch(k_expand_lb<uint16_t, 512>, g, 512, st, a);
+  } else if (ext == 1024) {
+    g = (unsigned)sm_count * 2;
+    if (pred_bytes == 1) pdl_launch(k_expand_lb<uint8_t, 1024>, g, 1024, st, a);
+    else pdl_launch(k_expand_lb<uint16_t, 1024>, g, 1024, st, a);
+  } else {
+    if (pred_bytes == 1) pdl_launch(k_expand_lb<uint8_t, 256>, g, 256, st, a);
+    else pdl_launch(k_expand_lb<uint16_t, 256>, g, 256, st, a);
+  }
   return cudaGetLastError();
 }
 
@@ -592,8 +621,9 @@ cudaError_t launch_prune_mark_d(const OutTab* ot, const uint32_t* parent, const 
   return cudaGetLastError();
 }
 
-constexpr int CA_T = 256, CA_I = 8, CA_TILE = CA_T * CA_I;
+constexpr int CA_T = 256;
 
+template <int CA_I>
 __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __restrict__ parent,
                                                           const uint32_t* __restrict__ bind,
                                                           const uint8_t* __restrict__ alive,
@@ -603,6 +633,7 @@ __global__ void __launch_bounds__(CA_T) k_compact_alive_lb(const uint32_t* __res
                                                           uint32_t* __restrict__ newidx,
                                                           unsigned long long* d_count, LBArgs lb) {
   GSM_PDL_ENTRY();
+  constexpr int CA_TILE = CA_T * CA_I;
   if (!ot->go) return;
   uint32_t* __restrict__ out_parent = k ? ot->parent[k] : nullptr;
   uint32_t* __restrict__ out_bind = ot->bind[k];
@@ -640,8 +671,11 @@ cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind
                                     const unsigned long long* d_n, const uint32_t* newidx_prev, const OutTab* ot,
                                     uint32_t k, uint32_t* newidx, unsigned long long* d_count, LBArgs lb,
                                     int sm_count, cudaStream_t st) {
-  pdl_launch(k_compact_alive_lb, (unsigned)sm_count * 8, CA_T, st, parent, bind, alive, d_n, newidx_prev, ot, k,
-             newidx, d_count, lb);
+  const char* ev = getenv("GSMART_CA_I");  // A/B: nodes per thread
+  const int cai = ev ? atoi(ev) : 4;  // 4: measured best (batch 4.67 vs 4.91 ms at 8)
+  auto kern = cai == 2 ? k_compact_alive_lb<2> : cai == 4 ? k_compact_alive_lb<4> : k_compact_alive_lb<8>;
+  pdl_launch(kern, (unsigned)sm_count * 8, CA_T, st, parent, bind, alive, d_n, newidx_prev, ot, k, newidx, d_count,
+             lb);
   return cudaGetLastError();
 }
 

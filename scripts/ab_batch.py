@@ -33,15 +33,8 @@ for var in args.variants.split(";"):
     env = {} if var == "default" else dict(kv.split("=") for kv in var.split(","))
     xflags = int(env.pop("flags", "0"))  # execute flags, e.g. flags=128 (GSMART_BACK_EDGES)
     old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        eng = G.Engine(0)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                del os.environ[k]
-            else:
-                os.environ[k] = v
+    os.environ.update(env)  # kept for the whole variant (some switches are read per launch)
+    eng = G.Engine(0)
     G.gsmart_load_triples(eng.ctx, s, p, o, N, P)
     G.gsmart_build_lspm(eng.ctx)
     plans = [G.gsmart_plan(eng.ctx, q) for q in qs]
@@ -80,3 +73,8 @@ for var in args.variants.split(";"):
     for pl in plans:
         G.gsmart_plan_free(pl)
     eng.close()
+    for k, v in old.items():
+        if v is None:
+            del os.environ[k]
+        else:
+            os.environ[k] = v
