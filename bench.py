@@ -448,15 +448,16 @@ def main():
                "sample": f"{n_q} queries of the batch, round-robin (~15 s of CPU work), index build excluded",
                "ms_per_batch": 1000 * cpu_s * len(qs) / n_q}
 
-    cfg = config_of(args)
-    cfg.update({"triples": int(len(s_h)), "entities": int(N), "predicates": int(P),
+    cfg = config_of(args)  # identical in both arms (same_config); sizes and layout beside it
+    info = {}
+    info.update({"triples": int(len(s_h)), "entities": int(N), "predicates": int(P),
                 "queries": [q.name for q in qs], "edges_per_step": int(sum(E)),
                 "parallelism": ("partitioned" if partitioned else "replicas") if world > 1 else "single",
                 "devices": n_dev, "oversubscribed": oversub})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg,
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg, "workload_info": info,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(3 * 4 * len(s_h)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * e2e_s,
