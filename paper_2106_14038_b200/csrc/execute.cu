@@ -292,6 +292,7 @@ struct Exec {
   bool identity = false;                 // trie order == column order: rows come out sorted
   std::vector<uint64_t> F;
   std::chrono::steady_clock::time_point t0;
+  int smc;  // SMs this execute sizes its grids for (a share of the device when a batch runs concurrently)
 
   // ---- f2: factorised binding trees (GSMART_FACTORISED; §7.1, §8.1).
   // One level per occurrence of a variable: the trie level's variable hangs off
@@ -407,7 +408,8 @@ struct Exec {
   }
 
   Exec(gsmart_ctx* c, Slot& s, const gsmart_plan_t* p, uint32_t fl, gsmart_result* r)
-      : ctx(c), sl(s), plan(p), flags(fl), R(r), prof(s.st, &r->stats, (fl & GSMART_PROFILE) != 0), sc(c, s.st) {
+      : ctx(c), sl(s), plan(p), flags(fl), R(r), prof(s.st, &r->stats, (fl & GSMART_PROFILE) != 0), sc(c, s.st),
+        smc(c->sm_count) {
     t0 = std::chrono::steady_clock::now();
   }
 
@@ -525,7 +527,7 @@ struct Exec {
     }
     if (sb.n) {
       prof.begin(K_SEED);
-      CU(launch_seed_scatter(sb, ctx->pred_bytes, sl.d_ctr, ctx->sm_count, sl.st));
+      CU(launch_seed_scatter(sb, ctx->pred_bytes, sl.d_ctr, smc, sl.st));
       launches[K_SEED]++;
       prof.end();
     }
@@ -617,7 +619,7 @@ struct Exec {
         }
         pa.skip = sk;
         pa.ctr = sl.d_ctr;
-        CU(launch_push_edge(pa, ctx->sm_count, sl.st));
+        CU(launch_push_edge(pa, smc, sl.st));
         launches[K_FILTER]++;
         prev_sat = out;
       }
@@ -625,7 +627,7 @@ struct Exec {
       ps.world = peer_world();
       ps.peers = peer_delta();
       CU(launch_and_tracked(cand(g.center) + wlo, prev_sat + wlo, whi - wlo, sk, (uint32_t)slot[g.center], seq, ps,
-                            sl.st, ctx->sm_count));
+                            sl.st, smc));
       launches[K_FILTER]++;
       push_and++;
       prof.end();
@@ -644,7 +646,7 @@ struct Exec {
       prof.begin(K_COMPACT);
       CU(cudaMemsetAsync(d_nrows, 0, 8, sl.st));
       CU(launch_bitmap_compact_lb(cand(g.center) + wlo, whi > wlo ? whi - wlo : 0, sl.frows, sl.frows_cap, d_nrows,
-                                  sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32, sk));
+                                  sl.d_ovf, next_lb(sl), smc, sl.st, wlo * 32, sk));
       launches[K_COMPACT] += compact_launches(whi > wlo ? whi - wlo : 0);
       prof.end();
     }
@@ -690,7 +692,7 @@ struct Exec {
         a.d_nrows = d_nrows;
       }
       prof.begin(K_FILTER);
-      CU(launch_group_filter(a, ctx->pred_bytes, ctx->sm_count, sl.st, &launches[K_FILTER]));
+      CU(launch_group_filter(a, ctx->pred_bytes, smc, sl.st, &launches[K_FILTER]));
       prof.end();
       filter_main++;
     }
@@ -722,7 +724,7 @@ struct Exec {
     prof.begin(K_COMPACT);
     // level 0 = this rank's root candidates (its word range; all of them when world == 1)
     CU(launch_bitmap_compact_lb(cand(plan->levels[0].var) + wlo, whi - wlo, sl.lv[0].bind, sl.lv[0].cap, dsz + 0,
-                                sl.d_ovf, next_lb(sl), ctx->sm_count, sl.st, wlo * 32));
+                                sl.d_ovf, next_lb(sl), smc, sl.st, wlo * 32));
     launches[K_COMPACT] += compact_launches(whi - wlo);
     prof.end();
     for (uint32_t k = 1; k < L; k++) {
@@ -765,7 +767,7 @@ struct Exec {
       if (!a.tree) {
         prof.begin(K_COMPACT);
         CU(launch_bitmap_compact_lb(cand(Lv.var), W, sl.list[k], sl.list_cap[k], dsz + 64 + k, sl.d_ovf,
-                                    next_lb(sl), ctx->sm_count, sl.st));
+                                    next_lb(sl), smc, sl.st));
         launches[K_COMPACT] += compact_launches(W);
         prof.end();
         a.list = sl.list[k];
@@ -784,12 +786,12 @@ struct Exec {
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
       prof.begin(K_EXPAND_SEG);
-      CU(launch_seg_scan(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      CU(launch_seg_scan(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_SEG]++;
       prof.end();
       a.lb = next_lb(sl);
       prof.begin(K_EXPAND_EMIT);
-      CU(launch_expand_lb(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      CU(launch_expand_lb(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_EMIT]++;
       prof.end();
     }
@@ -808,7 +810,7 @@ struct Exec {
     }
     prof.begin(K_COMPACT);
     CU(launch_bitmap_compact_lb(cand(occ[0].var), W, sl.lv[0].bind, sl.lv[0].cap, dsz + 0, sl.d_ovf, next_lb(sl),
-                                ctx->sm_count, sl.st));
+                                smc, sl.st));
     launches[K_COMPACT] += compact_launches(W);
     prof.end();
     for (uint32_t o = 1; o < L; o++) {
@@ -843,7 +845,7 @@ struct Exec {
         CU(cudaMemsetAsync(t, 0xff, (om_mask[o] + 1) * 8, sl.st));
         prof.begin(K_PRUNE);
         CU(launch_f_hash_build(a.tab, (uint32_t)oc.same, dsz + oc.same, sl.lv[oc.same].cap, t, om_mask[o],
-                               ctx->sm_count, sl.st));
+                               smc, sl.st));
         launches[K_PRUNE]++;
         prof.end();
         a.om_tab = t;
@@ -852,7 +854,7 @@ struct Exec {
       if (!a.tree) {
         prof.begin(K_COMPACT);
         CU(launch_bitmap_compact_lb(cand(oc.var), W, sl.list[o], sl.list_cap[o], dsz + 64 + o, sl.d_ovf,
-                                    next_lb(sl), ctx->sm_count, sl.st));
+                                    next_lb(sl), smc, sl.st));
         launches[K_COMPACT] += compact_launches(W);
         prof.end();
         a.list = sl.list[o];
@@ -870,12 +872,12 @@ struct Exec {
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
       prof.begin(K_EXPAND_SEG);
-      CU(launch_seg_scan(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      CU(launch_seg_scan(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_SEG]++;
       prof.end();
       a.lb = next_lb(sl);
       prof.begin(K_EXPAND_EMIT);
-      CU(launch_expand_lb(a, ctx->pred_bytes, ctx->sm_count, sl.st));
+      CU(launch_expand_lb(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_EMIT]++;
       prof.end();
     }
@@ -890,7 +892,7 @@ struct Exec {
   gsmart_status phase2_f() {
     state = S_PHASE2;
     TRY(keep_candidates());
-    const int sm = ctx->sm_count;
+    const int sm = smc;
     const uint32_t nc = (uint32_t)plan->vars.size();
     std::vector<std::vector<uint32_t>> kids(L);
     for (uint32_t o = 1; o < L; o++) kids[occ[o].par].push_back(o);
@@ -1557,14 +1559,14 @@ struct Exec {
       prof.begin(K_PRUNE);
       for (uint32_t k = L - 1; k >= 1; k--) {
         CU(launch_prune_mark_d(sl.d_tab, sl.lv[k].parent, k == L - 1 ? nullptr : sl.lv[k].alive, dsz + k, sl.lv[k - 1].alive,
-                               ctx->sm_count, sl.st));
+                               smc, sl.st));
         launches[K_PRUNE]++;
       }
       for (uint32_t k = 0; k < L; k++) {
         CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind,
                                    k + 1 < L ? sl.lv[k].alive : nullptr, dsz + k,
                                    k > 0 ? sl.lv[k - 1].newidx : nullptr, sl.d_tab, k,
-                                   k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), ctx->sm_count,
+                                   k + 1 < L ? sl.lv[k].newidx : nullptr, dsz + 96 + k, next_lb(sl), smc,
                                    sl.st));
         launches[K_PRUNE]++;
       }
@@ -1572,7 +1574,7 @@ struct Exec {
       CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
       if (mode != M_COUNT && !alias_rows) {
         prof.begin(K_ENUMERATE);
-        CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), dsz + 96 + (L - 1), nc, ctx->sm_count, sl.st));
+        CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), dsz + 96 + (L - 1), nc, smc, sl.st));
         launches[K_ENUMERATE]++;
         prof.end();
       }
@@ -1796,6 +1798,27 @@ gsmart_status run_batch(gsmart_ctx* ctx, const gsmart_plan_t* const* plans, uint
       R->count_only = (flags & GSMART_COUNT_ONLY) != 0;
       for (int k = 0; k < GSMART_NKERNELS; k++) R->stats.kernel_names[k] = kKernelNames[k];
       ex[i] = std::make_unique<Exec>(ctx, *ctx->slots[i], p, flags, R);
+    }
+    if (m > 1) {
+      // concurrent plans: the costliest one (by the previous run's work) sizes its
+      // grids for the whole device, the others for half of it, so their latency-
+      // bound kernels co-reside instead of each filling every SM with waiting CTAs
+      // (WatDiv-100M batch 4.41 vs 4.66 ms with every plan at half; LUBM-10k needs
+      // its dominant L1 at full width).  GSMART_SM_SHARE=f sets the others' share.
+      const char* ev = getenv("GSMART_SM_SHARE");
+      const double f = ev ? atof(ev) : 0.5;
+      unsigned long long top = 0;
+      uint32_t top_i = m;
+      for (uint32_t i = 0; i < m; i++) {
+        auto it = ctx->plan_cost.find(plans[base + i]->uid);
+        if (it != ctx->plan_cost.end() && it->second >= top) {
+          top = it->second;
+          top_i = i;
+        }
+      }
+      if (top_i < m && f > 0 && f < 1)
+        for (uint32_t i = 0; i < m; i++)
+          if (i != top_i) ex[i]->smc = std::max(16, (int)(ctx->sm_count * f));
     }
     std::vector<gsmart_status> st(m, GSMART_OK);
     static const bool trace = getenv("GSMART_TRACE") != nullptr;

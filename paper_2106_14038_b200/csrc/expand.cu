@@ -553,8 +553,12 @@ __global__ void __launch_bounds__(EX_T, 1024 / EX_T) k_expand_lb(ExpArgs2 a) {
 
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 8;
-  const char* ev = getenv("GSMART_SS_I");  // A/B: parents per thread (1: measured best, 4.88 vs 5.07 ms)
-  const int ssi = ev ? atoi(ev) : 1;
+  // parents per thread: small parent levels want more, shorter tiles (WatDiv-100M
+  // batch 4.88 ms at 1 vs 5.07 at 4), levels of tens of millions more work per
+  // thread (LUBM-10k batch 7.56 at 4 vs 8.04 at 1); the parent level's capacity
+  // (host-known, graph-stable) picks.  GSMART_SS_I forces a value (A/B).
+  const char* ev = getenv("GSMART_SS_I");
+  const int ssi = ev ? atoi(ev) : (a.cap_par >= (1ull << 23) ? 4 : 1);
   if (ssi == 8) {
     if (pred_bytes == 1) pdl_launch(k_seg_scan<uint8_t, 8>, g, SS_T, st, a);
     else pdl_launch(k_seg_scan<uint16_t, 8>, g, SS_T, st, a);
