@@ -1562,7 +1562,10 @@ struct Exec {
                                smc, sl.st));
         launches[K_PRUNE]++;
       }
-      for (uint32_t k = 0; k < L; k++) {
+      // rows wanted and >= 2 levels: the last level's compaction (a copy) happens
+      // inside the enumeration
+      const bool fuse_last = L >= 2 && mode != M_COUNT && !alias_rows;
+      for (uint32_t k = 0; k < (fuse_last ? L - 1 : L); k++) {
         CU(launch_compact_alive_lb(k > 0 ? sl.lv[k].parent : nullptr, sl.lv[k].bind,
                                    k + 1 < L ? sl.lv[k].alive : nullptr, dsz + k,
                                    k > 0 ? sl.lv[k - 1].newidx : nullptr, sl.d_tab, k,
@@ -1571,13 +1574,21 @@ struct Exec {
         launches[K_PRUNE]++;
       }
       prof.end();
-      CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
       if (mode != M_COUNT && !alias_rows) {
+        LastLevel lf;
+        if (fuse_last) {
+          lf.bind = sl.lv[L - 1].bind;
+          lf.parent = sl.lv[L - 1].parent;
+          lf.newidx_prev = sl.lv[L - 2].newidx;
+          lf.d_n_out = dsz + 96 + (L - 1);
+        }
         prof.begin(K_ENUMERATE);
-        CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), dsz + 96 + (L - 1), nc, smc, sl.st));
+        CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), fuse_last ? dsz + (L - 1) : dsz + 96 + (L - 1), nc,
+                            smc, sl.st, lf));
         launches[K_ENUMERATE]++;
         prof.end();
       }
+      CU(cudaMemcpyAsync(sl.h_pin + 128, dsz + 96, 32 * 8, cudaMemcpyDeviceToHost, sl.st));
       if (mode == M_SORT_SMALL) {
         prof.begin(K_SORT_ROWS);
         CU(sort_rows_small(sl.d_tab, dsz + 96 + (L - 1), nc, sl.st, &launches[K_SORT_ROWS]));

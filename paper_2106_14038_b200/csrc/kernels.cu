@@ -1304,20 +1304,36 @@ struct ColMap {
 // CTA writes the tile's contiguous n_cols * 256 words with coalesced stores
 // (a direct store per column would touch n_cols * 32 scattered words per warp).
 constexpr int EN_T = 256;
+// Fused last level (lf.bind != null): every node of the last trie level is a
+// solution (a8 removes none), so its compaction is a copy — the kernel reads the
+// uncompacted level, remaps parents through the previous level's new indices,
+// writes the compacted level into the result and the rows in the same pass.
 __global__ void __launch_bounds__(EN_T) k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
-                                                   const unsigned long long* __restrict__ d_n_last, uint32_t n_cols) {
+                                                   const unsigned long long* __restrict__ d_n_last, uint32_t n_cols,
+                                                   LastLevel lf) {
   GSM_PDL_ENTRY();
   if (!ot->go) return;
   extern __shared__ uint32_t s_rows[];
   const uint32_t n_last = (uint32_t)*d_n_last;
   uint32_t* __restrict__ rows = ot->rows;
   uint32_t* __restrict__ rank = ot->rank;
+  const bool fused = lf.bind != nullptr;
+  if (fused && blockIdx.x == 0 && threadIdx.x == 0) *lf.d_n_out = n_last;
   for (uint64_t base = (uint64_t)blockIdx.x * EN_T; base < n_last; base += (uint64_t)gridDim.x * EN_T) {
     const uint64_t m = base + threadIdx.x;
     if (m < n_last) {
       uint32_t idx = (uint32_t)m;
       uint32_t* r = s_rows + threadIdx.x * n_cols;
-      for (int k = (int)L - 1; k >= 0; k--) {
+      int k = (int)L - 1;
+      if (fused) {
+        const uint32_t b = __ldcs(lf.bind + m), p = __ldg(lf.newidx_prev + __ldcs(lf.parent + m));
+        __stcs(ot->bind[k] + m, b);
+        __stcs(ot->parent[k] + m, p);
+        r[cm.c[k]] = b;
+        idx = p;
+        k--;
+      }
+      for (; k >= 0; k--) {
         r[cm.c[k]] = __ldg(ot->bind[k] + idx);
         if (k > 0) idx = __ldg(ot->parent[k] + idx);
       }
@@ -1333,7 +1349,8 @@ __global__ void __launch_bounds__(EN_T) k_enumerate(const OutTab* __restrict__ o
 }
 
 cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
-                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st) {
+                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st,
+                             LastLevel lf) {
   ColMap cm;
   for (uint32_t k = 0; k < MAXL; k++) cm.c[k] = k < n_levels ? col_of_level[k] : 0;
   const size_t smem = (size_t)EN_T * n_cols * 4;
@@ -1342,7 +1359,7 @@ cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t
     cudaFuncSetAttribute(k_enumerate, cudaFuncAttributeMaxDynamicSharedMemorySize, EN_T * MAXL * 4);
     attr = true;
   }
-  pdl_launch_smem(k_enumerate, (unsigned)sm_count * 8, EN_T, smem, st, ot, n_levels, cm, d_n_last, n_cols);
+  pdl_launch_smem(k_enumerate, (unsigned)sm_count * 8, EN_T, smem, st, ot, n_levels, cm, d_n_last, n_cols, lf);
   return cudaGetLastError();
 }
 

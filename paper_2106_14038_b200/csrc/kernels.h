@@ -371,8 +371,18 @@ cudaError_t launch_compact_alive_lb(const uint32_t* parent, const uint32_t* bind
 
 // ----------------------------------------------------------------- a8 prune, a9 rows
 // one row per leaf; n_last read from device memory (grid-stride)
+// the uncompacted last level (its compaction fused into the enumeration): raw
+// bindings/parents, the previous level's new indices, where to write its count
+struct LastLevel {
+  const uint32_t* bind = nullptr;
+  const uint32_t* parent = nullptr;
+  const uint32_t* newidx_prev = nullptr;
+  unsigned long long* d_n_out = nullptr;
+};
+// d_n_last: rows (= nodes of the last level; with lf.bind its uncompacted count)
 cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
-                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st);
+                             const unsigned long long* d_n_last, uint32_t n_cols, int sm_count, cudaStream_t st,
+                             LastLevel lf = LastLevel());
 // rank sort of ot->rows into ot->sorted for n (device) <= SORT_SMALL_MAXN, n_cols <= SORT_SMALL_MAXC
 inline bool sort_small_ok(uint64_t n, uint32_t n_cols) { return n <= SORT_SMALL_MAXN && n_cols <= SORT_SMALL_MAXC; }
 cudaError_t sort_rows_small(const OutTab* ot, const unsigned long long* d_n, uint32_t n_cols, cudaStream_t st,
