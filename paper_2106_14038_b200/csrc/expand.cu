@@ -215,6 +215,15 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
                                      unsigned long long* d_count, int* overflow, LBArgs lb, int sm_count,
                                      cudaStream_t st, uint32_t id_base, SkipIf skip) {
   if (n_words == 0) return cudaMemsetAsync(d_count, 0, 8, st);
+  const char* ev = getenv("GSMART_BC_W");  // A/B: words per lane per slice (8 default, 1)
+  if (ev && atoi(ev) == 1) {
+    const uint32_t chunk = bc_chunk_words<1>(n_words, sm_count);
+    const uint32_t nch = (n_words + chunk - 1) / chunk;
+    if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
+    pdl_launch(k_bitmap_compact<1>, nch, BC_T, st, bm, n_words, chunk, ids, cap, d_count, overflow, lb, id_base,
+               skip);
+    return cudaGetLastError();
+  }
   const uint32_t chunk = bc_chunk_words<BC_W_DEFAULT>(n_words, sm_count);
   const uint32_t nch = (n_words + chunk - 1) / chunk;
   if (nch > BC_MAX_CHUNKS || nch > lb.cap_tiles) return cudaErrorInvalidValue;
