@@ -270,9 +270,15 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
 #pragma unroll
       for (int j = 0; j < SS_I; j++)
         b[j] = ((act >> j) & 1u) ? anc_binding(a, a.par_idx, (uint32_t)(base + j), a.parent_level) : 0u;
+      // consecutive nodes of a thread with the same parent-side binding (a run
+      // under one ancestor) share its segment: only the first of a run searches
+      uint32_t srch = act;
+#pragma unroll
+      for (int j = 1; j < SS_I; j++)
+        if (((act >> j) & 1u) && b[j] == b[j - 1]) srch &= ~(1u << j);
 #pragma unroll
       for (int j = 0; j < SS_I; j++)
-        if ((act >> j) & 1u) {
+        if ((srch >> j) & 1u) {
           lo[j] = __ldg(f.rp + b[j]);
           e[j] = hi[j] = __ldg(f.rp + b[j] + 1);
         }
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
 #pragma unroll
       for (int pass = 0; pass < 2; pass++) {
         const uint32_t key = a.label + (uint32_t)pass;
-        uint32_t live = act;
+        uint32_t live = srch;
         while (live) {
 #pragma unroll
           for (int j = 0; j < SS_I; j++) {
@@ -307,6 +313,12 @@ __global__ void __launch_bounds__(SS_T) k_seg_scan(ExpArgs2 a) {
           }
         }
       }
+#pragma unroll
+      for (int j = 1; j < SS_I; j++)
+        if (((act >> j) & 1u) && !((srch >> j) & 1u)) {
+          lo[j] = lo[j - 1];
+          hi[j] = hi[j - 1];
+        }
     }
 #pragma unroll
     for (int j = 0; j < SS_I; j++) {
