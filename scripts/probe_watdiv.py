@@ -77,5 +77,11 @@ if args.oracle or args.parity:
             got = G.gsmart_result_rows(r)
             G.gsmart_result_free(r)
             line += f" parity={got.shape == exp.shape and np.array_equal(got, exp)}"
+            r = G.gsmart_execute(eng.ctx, pl, G.GSMART_FACTORISED)  # f2: rows read off the factorised trees
+            got = G.gsmart_result_rows(r)
+            fst = G.gsmart_result_stats(r)
+            G.gsmart_result_free(r)
+            line += (f" factorised_parity={got.shape == exp.shape and np.array_equal(got, exp)}"
+                     f" (omega={fst['n_omega']} nodes={sum(fst['level_nodes'])})")
         print(line, flush=True)
 eng.close()
