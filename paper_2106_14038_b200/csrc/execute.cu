@@ -785,6 +785,13 @@ struct Exec {
       a.overflow = sl.d_ovf;
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
+      if (a.tree && functional_edge(a.dir & 1, Lv.label)) {  // <= 1 child per parent: one fused pass
+        prof.begin(K_EXPAND_EMIT);
+        CU(launch_expand_func(a, ctx->pred_bytes, smc, sl.st));
+        launches[K_EXPAND_EMIT]++;
+        prof.end();
+        continue;
+      }
       prof.begin(K_EXPAND_SEG);
       CU(launch_seg_scan(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_SEG]++;
@@ -797,6 +804,14 @@ struct Exec {
     }
     CU(cudaMemcpyAsync(sl.h_pin, dsz, 128 * 8, cudaMemcpyDeviceToHost, sl.st));
     return GSMART_OK;
+  }
+
+  // a tree edge over `label` read from format `fmt`'s rows reaches at most one child
+  // per parent (exact build statistic); GSMART_NO_FUNC=1 disables the fused pass (A/B)
+  bool functional_edge(uint32_t fmt, uint32_t label) const {
+    const char* ev = getenv("GSMART_NO_FUNC");
+    const auto& fu = ctx->f[fmt].functional;
+    return !(ev && atoi(ev) != 0) && label < fu.size() && fu[label];
   }
 
   // f2: level 0 as in the trie, then every occurrence from its parent occurrence

@@ -572,6 +572,112 @@ __global__ void __launch_bounds__(EX_T, 1024 / EX_T) k_expand_lb(ExpArgs2 a) {
   }
 }
 
+// ------------------------------------------------------------------ level k: functional tree edge
+// The tree edge's label holds at most one entry per row of the parent's format
+// (Lspm::functional, exact from the build): every parent has 0 or 1 child, so
+// the segment scan and the load-balanced emit collapse into one pass — per
+// parent (one per thread): its binding, the label's first entry in its row,
+// the child, candidate probe, closing checks; a block scan + look-back keeps
+// the emit order (parent[] non-decreasing).
+template <typename PT>
+__device__ __forceinline__ bool closing_ok1(const ExpArgs2& a, const Fmt<PT>& f0, const Fmt<PT>& f1, bool csr_only,
+                                           uint32_t child, uint32_t node) {
+  for (uint32_t q = 0; q < a.ncl; q++) {
+    const ClosingDev cl = a.cl[q];
+    // (c, l, tgt) in the child's row of format dir <=> (tgt, l, c) in tgt's row of the other
+    const Fmt<PT>& fc = cl.dir ? f1 : f0;
+    const Fmt<PT>& fo = cl.dir ? f0 : f1;
+    const uint32_t tgt = cl.self ? child : anc_binding(a, a.cl_idx[q], node, cl.other_level);
+    const bool use_c = !csr_only || cl.dir == 0, use_g = !csr_only || cl.dir == 1;
+    const uint32_t c0 = use_c ? __ldg(fc.rp + child) : 0u, c1 = use_c ? __ldg(fc.rp + child + 1) : 0u;
+    const uint32_t g0 = use_g ? __ldg(fo.rp + tgt) : 0u, g1 = use_g ? __ldg(fo.rp + tgt + 1) : 0u;
+    const bool useo = csr_only ? cl.dir == 1 : (g1 - g0) < (c1 - c0);
+    const uint32_t key = useo ? child : tgt;
+    uint32_t lo = useo ? g0 : c0, hi = useo ? g1 : c1;
+    const PT* pr = useo ? fo.pred : fc.pred;
+    const uint32_t* co = useo ? fo.col : fc.col;
+    bool found = false;
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      const uint32_t p = __ldg(pr + m), cc = __ldg(co + m);
+      if (p == cl.label && cc == key) {
+        found = true;
+        break;
+      }
+      if (p < cl.label || (p == cl.label && cc < key)) lo = m + 1; else hi = m;
+    }
+    if (!found) return false;
+  }
+  return true;
+}
+
+constexpr int FX_T = 256;
+
+template <typename PT>
+__global__ void __launch_bounds__(FX_T) k_expand_func(ExpArgs2 a) {
+  GSM_PDL_ENTRY();
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_red[32];
+  __shared__ unsigned long long s_pref;
+  const uint64_t F = *a.d_nparent;
+  if (F > a.cap_par) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.overflow, 1);
+    return;
+  }
+  const uint32_t ntiles = (uint32_t)((F + FX_T - 1) / FX_T);
+  const Fmt<PT> fsrc = fmt_of<PT>(a.f[a.dir & 1]);
+  const Fmt<PT> f0 = fmt_of<PT>(a.f[0]), f1 = fmt_of<PT>(a.f[1]);
+  const bool csr_only = a.closing_csr != 0 || a.f[1].rp == nullptr;
+  unsigned long long n_exam = 0;
+  while (true) {
+    const uint32_t tile = lb_claim(a.lb.counter(), &s_tile);
+    if (tile >= ntiles) break;
+    const uint64_t n = (uint64_t)tile * FX_T + threadIdx.x;
+    uint32_t child = 0;
+    bool keep = false;
+    if (n < F) {
+      const uint32_t b = anc_binding(a, a.par_idx, (uint32_t)n, a.parent_level);
+      const uint32_t e = __ldg(fsrc.rp + b + 1);
+      uint32_t lo = __ldg(fsrc.rp + b), hi = e;
+      while (lo < hi) {  // first entry with label >= l
+        const uint32_t m = (lo + hi) >> 1;
+        if ((uint32_t)__ldg(fsrc.pred + m) < a.label) lo = m + 1; else hi = m;
+      }
+      if (lo < e && (uint32_t)__ldg(fsrc.pred + lo) == a.label) {
+        child = __ldg(fsrc.col + lo);
+        n_exam++;
+        keep = bit_of(a.cand, child) && closing_ok1<PT>(a, f0, f1, csr_only, child, (uint32_t)n);
+      }
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_scan<unsigned long long>(keep ? 1ull : 0ull, s_red, &tot);
+    const uint64_t pref = lb_prefix(a.lb.status, a.lb.epoch(), tile, tot, &s_pref);
+    if (pref + tot > a.cap_out) {  // capacity: flag, the host grows and re-runs
+      if (threadIdx.x == 0 && tot) atomicOr(a.overflow, 1);
+      keep = false;
+    }
+    if (keep) {
+      const uint64_t pos = pref + ex;
+      a.out_parent[pos] = (uint32_t)n;
+      a.out_bind[pos] = child;
+      if (a.out_alive) a.out_alive[pos] = 0;
+      for (uint32_t i = 0; i < a.n_anc_out; i++)
+        a.out_anc[i][pos] = a.anc_src[i] == ANC_BIND ? __ldg(a.tab.bind[a.k - 1] + n) : __ldg(a.par_anc[a.anc_src[i]] + n);
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) *a.d_nout = pref + tot;
+  }
+  if (ntiles == 0 && blockIdx.x == 0 && threadIdx.x == 0) *a.d_nout = 0;
+  n_exam = __reduce_add_sync(GSM_FULL, (uint32_t)n_exam);
+  if ((threadIdx.x & 31) == 0 && n_exam) atomicAdd(a.ctr + C_EXPAND, n_exam);
+}
+
+cudaError_t launch_expand_func(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
+  const unsigned g = (unsigned)sm_count * 8;
+  if (pred_bytes == 1) pdl_launch(k_expand_func<uint8_t>, g, FX_T, st, a);
+  else pdl_launch(k_expand_func<uint16_t>, g, FX_T, st, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st) {
   unsigned g = (unsigned)sm_count * 8;
   // parents per thread: small parent levels want more, shorter tiles (WatDiv-100M

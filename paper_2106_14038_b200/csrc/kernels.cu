@@ -350,10 +350,13 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // labels < LR_MAX): the fan-out statistics of the trie order.
 constexpr uint32_t LR_MAX = 4096;
 
+// Also (every row, exact): nonfunc bit l is set iff some row holds >= 2 entries
+// with label l — a pattern with label l seen from this format's rows then has
+// at most one child per parent (a "functional" level, expanded by k_expand_func).
 template <typename PT>
 __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restrict__ pred, uint32_t n_rows,
                              uint32_t* __restrict__ lmask, unsigned long long* __restrict__ label_rows,
-                             uint32_t n_labels) {
+                             uint32_t n_labels, uint32_t* __restrict__ nonfunc) {
   extern __shared__ uint32_t s_lr[];
   const bool count = label_rows != nullptr;
   if (count) {  // [0, n_labels): rows holding the label, [n_labels, 2 n_labels): its entries
@@ -380,6 +383,8 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
         }
         k = lo;
       }
+      if (nonfunc && k - k0 > 1 && !((__ldcg(nonfunc + (l >> 5)) >> (l & 31)) & 1u))
+        atomicOr(nonfunc + (l >> 5), 1u << (l & 31));
       if (count && (r & 15u) == 0 && l < n_labels) {  // a 1-in-16 row sample: the ratio is what matters
         atomicAdd(&s_lr[l], 1u);
         atomicAdd(&s_lr[n_labels + l], k - k0);
@@ -395,14 +400,15 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
 }
 
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
-                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st) {
+                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st,
+                              uint32_t* nonfunc) {
   const unsigned g = grid_for(n_rows, 256, 148 * 16);
   if (n_labels > LR_MAX) label_rows = nullptr;
   const size_t sm = label_rows ? (size_t)n_labels * 8 : 0;
   if (pred_bytes == 1)
-    k_label_mask<uint8_t><<<g, 256, sm, st>>>(rp, (const uint8_t*)pred, n_rows, lmask, label_rows, n_labels);
+    k_label_mask<uint8_t><<<g, 256, sm, st>>>(rp, (const uint8_t*)pred, n_rows, lmask, label_rows, n_labels, nonfunc);
   else
-    k_label_mask<uint16_t><<<g, 256, sm, st>>>(rp, (const uint16_t*)pred, n_rows, lmask, label_rows, n_labels);
+    k_label_mask<uint16_t><<<g, 256, sm, st>>>(rp, (const uint16_t*)pred, n_rows, lmask, label_rows, n_labels, nonfunc);
   return cudaGetLastError();
 }
 

@@ -103,7 +103,8 @@ cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* 
 // label_rows (optional, n_labels <= 4096; 2 n_labels words): over every 16th row,
 // [l] += rows holding label l, [n_labels + l] += its entries (fan-out statistics)
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
-                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st);
+                              uint32_t* lmask, unsigned long long* label_rows, uint32_t n_labels, cudaStream_t st,
+                              uint32_t* nonfunc = nullptr);
 
 // ----------------------------------------------------------------- bitmaps
 cudaError_t launch_fill_ones(uint32_t* bm, uint32_t n_words, uint32_t n_bits, cudaStream_t st);
@@ -342,6 +343,8 @@ cudaError_t launch_bitmap_compact_lb(const uint32_t* bm, uint32_t n_words, uint3
                                      cudaStream_t st, uint32_t id_base = 0, SkipIf skip = SkipIf());
 cudaError_t launch_seg_scan(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 cudaError_t launch_expand_lb(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
+// one launch for a level whose tree-edge label is functional in the parent's format
+cudaError_t launch_expand_func(const ExpArgs2& a, int pred_bytes, int sm_count, cudaStream_t st);
 struct OutTab;
 cudaError_t launch_prune_mark_d(const OutTab* ot, const uint32_t* parent, const uint8_t* alive, const unsigned long long* d_n,
                                 uint8_t* alive_prev, int sm_count, cudaStream_t st);

@@ -448,6 +448,24 @@ static gsmart_status label_rows_readback(gsmart_ctx* ctx, const unsigned long lo
   return GSMART_OK;
 }
 
+// functional labels of a format (no row holds two entries of the label; OR of
+// the ranks' non-functional bits when world > 1)
+static gsmart_status functional_readback(gsmart_ctx* ctx, const uint32_t* d, std::vector<uint8_t>* out) {
+  const size_t words = ((size_t)ctx->P + 1 + 31) / 32;
+  std::vector<uint32_t> h(words);
+  CU(cudaMemcpyAsync(h.data(), d, words * 4, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  if (ctx->world > 1) {
+    std::vector<uint32_t> all(words * ctx->world);
+    TRY(host_allgather(ctx, h.data(), words * 4, all.data()));
+    for (size_t i = 0; i < words; i++)
+      for (int q = 0; q < ctx->world; q++) h[i] |= all[(size_t)q * words + i];
+  }
+  out->assign((size_t)ctx->P + 1, 0);
+  for (size_t l = 0; l <= ctx->P; l++) (*out)[l] = ((h[l >> 5] >> (l & 31)) & 1u) ? 0 : 1;
+  return GSMART_OK;
+}
+
 static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
   Lspm& L = ctx->f[fmt];
   const uint64_t n = ctx->n_triples;
@@ -505,8 +523,13 @@ static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* 
   unsigned long long* lrows = nullptr;
   TRY(sc.get(&lrows, 2 * ((uint64_t)ctx->P + 1)));
   CU(cudaMemsetAsync(lrows, 0, ((size_t)ctx->P + 1) * 16, ctx->st));
-  if (nloc) CU(launch_label_mask(L.rp + rlo, L.pred, pbytes, nloc, L.lmask + rlo, lrows, ctx->P + 1, ctx->st));
+  uint32_t* nonfunc = nullptr;
+  TRY(sc.get(&nonfunc, ((uint64_t)ctx->P + 1 + 31) / 32));
+  CU(cudaMemsetAsync(nonfunc, 0, ((size_t)ctx->P + 1 + 31) / 32 * 4, ctx->st));
+  if (nloc)
+    CU(launch_label_mask(L.rp + rlo, L.pred, pbytes, nloc, L.lmask + rlo, lrows, ctx->P + 1, ctx->st, nonfunc));
   TRY(label_rows_readback(ctx, lrows, &L.label_rows));
+  TRY(functional_readback(ctx, nonfunc, &L.functional));
   CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
   if (nloc) CU(launch_heavy_stats(L.rp + rlo, nloc, ctx->d_ctr + 42, ctx->st));
   unsigned long long hv[2];
@@ -552,8 +575,12 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
   unsigned long long* lrows = nullptr;
   TRY(sc.get(&lrows, 2 * ((uint64_t)ctx->P + 1)));
   CU(cudaMemsetAsync(lrows, 0, ((size_t)ctx->P + 1) * 16, ctx->st));
-  CU(launch_label_mask(L.rp, L.pred, ctx->pred_bytes, N, L.lmask, lrows, ctx->P + 1, ctx->st));
+  uint32_t* nonfunc = nullptr;
+  TRY(sc.get(&nonfunc, ((uint64_t)ctx->P + 1 + 31) / 32));
+  CU(cudaMemsetAsync(nonfunc, 0, ((size_t)ctx->P + 1 + 31) / 32 * 4, ctx->st));
+  CU(launch_label_mask(L.rp, L.pred, ctx->pred_bytes, N, L.lmask, lrows, ctx->P + 1, ctx->st, nonfunc));
   TRY(label_rows_readback(ctx, lrows, &L.label_rows));
+  TRY(functional_readback(ctx, nonfunc, &L.functional));
   CU(cudaMemsetAsync(ctx->d_ctr + 42, 0, 16, ctx->st));
   CU(launch_heavy_stats(L.rp, N, ctx->d_ctr + 42, ctx->st));
   unsigned long long hv[2];

@@ -59,6 +59,9 @@ struct Lspm {
   // [l]: rows holding label l, [P + 1 + l]: its entries (empty when P > 4095);
   // entries / rows = the expected fan-out of a pattern from this side
   std::vector<unsigned long long> label_rows;
+  // [l] = 1: no row holds two entries with label l (exact, every row): a trie
+  // level reached over label l from this format's rows is "functional"
+  std::vector<uint8_t> functional;
 };
 
 // Label-major entry lists: the kept, de-duplicated triples grouped by predicate,
