@@ -886,6 +886,13 @@ struct Exec {
       a.overflow = sl.d_ovf;
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
+      if (a.tree && !a.om_tab && functional_edge(a.dir & 1, oc.label)) {  // <= 1 child per parent
+        prof.begin(K_EXPAND_EMIT);
+        CU(launch_expand_func(a, ctx->pred_bytes, smc, sl.st));
+        launches[K_EXPAND_EMIT]++;
+        prof.end();
+        continue;
+      }
       prof.begin(K_EXPAND_SEG);
       CU(launch_seg_scan(a, ctx->pred_bytes, smc, sl.st));
       launches[K_EXPAND_SEG]++;
