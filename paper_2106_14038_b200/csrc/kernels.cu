@@ -359,10 +359,15 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
                              uint32_t n_labels, uint32_t* __restrict__ nonfunc) {
   extern __shared__ uint32_t s_lr[];
   const bool count = label_rows != nullptr;
+  // non-functional bits gathered per CTA in shared memory (a global word per
+  // label would be one L2 hot spot for every thread of the grid)
+  uint32_t* s_nf = s_lr + (count ? 2 * n_labels : 0);
+  const uint32_t nf_words = nonfunc ? (n_labels + 31) / 32 : 0;
+  for (uint32_t i = threadIdx.x; i < nf_words; i += blockDim.x) s_nf[i] = 0;
   if (count) {  // [0, n_labels): rows holding the label, [n_labels, 2 n_labels): its entries
     for (uint32_t i = threadIdx.x; i < 2 * n_labels; i += blockDim.x) s_lr[i] = 0;
-    __syncthreads();
   }
+  __syncthreads();
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
     uint32_t k = rp[r];
     const uint32_t e = rp[r + 1];
@@ -383,8 +388,8 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
         }
         k = lo;
       }
-      if (nonfunc && k - k0 > 1 && !((__ldcg(nonfunc + (l >> 5)) >> (l & 31)) & 1u))
-        atomicOr(nonfunc + (l >> 5), 1u << (l & 31));
+      if (nonfunc && k - k0 > 1 && l < n_labels && !((s_nf[l >> 5] >> (l & 31)) & 1u))
+        atomicOr(s_nf + (l >> 5), 1u << (l & 31));
       if (count && (r & 15u) == 0 && l < n_labels) {  // a 1-in-16 row sample: the ratio is what matters
         atomicAdd(&s_lr[l], 1u);
         atomicAdd(&s_lr[n_labels + l], k - k0);
@@ -392,11 +397,12 @@ __global__ void k_label_mask(const uint32_t* __restrict__ rp, const PT* __restri
     }
     lmask[r] = m;
   }
-  if (count) {
-    __syncthreads();
+  __syncthreads();
+  if (count)
     for (uint32_t i = threadIdx.x; i < 2 * n_labels; i += blockDim.x)
       if (s_lr[i]) atomicAdd(label_rows + i, (unsigned long long)s_lr[i]);
-  }
+  for (uint32_t i = threadIdx.x; i < nf_words; i += blockDim.x)
+    if (s_nf[i]) atomicOr(nonfunc + i, s_nf[i]);
 }
 
 cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_bytes, uint32_t n_rows,
@@ -404,7 +410,7 @@ cudaError_t launch_label_mask(const uint32_t* rp, const void* pred, int pred_byt
                               uint32_t* nonfunc) {
   const unsigned g = grid_for(n_rows, 256, 148 * 16);
   if (n_labels > LR_MAX) label_rows = nullptr;
-  const size_t sm = label_rows ? (size_t)n_labels * 8 : 0;
+  const size_t sm = (label_rows ? (size_t)n_labels * 8 : 0) + (nonfunc ? ((size_t)n_labels + 31) / 32 * 4 : 0);
   if (pred_bytes == 1)
     k_label_mask<uint8_t><<<g, 256, sm, st>>>(rp, (const uint8_t*)pred, n_rows, lmask, label_rows, n_labels, nonfunc);
   else
