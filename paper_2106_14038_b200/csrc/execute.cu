@@ -1075,6 +1075,7 @@ struct Exec {
       fo.col = occ[o].col;
       fo.same = occ[o].same;
       fo.leaf = kids[o].empty() ? 1 : 0;
+      fo.first = (o > 0 && kids[occ[o].par].front() == o) ? 1 : 0;
     }
     ea.n_occ = L;
     ea.n_root = (uint32_t)F[0];
@@ -1107,7 +1108,7 @@ struct Exec {
     TRY(sc.get(&raw, n_rows * nc));
     TRY(alloc_result((void**)&R->d_rows, n_rows * nc * 4));
     ea.count_only = 0;
-    ea.rows = raw;
+    ea.rows = R->d_rows;  // enumerated into the result, sorted in place (raw = scratch if unsorted)
     ea.cap_rows = n_rows;
     if (filtered) CU(cudaMemsetAsync(d_cnt, 0, 8, sl.st));
     prof.begin(K_ENUMERATE);
@@ -1119,7 +1120,7 @@ struct Exec {
     TRY(sc.get((char**)&tmp, std::max<size_t>(tb, 256)));
     prof.begin(K_SORT_ROWS);
     CU(sort_rows(raw, R->d_rows, n_rows, nc, nc, bits_for(ctx->N ? ctx->N - 1 : 0), tmp, tb, sl.st,
-                 &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50)));
+                 &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50), true));
     prof.end();
     return GSMART_OK;
   }

@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t f_pick(const unsigned long long* __restrict_
 __global__ void __launch_bounds__(256) k_f_enum(const FEnumArgs a) {
   GSM_PDL_ENTRY();
   uint32_t node[MAXOCC];
-  unsigned long long rem[MAXOCC];
+  unsigned long long rem[MAXOCC], dig[MAXOCC];
   const uint32_t lane = threadIdx.x & 31;
   for (unsigned long long g0 = blockIdx.x * (unsigned long long)blockDim.x + (threadIdx.x & ~31u); g0 < a.total;
        g0 += (unsigned long long)gridDim.x * blockDim.x) {
@@ -174,10 +174,22 @@ __global__ void __launch_bounds__(256) k_f_enum(const FEnumArgs a) {
       for (uint32_t o = 1; o < a.n_occ; o++) {
         const FOcc& oc = a.o[o];
         const uint32_t np = node[oc.par];
+        if (oc.first) {
+          // the parent's combination index splits over its child occurrences with the
+          // first one most significant, so rows come out ordered by the occurrences
+          // (= the trie's visitation order) and often need no sort: digits are taken
+          // from the last child occurrence backwards
+          for (int q = (int)a.n_occ - 1; q >= (int)o; q--) {
+            if (a.o[q].par != oc.par) continue;
+            const uint32_t bq = __ldg(a.o[q].beg + np), eq = __ldg(a.o[q].end + np);
+            const unsigned long long Sq = __ldg(a.o[q].P + eq) - __ldg(a.o[q].P + bq);
+            dig[q] = rem[oc.par] % Sq;
+            rem[oc.par] /= Sq;
+          }
+        }
         const uint32_t b = __ldg(oc.beg + np), e = __ldg(oc.end + np);
         const unsigned long long base = __ldg(oc.P + b), S = __ldg(oc.P + e) - base;
-        const unsigned long long i = rem[oc.par] % S;
-        rem[oc.par] /= S;
+        const unsigned long long i = dig[o];
         // a leaf occurrence whose children all live (counts 0/1 summing to e - b): direct index
         const uint32_t m = (oc.leaf && S == (unsigned long long)(e - b)) ? b + (uint32_t)i : f_pick(oc.P, b, e, base + i);
         node[o] = m;

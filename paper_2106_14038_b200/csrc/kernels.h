@@ -435,6 +435,7 @@ struct FOcc {               // one occurrence, as the enumeration reads it
   int col;                      // output column, -1 for a second occurrence (Ω)
   int same;                     // Ω: the first occurrence of the same variable, else -1
   int leaf;                     // no child occurrences: every node counts 0 or 1
+  int first;                    // the first child occurrence of its parent (splits the parent's index)
 };
 struct FEnumArgs {
   FOcc o[MAXOCC];
