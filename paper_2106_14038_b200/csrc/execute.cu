@@ -806,6 +806,26 @@ struct Exec {
     return GSMART_OK;
   }
 
+  // Rows leave the trie in visitation (pi-lexicographic) order.  They are also in
+  // column order when every level k that an earlier level d precedes in pi but
+  // follows in column order is determined by levels before d: the chain of
+  // functional tree edges above k reaches a level < d (two rows that first differ
+  // at d then agree on every column before d's).  Then no sort runs.
+  bool sorted_by_construction() const {
+    const uint32_t LT = (uint32_t)plan->levels.size();
+    std::vector<uint32_t> root(LT);  // anc_func: the top of k's chain of functional tree edges
+    for (uint32_t k = 0; k < LT; k++) {
+      const Level& Lv = plan->levels[k];
+      root[k] = (k > 0 && Lv.tree_edge >= 0 && functional_edge(Lv.dir == OUT ? 0u : 1u, Lv.label))
+                    ? root[Lv.parent_level]
+                    : k;
+    }
+    for (uint32_t d = 0; d < LT; d++)
+      for (uint32_t k = d + 1; k < LT; k++)
+        if (plan->col_of[plan->levels[k].var] < plan->col_of[plan->levels[d].var] && root[k] >= d) return false;
+    return true;
+  }
+
   // a tree edge over `label` read from format `fmt`'s rows reaches at most one child
   // per parent (exact build statistic); GSMART_NO_FUNC=1 disables the fused pass (A/B)
   bool functional_edge(uint32_t fmt, uint32_t label) const {
@@ -1353,6 +1373,7 @@ struct Exec {
     identity = true;
     for (uint32_t k = 0; k < L; k++)
       if ((uint32_t)plan->col_of[plan->levels[k].var] != k) identity = false;
+    if (!identity && !(flags & GSMART_FACTORISED)) identity = sorted_by_construction();
     R->n_words = W;
     R->stride_words = Wpad;
     slot.assign(plan->n_vertices, -1);
