@@ -1,6 +1,7 @@
 // sm_100a kernels of the gSmart hot path (§5-§8).
 // Every kernel here is HBM/L2-bound integer/boolean work: no tensor cores
 // (not a dense contraction — BASELINE.json north_star).
+#include <cstdlib>
 #include "kernels.h"
 
 namespace gsm {
@@ -1198,7 +1199,8 @@ __device__ __forceinline__ void push_load(const PushArgs& a, uint64_t b4, uint64
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_push_edge(PushArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_push_edge(PushArgs a) {
   GSM_PDL_ENTRY();
   if (a.skip.skip()) return;
   if (a.in_cnt && *(volatile const unsigned long long*)a.in_cnt == 0) return;  // no row left to mark
@@ -1265,8 +1267,12 @@ __global__ void __launch_bounds__(256, 3) k_push_edge(PushArgs a) {
 cudaError_t launch_push_edge(const PushArgs& a, int sm_count, cudaStream_t st) {
   const uint64_t n4 = a.end > a.beg ? (a.end - (a.beg & ~3ull) + 3) / 4 : 0;
   const uint64_t per_cta = 256ull * PU_G;
-  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n4 + per_cta - 1) / per_cta, (uint64_t)sm_count * 3));
-  return pdl_launch(k_push_edge, g, 256, st, a);
+  const char* ev = getenv("GSMART_PUSH_MINB");  // A/B: resident CTAs per SM (register budget)
+  const int mb = ev ? atoi(ev) : 3;
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n4 + per_cta - 1) / per_cta, (uint64_t)sm_count * mb));
+  if (mb == 4) return pdl_launch(k_push_edge<4>, g, 256, st, a);
+  if (mb == 6) return pdl_launch(k_push_edge<6>, g, 256, st, a);
+  return pdl_launch(k_push_edge<3>, g, 256, st, a);
 }
 
 // cand[0, n_words) &= sat — this rank's word range; world > 1: the new words are
