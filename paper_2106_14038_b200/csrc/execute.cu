@@ -1626,6 +1626,12 @@ struct Exec {
           lf.newidx_prev = sl.lv[L - 2].newidx;
           lf.d_n_out = dsz + 96 + (L - 1);
         }
+        if (mode == M_SORT_BIG) {  // the sortedness check rides along with the enumeration
+          int* fl = reinterpret_cast<int*>(sl.d_ctr + 50);
+          CU(cudaMemsetAsync(fl, 0, 4, sl.st));
+          CU(cudaMemsetAsync(fl, 1, 1, sl.st));
+          lf.sorted = fl;
+        }
         prof.begin(K_ENUMERATE);
         CU(launch_enumerate(sl.d_tab, L, col_of_level.data(), fuse_last ? dsz + (L - 1) : dsz + 96 + (L - 1), nc,
                             smc, sl.st, lf));
@@ -1652,7 +1658,7 @@ struct Exec {
       void* tmp = sl.p2 + al(n_rows * nc * 4);
       prof.begin(K_SORT_ROWS);
       CU(sort_rows((const uint32_t*)sl.p2, R->d_rows, n_rows, nc, n_key, bits_for(ctx->N - 1), tmp, tb, sl.st,
-                   &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50), true));
+                   &launches[K_SORT_ROWS], reinterpret_cast<int*>(sl.d_ctr + 50), true, true));
       prof.end();
     }
     return GSMART_OK;

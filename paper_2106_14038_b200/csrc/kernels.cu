@@ -1326,6 +1326,33 @@ constexpr int EN_T = 256;
 // solution (a8 removes none), so its compaction is a copy — the kernel reads the
 // uncompacted level, remaps parents through the previous level's new indices,
 // writes the compacted level into the result and the rows in the same pass.
+__device__ __forceinline__ void walk_row(const OutTab* __restrict__ ot, uint32_t L, const ColMap& cm,
+                                         const LastLevel& lf, uint32_t m, uint32_t* r, bool store_level) {
+  uint32_t idx = m;
+  int k = (int)L - 1;
+  if (lf.bind) {
+    const uint32_t b = __ldcs(lf.bind + m), p = __ldg(lf.newidx_prev + __ldcs(lf.parent + m));
+    if (store_level) {
+      __stcs(ot->bind[k] + m, b);
+      __stcs(ot->parent[k] + m, p);
+    }
+    r[cm.c[k]] = b;
+    idx = p;
+    k--;
+  }
+  for (; k >= 0; k--) {
+    r[cm.c[k]] = __ldg(ot->bind[k] + idx);
+    if (k > 0) idx = __ldg(ot->parent[k] + idx);
+  }
+}
+
+// lexicographic a > b over n columns
+__device__ __forceinline__ bool row_gt(const uint32_t* a, const uint32_t* b, uint32_t n) {
+  for (uint32_t c = 0; c < n; c++)
+    if (a[c] != b[c]) return a[c] > b[c];
+  return false;
+}
+
 __global__ void __launch_bounds__(EN_T) k_enumerate(const OutTab* __restrict__ ot, uint32_t L, ColMap cm,
                                                    const unsigned long long* __restrict__ d_n_last, uint32_t n_cols,
                                                    LastLevel lf) {
@@ -1335,35 +1362,31 @@ __global__ void __launch_bounds__(EN_T) k_enumerate(const OutTab* __restrict__ o
   const uint32_t n_last = (uint32_t)*d_n_last;
   uint32_t* __restrict__ rows = ot->rows;
   uint32_t* __restrict__ rank = ot->rank;
-  const bool fused = lf.bind != nullptr;
-  if (fused && blockIdx.x == 0 && threadIdx.x == 0) *lf.d_n_out = n_last;
+  if (lf.bind && blockIdx.x == 0 && threadIdx.x == 0) *lf.d_n_out = n_last;
+  bool descent = false;
   for (uint64_t base = (uint64_t)blockIdx.x * EN_T; base < n_last; base += (uint64_t)gridDim.x * EN_T) {
     const uint64_t m = base + threadIdx.x;
     if (m < n_last) {
-      uint32_t idx = (uint32_t)m;
-      uint32_t* r = s_rows + threadIdx.x * n_cols;
-      int k = (int)L - 1;
-      if (fused) {
-        const uint32_t b = __ldcs(lf.bind + m), p = __ldg(lf.newidx_prev + __ldcs(lf.parent + m));
-        __stcs(ot->bind[k] + m, b);
-        __stcs(ot->parent[k] + m, p);
-        r[cm.c[k]] = b;
-        idx = p;
-        k--;
-      }
-      for (; k >= 0; k--) {
-        r[cm.c[k]] = __ldg(ot->bind[k] + idx);
-        if (k > 0) idx = __ldg(ot->parent[k] + idx);
-      }
+      walk_row(ot, L, cm, lf, (uint32_t)m, s_rows + threadIdx.x * n_cols, true);
       if (rank && m < SORT_SMALL_MAXN) rank[m] = 0;  // the rank sort adds into it
     }
     __syncthreads();
+    if (lf.sorted && m < n_last) {  // the sort check rides along: each row against its predecessor
+      if (threadIdx.x > 0) {
+        descent = descent || row_gt(s_rows + (threadIdx.x - 1) * n_cols, s_rows + threadIdx.x * n_cols, n_cols);
+      } else if (base > 0) {  // the previous tile's last row, recomputed
+        uint32_t prev[MAXL];
+        walk_row(ot, L, cm, lf, (uint32_t)(base - 1), prev, false);
+        descent = descent || row_gt(prev, s_rows, n_cols);
+      }
+    }
     const uint64_t nr = min((uint64_t)EN_T, (uint64_t)n_last - base);
     const uint32_t words = (uint32_t)(nr * n_cols);
     uint32_t* out = rows + base * n_cols;
     for (uint32_t i = threadIdx.x; i < words; i += EN_T) __stcs(out + i, s_rows[i]);
     __syncthreads();
   }
+  if (lf.sorted && __any_sync(GSM_FULL, descent) && (threadIdx.x & 31) == 0) *lf.sorted = 0;
 }
 
 cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
@@ -1534,7 +1557,7 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols) {
 // sort, radix.cu, permutation as payload), least significant chunk first; stable.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
                       int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches, int* sorted_flag,
-                      bool inplace) {
+                      bool inplace, bool prechecked) {
   const size_t s4 = ((n * 4 + 255) / 256) * 256, s8 = ((n * 8 + 255) / 256) * 256;
   uint32_t* perm = (uint32_t*)tmp;
   uint32_t* perm2 = (uint32_t*)((char*)tmp + s4);
@@ -1545,7 +1568,13 @@ cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint
   unsigned g = grid_for(n, 256, 148 * 32);
   int nl = 1;
   if (inplace && !sorted_flag) return cudaErrorInvalidValue;
-  if (sorted_flag) {  // rows often arrive sorted (functional patterns first in the trie): check once
+  if (sorted_flag && prechecked) {  // the enumeration already set the flag
+    if (inplace) {
+      pdl_launch(k_copy_unless_sorted, grid_for(n * n_cols / 4 + 1, 256, 148 * 32), 256, st, (const uint32_t*)rows_out,
+                 const_cast<uint32_t*>(rows), n * n_cols, (const int*)sorted_flag);
+      nl++;
+    }
+  } else if (sorted_flag) {  // rows often arrive sorted (functional patterns first in the trie): check once
     cudaError_t e = cudaMemsetAsync(sorted_flag, 0, 4, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(sorted_flag, 1, 1, st);  // little-endian int 1
     if (e != cudaSuccess) return e;

@@ -381,6 +381,7 @@ struct LastLevel {
   const uint32_t* parent = nullptr;
   const uint32_t* newidx_prev = nullptr;
   unsigned long long* d_n_out = nullptr;
+  int* sorted = nullptr;  // set to 1 beforehand: cleared if a row is smaller than its predecessor
 };
 // d_n_last: rows (= nodes of the last level; with lf.bind its uncompacted count)
 cudaError_t launch_enumerate(const OutTab* ot, uint32_t n_levels, const uint32_t* col_of_level,
@@ -401,7 +402,7 @@ size_t sort_rows_tmp_bytes(uint64_t n, uint32_t n_cols);
 // when the rows turn out unsorted); needs sorted_flag.
 cudaError_t sort_rows(const uint32_t* rows, uint32_t* rows_out, uint64_t n, uint32_t n_cols, uint32_t n_key,
                       int key_bits, void* tmp, size_t tmp_bytes, cudaStream_t st, int* launches,
-                      int* sorted_flag = nullptr, bool inplace = false);
+                      int* sorted_flag = nullptr, bool inplace = false, bool prechecked = false);
 
 
 // ----------------------------------------------------------------- f2 factorised trees (factorised.cu)
