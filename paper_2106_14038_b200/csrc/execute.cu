@@ -404,6 +404,17 @@ struct Exec {
     }
     if (occ.size() > (size_t)MAXOCC || occ.size() > (size_t)GSMART_MAX_LEVELS)
       FAIL(GSMART_E_UNSUPPORTED, "GSMART_FACTORISED: more than 32 occurrences");
+    // a second occurrence reads its center's row in the pattern's direction, which
+    // the trie never does: that format must hold the label (keep-sets, CSR-only)
+    for (size_t o = 1; o < occ.size(); o++) {
+      if (!occ[o].tree) continue;
+      const int fmt = occ[o].dir == OUT ? 0 : 1;
+      const auto& kp = ctx->keep[fmt];
+      if (!ctx->f[fmt].built || (occ[o].label < kp.size() && !kp[occ[o].label]))
+        FAIL(GSMART_E_STATE, std::string("GSMART_FACTORISED: the ") + (fmt ? "CSC" : "CSR") +
+                                 " LSpM does not hold predicate " + std::to_string(occ[o].label) +
+                                 " that an occurrence expands over (build it with that label)");
+    }
     return GSMART_OK;
   }
 

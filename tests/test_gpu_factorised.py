@@ -202,3 +202,37 @@ def test_skewed_graphs_rows(G, eng, seed, N, P, M, skew):
             continue
         got = eng.query(q, flags=G.GSMART_FACTORISED)
         assert got.shape == exp.shape and np.array_equal(got, exp), q
+
+
+def test_direction_plans_rows(G, eng):
+    """Direction-driven plans (multi-root, §8.2's Φ variables as occurrences)."""
+    n = 0
+    for seed in range(300):
+        (s, p, o), nn, P, q = tiny.random_case(40000 + seed, n_consts=0)
+        exp = R.brute_force(s, p, o, nn, q)
+        eng.load(s, p, o, nn, P)
+        with eng.plan(q, traversal=G.GSMART_DIRECTION) as pl:
+            got = pl.run(flags=G.GSMART_FACTORISED)
+        assert _rows(got) == exp, (seed, q)
+        n += 1
+    assert n == 300
+
+
+def test_split_keep_sets_refused_or_exact(G, eng):
+    """With query-dependent keep-sets a second occurrence may need a label its
+    format does not hold: the execute is refused (E_STATE), never wrong."""
+    s, p, o = fixtures.fig1_triples()
+    q = fixtures.fig2_query()
+    exp = R.brute_force(s, p, o, 8, q)
+    eng.load(s, p, o, 8, 4)
+    with eng.plan(q) as pl:
+        csr, csc = G.gsmart_plan_keep_sets([pl.h])
+    G.gsmart_build_lspm_split(eng.ctx, csr, csc)
+    with eng.plan(q) as pl:
+        assert _rows(pl.run()) == exp  # the trie reads only what the keep-sets hold
+        try:
+            got = pl.run(flags=G.GSMART_FACTORISED)
+        except G.GsmartError as e:
+            assert "E_STATE" in str(e), e
+        else:
+            assert _rows(got) == exp
