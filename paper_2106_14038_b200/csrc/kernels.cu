@@ -181,6 +181,50 @@ __global__ void k_unpack_pso(const uint64_t* __restrict__ keys, uint64_t n, cons
   }
 }
 
+// the CSR's sorted keys (s, p, o) without duplicates / dropped labels, compacted
+// (the label-major lists are then one stable pass on the label bits away)
+__global__ void k_compact_keys(const uint64_t* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ pos,
+                               int drop_bit, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    if (!((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k)) out[pos[i]] = k;
+  }
+}
+
+cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, uint64_t* out,
+                                cudaStream_t st) {
+  k_compact_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, out);
+  return cudaGetLastError();
+}
+
+// label-major lists from (s, p, o) keys already stably sorted by p: ls/lo and
+// entries per label (warp-aggregated counts)
+__global__ void k_unpack_spo_lm(const uint64_t* __restrict__ keys, uint64_t n, int nb, int pb,
+                                uint32_t* __restrict__ ls, uint32_t* __restrict__ lo, uint32_t* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t m = (1ull << nb) - 1, pm = (1ull << pb) - 1;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t l = 0xffffffffu;
+    const bool valid = i < n;
+    if (valid) {
+      const uint64_t k = keys[i];
+      l = (uint32_t)((k >> nb) & pm);
+      ls[i] = (uint32_t)(k >> (nb + pb));
+      lo[i] = (uint32_t)(k & m);
+    }
+    const uint32_t peers = __match_any_sync(GSM_FULL, l);
+    const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + l, cnt);
+  }
+}
+
+cudaError_t launch_unpack_spo_lm(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* ls, uint32_t* lo,
+                                 uint32_t* counts, cudaStream_t st) {
+  k_unpack_spo_lm<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, nb, pb, ls, lo, counts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
                               uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st) {
   k_unpack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, nb, ls, lo, counts);

@@ -207,6 +207,10 @@ gsmart_status gsm::ctx_sync(gsmart_ctx* ctx) {
 }
 
 void gsm::free_lspm(gsmart_ctx* ctx) {
+  if (ctx->lm_keys) {  // a build that failed between the CSR and the label-major lists
+    dfree(ctx, ctx->lm_keys);
+    ctx->lm_keys = nullptr;
+  }
   for (auto& f : ctx->f) {
     if (f.sym) {
       cudaStreamSynchronize(ctx->st);
@@ -544,7 +548,7 @@ static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* 
   return GSMART_OK;
 }
 
-static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep) {
+static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep, bool lm_from_csr = false) {
   if (ctx->world > 1) return build_format_part(ctx, fmt, d_keep);
   Lspm& L = ctx->f[fmt];
   const uint64_t n = ctx->n_triples;
@@ -566,6 +570,11 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
     CU(launch_unpack(sk.k, n, sk.pos, sk.drop, nb + pb, nb, L.col, L.pred, ctx->pred_bytes, L.rp, ctx->st));
   else if (n)
     CU(launch_unpack2(sk.k, sk.lo, n, sk.pos, sk.drop, pb, 0, L.col, L.pred, ctx->pred_bytes, nullptr, L.rp, ctx->st));
+  if (fmt == 0 && lm_from_csr && n && !sk.wide && M) {  // hand the unique (s, p, o) keys to the label-major build
+    TRY(dalloc(ctx, &ctx->lm_keys, M));
+    CU(launch_compact_keys(sk.k, n, sk.pos, sk.drop, ctx->lm_keys, ctx->st));
+    ctx->lm_keys_n = M;
+  }
   {
     void* stmp = nullptr;
     TRY(sc.get((char**)&stmp, scan_tmp_bytes((uint64_t)N + 1)));
@@ -604,6 +613,32 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
   uint32_t* cnt = nullptr;
   TRY(sc.get(&cnt, (uint64_t)ctx->P + 2));
   CU(cudaMemsetAsync(cnt, 0, ((size_t)ctx->P + 2) * 4, ctx->st));
+  if (!in_side && ctx->lm_keys) {
+    // the CSR's keys are sorted by (s, p, o): a stable LSD pass on the label bits
+    // alone gives (p, s, o) — one radix pass instead of a full key sort
+    const int pb = bits_for(ctx->P);
+    const unsigned long long M = ctx->lm_keys_n;
+    uint64_t* k1 = nullptr;
+    void* rtmp = nullptr;
+    TRY(sc.get(&k1, M));
+    const size_t rb = radix_tmp_bytes(M);
+    TRY(sc.get((char**)&rtmp, rb));
+    int second = 0;
+    CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, nb, nb + pb, rtmp, rb, ctx->st, &second, nullptr, true));
+    TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
+    TRY(dalloc(ctx, &L.o, M + 4));
+    CU(launch_unpack_spo_lm(second ? k1 : ctx->lm_keys, M, nb, pb, L.s, L.o, cnt, ctx->st));
+    std::vector<uint32_t> h(ctx->P + 2);
+    CU(cudaMemcpyAsync(h.data(), cnt, h.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CU(cudaStreamSynchronize(ctx->st));
+    dfree(ctx, ctx->lm_keys);
+    ctx->lm_keys = nullptr;
+    L.off.assign(ctx->P + 2, 0);
+    for (uint32_t l = 0; l + 1 < ctx->P + 2; l++) L.off[l + 1] = L.off[l] + h[l];
+    L.M = M;
+    L.built = true;
+    return GSMART_OK;
+  }
   SortedKeys sk;
   const uint32_t rlo = ctx->world > 1 ? ctx->part.v[ctx->rank] : 0u;
   const uint32_t rhi = ctx->world > 1 ? ctx->part.v[ctx->rank + 1] : 0xffffffffu;
@@ -688,8 +723,12 @@ static gsmart_status build_lspm_masks(gsmart_ctx* ctx, const std::vector<uint8_t
   };
   if (ctx->world > 1) TRY(compute_partition(ctx, d_keep));
   lap("partition");
+  // world == 1 and the CSR holds every kept label: the label-major lists come from
+  // the CSR's sorted keys (one pass on the label bits) instead of a sort of their own
+  const bool lm_csr = ctx->world == 1 && formats == (GSMART_CSR | GSMART_CSC) && keep == kcsr &&
+                      !getenv("GSMART_LM_SORT");
   for (int fmt = 0; fmt < 2; fmt++) {
-    if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_kf[fmt]));
+    if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_kf[fmt], lm_csr));
     lap(fmt == 0 ? "csr" : "csc");
   }
   if (formats == (GSMART_CSR | GSMART_CSC)) {

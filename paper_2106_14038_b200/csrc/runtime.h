@@ -264,6 +264,8 @@ struct gsmart_ctx {
   int pred_bytes = 1;
   gsm::Lspm f[2];
   std::vector<uint8_t> keep[2];  // labels each format holds (P + 1 flags) since the last build
+  uint64_t* lm_keys = nullptr;    // build-time hand-off: the CSR's unique (s, p, o) keys (label-major source)
+  unsigned long long lm_keys_n = 0;
   gsm::LabelMajor lm;
   gsm::LabelMajor lm_in;     // world > 1: label-major entries whose OBJECT is this rank's (stored as (o, s))
   gsm::Partition part;       // world > 1: vertex ranges of the ranks
