@@ -183,17 +183,23 @@ __global__ void k_unpack_pso(const uint64_t* __restrict__ keys, uint64_t n, cons
 
 // the CSR's sorted keys (s, p, o) without duplicates / dropped labels, compacted
 // (the label-major lists are then one stable pass on the label bits away)
+// (compacted and re-laid out as (p, s, o) keys: p above bit 2 nb, so a stable
+// pass on the label digit — whose window above the label holds zeros — sorts them)
 __global__ void k_compact_keys(const uint64_t* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ pos,
-                               int drop_bit, uint64_t* __restrict__ out) {
+                               int drop_bit, int nb, int pb, uint64_t* __restrict__ out) {
+  const uint64_t m = (1ull << nb) - 1, pm = (1ull << pb) - 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[i];
-    if (!((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k)) out[pos[i]] = k;
+    if (!((k >> drop_bit) & 1ull) && (i == 0 || keys[i - 1] != k)) {
+      const uint64_t srow = k >> (nb + pb), p = (k >> nb) & pm, o = k & m;
+      out[pos[i]] = (p << (2 * nb)) | (srow << nb) | o;
+    }
   }
 }
 
-cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, uint64_t* out,
-                                cudaStream_t st) {
-  k_compact_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, out);
+cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb, int pb,
+                                uint64_t* out, cudaStream_t st) {
+  k_compact_keys<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, nb, pb, out);
   return cudaGetLastError();
 }
 
@@ -207,10 +213,10 @@ __global__ void k_unpack_spo_lm(const uint64_t* __restrict__ keys, uint64_t n, i
     const uint64_t i = base + threadIdx.x;
     uint32_t l = 0xffffffffu;
     const bool valid = i < n;
-    if (valid) {
+    if (valid) {  // (p, s, o) layout
       const uint64_t k = keys[i];
-      l = (uint32_t)((k >> nb) & pm);
-      ls[i] = (uint32_t)(k >> (nb + pb));
+      l = (uint32_t)((k >> (2 * nb)) & pm);
+      ls[i] = (uint32_t)((k >> nb) & m);
       lo[i] = (uint32_t)(k & m);
     }
     const uint32_t peers = __match_any_sync(GSM_FULL, l);

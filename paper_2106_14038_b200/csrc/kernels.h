@@ -97,8 +97,8 @@ cudaError_t launch_heavy_stats(const uint32_t* rp, uint32_t n_rows, unsigned lon
 // into s/o arrays grouped by label; counts[p] += entries of label p
 cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t* o, uint64_t n, const uint8_t* keep,
                             int nb, int drop_bit, uint32_t rlo, uint32_t rhi, uint64_t* keys, cudaStream_t st);
-cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, uint64_t* out,
-                                cudaStream_t st);
+cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb, int pb,
+                                uint64_t* out, cudaStream_t st);
 cudaError_t launch_unpack_spo_lm(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* ls, uint32_t* lo,
                                  uint32_t* counts, cudaStream_t st);
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,

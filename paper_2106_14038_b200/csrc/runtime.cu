@@ -572,7 +572,7 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
     CU(launch_unpack2(sk.k, sk.lo, n, sk.pos, sk.drop, pb, 0, L.col, L.pred, ctx->pred_bytes, nullptr, L.rp, ctx->st));
   if (fmt == 0 && lm_from_csr && n && !sk.wide && M) {  // hand the unique (s, p, o) keys to the label-major build
     TRY(dalloc(ctx, &ctx->lm_keys, M));
-    CU(launch_compact_keys(sk.k, n, sk.pos, sk.drop, ctx->lm_keys, ctx->st));
+    CU(launch_compact_keys(sk.k, n, sk.pos, sk.drop, nb, pb, ctx->lm_keys, ctx->st));
     ctx->lm_keys_n = M;
   }
   {
@@ -614,8 +614,8 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
   TRY(sc.get(&cnt, (uint64_t)ctx->P + 2));
   CU(cudaMemsetAsync(cnt, 0, ((size_t)ctx->P + 2) * 4, ctx->st));
   if (!in_side && ctx->lm_keys) {
-    // the CSR's keys are sorted by (s, p, o): a stable LSD pass on the label bits
-    // alone gives (p, s, o) — one radix pass instead of a full key sort
+    // the CSR's keys are in (s, p, o) order, re-laid out as (p, s, o) keys: a stable
+    // LSD pass on the label bits alone sorts them — one radix pass instead of a full sort
     const int pb = bits_for(ctx->P);
     const unsigned long long M = ctx->lm_keys_n;
     uint64_t* k1 = nullptr;
@@ -624,7 +624,7 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
     const size_t rb = radix_tmp_bytes(M);
     TRY(sc.get((char**)&rtmp, rb));
     int second = 0;
-    CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, nb, nb + pb, rtmp, rb, ctx->st, &second, nullptr, true));
+    CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, 2 * nb, 2 * nb + pb, rtmp, rb, ctx->st, &second, nullptr, true));
     TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
     TRY(dalloc(ctx, &L.o, M + 4));
     CU(launch_unpack_spo_lm(second ? k1 : ctx->lm_keys, M, nb, pb, L.s, L.o, cnt, ctx->st));
