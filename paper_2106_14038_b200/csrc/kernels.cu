@@ -231,6 +231,37 @@ cudaError_t launch_unpack_spo_lm(const uint64_t* keys, uint64_t n, int nb, int p
   return cudaGetLastError();
 }
 
+// CSC entries from (p, s, o)-layout keys in (o, p, s) order: row o, label p,
+// column s; warp-aggregated row counts
+template <typename PT>
+__global__ void k_unpack_lm_csc(const uint64_t* __restrict__ keys, uint64_t n, int nb, int pb,
+                                uint32_t* __restrict__ col, PT* __restrict__ pred, uint32_t* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t m = (1ull << nb) - 1, pm = (1ull << pb) - 1;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    uint32_t row = 0xffffffffu;
+    if (valid) {
+      const uint64_t k = keys[i];
+      row = (uint32_t)(k & m);
+      col[i] = (uint32_t)((k >> nb) & m);
+      pred[i] = (PT)((k >> (2 * nb)) & pm);
+    }
+    const uint32_t peers = __match_any_sync(GSM_FULL, row);
+    const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + row, cnt);
+  }
+}
+
+cudaError_t launch_unpack_lm_csc(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* col, void* pred,
+                                 int pred_bytes, uint32_t* counts, cudaStream_t st) {
+  const unsigned g = grid_for(n, 256, 148 * 32);
+  if (pred_bytes == 1) k_unpack_lm_csc<uint8_t><<<g, 256, 0, st>>>(keys, n, nb, pb, col, (uint8_t*)pred, counts);
+  else k_unpack_lm_csc<uint16_t><<<g, 256, 0, st>>>(keys, n, nb, pb, col, (uint16_t*)pred, counts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,
                               uint32_t* ls, uint32_t* lo, uint32_t* counts, cudaStream_t st) {
   k_unpack_pso<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, pos, drop_bit, nb, ls, lo, counts);

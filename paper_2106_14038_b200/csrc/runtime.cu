@@ -548,6 +548,8 @@ static gsmart_status build_format_part(gsmart_ctx* ctx, int fmt, const uint8_t* 
   return GSMART_OK;
 }
 
+static gsmart_status finish_format(gsmart_ctx* ctx, int fmt, unsigned long long M);
+
 static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_keep, bool lm_from_csr = false) {
   if (ctx->world > 1) return build_format_part(ctx, fmt, d_keep);
   Lspm& L = ctx->f[fmt];
@@ -575,6 +577,16 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
     CU(launch_compact_keys(sk.k, n, sk.pos, sk.drop, nb, pb, ctx->lm_keys, ctx->st));
     ctx->lm_keys_n = M;
   }
+  return finish_format(ctx, fmt, M);
+}
+
+// row counts in L.rp -> row pointers; row label signatures, label statistics,
+// functional labels, heavy-row statistics
+static gsmart_status finish_format(gsmart_ctx* ctx, int fmt, unsigned long long M) {
+  Lspm& L = ctx->f[fmt];
+  const uint32_t N = ctx->N;
+  Scratch sc(ctx);
+  unsigned long long* tot = ctx->d_ctr + 40;
   {
     void* stmp = nullptr;
     TRY(sc.get((char**)&stmp, scan_tmp_bytes((uint64_t)N + 1)));
@@ -605,7 +617,8 @@ static gsmart_status build_format(gsmart_ctx* ctx, int fmt, const uint8_t* d_kee
 // world > 1 (in_side = false): only this rank's subjects; in_side = true: this
 // rank's objects, sorted by (p, o, s) and stored as (o, s) — the center of an
 // IN edge comes first, like the subject of an OUT edge.
-static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, bool in_side = false) {
+static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, bool in_side = false,
+                                       bool keep_keys = false) {
   LabelMajor& L = in_side ? ctx->lm_in : ctx->lm;
   const uint64_t n = ctx->n_triples;
   const int nb = bits_for(ctx->N - 1);
@@ -620,19 +633,21 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
     const unsigned long long M = ctx->lm_keys_n;
     uint64_t* k1 = nullptr;
     void* rtmp = nullptr;
-    TRY(sc.get(&k1, M));
+    TRY(dalloc(ctx, &k1, M));
     const size_t rb = radix_tmp_bytes(M);
     TRY(sc.get((char**)&rtmp, rb));
     int second = 0;
     CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, 2 * nb, 2 * nb + pb, rtmp, rb, ctx->st, &second, nullptr, true));
     TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
     TRY(dalloc(ctx, &L.o, M + 4));
-    CU(launch_unpack_spo_lm(second ? k1 : ctx->lm_keys, M, nb, pb, L.s, L.o, cnt, ctx->st));
+    uint64_t* sorted = second ? k1 : ctx->lm_keys;
+    CU(launch_unpack_spo_lm(sorted, M, nb, pb, L.s, L.o, cnt, ctx->st));
     std::vector<uint32_t> h(ctx->P + 2);
     CU(cudaMemcpyAsync(h.data(), cnt, h.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
     CU(cudaStreamSynchronize(ctx->st));
-    dfree(ctx, ctx->lm_keys);
-    ctx->lm_keys = nullptr;
+    dfree(ctx, second ? ctx->lm_keys : k1);
+    ctx->lm_keys = keep_keys ? sorted : nullptr;  // the CSC is one stable sort on the object away
+    if (!keep_keys) dfree(ctx, sorted);
     L.off.assign(ctx->P + 2, 0);
     for (uint32_t l = 0; l + 1 < ctx->P + 2; l++) L.off[l + 1] = L.off[l] + h[l];
     L.M = M;
@@ -657,6 +672,33 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
   L.M = M;
   L.built = true;
   return GSMART_OK;
+}
+
+// CSC from the label-major keys ((p, s, o) layout, in (p, s, o) order): a stable
+// LSD sort on the object field alone gives (o, p, s) order — the CSC's entry
+// order — in nb/8 passes instead of a full sort of freshly packed keys
+static gsmart_status build_csc_from_lm(gsmart_ctx* ctx) {
+  Lspm& L = ctx->f[1];
+  const uint32_t N = ctx->N;
+  const int nb = bits_for(N - 1), pb = bits_for(ctx->P);
+  const unsigned long long M = ctx->lm_keys_n;
+  Scratch sc(ctx);
+  uint64_t* k1 = nullptr;
+  void* rtmp = nullptr;
+  TRY(sc.get(&k1, M));
+  const size_t rb = radix_tmp_bytes(M);
+  TRY(sc.get((char**)&rtmp, rb));
+  int second = 0;
+  CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, 0, nb, rtmp, rb, ctx->st, &second, nullptr, true));
+  TRY(dalloc(ctx, &L.rp, (uint64_t)N + 1));
+  TRY(dalloc(ctx, &L.col, M));
+  TRY(dalloc(ctx, (uint8_t**)&L.pred, M * ctx->pred_bytes + 64));
+  CU(cudaMemsetAsync(L.rp, 0, ((uint64_t)N + 1) * 4, ctx->st));
+  CU(launch_unpack_lm_csc(second ? k1 : ctx->lm_keys, M, nb, pb, L.col, L.pred, ctx->pred_bytes, L.rp, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  dfree(ctx, ctx->lm_keys);
+  ctx->lm_keys = nullptr;
+  return finish_format(ctx, 1, M);
 }
 
 static gsmart_status keep_mask(gsmart_ctx* ctx, const uint32_t* ids, uint32_t n, bool all, std::vector<uint8_t>* out) {
@@ -727,14 +769,25 @@ static gsmart_status build_lspm_masks(gsmart_ctx* ctx, const std::vector<uint8_t
   // the CSR's sorted keys (one pass on the label bits) instead of a sort of their own
   const bool lm_csr = ctx->world == 1 && formats == (GSMART_CSR | GSMART_CSC) && keep == kcsr &&
                       !getenv("GSMART_LM_SORT");
-  for (int fmt = 0; fmt < 2; fmt++) {
-    if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_kf[fmt], lm_csr));
-    lap(fmt == 0 ? "csr" : "csc");
-  }
-  if (formats == (GSMART_CSR | GSMART_CSC)) {
-    TRY(build_label_major(ctx, d_keep));
-    if (ctx->world > 1) TRY(build_label_major(ctx, d_keep, true));
+  if (lm_csr && kcsc == keep) {  // CSR -> label-major lists -> CSC, each from the previous one's keys
+    TRY(build_format(ctx, 0, d_kf[0], true));
+    lap("csr");
+    const bool derive = ctx->lm_keys != nullptr;
+    TRY(build_label_major(ctx, d_keep, false, derive));
     lap("label-major");
+    if (derive) TRY(build_csc_from_lm(ctx));
+    else TRY(build_format(ctx, 1, d_kf[1]));
+    lap("csc");
+  } else {
+    for (int fmt = 0; fmt < 2; fmt++) {
+      if (formats & (fmt == 0 ? GSMART_CSR : GSMART_CSC)) TRY(build_format(ctx, fmt, d_kf[fmt], lm_csr));
+      lap(fmt == 0 ? "csr" : "csc");
+    }
+    if (formats == (GSMART_CSR | GSMART_CSC)) {
+      TRY(build_label_major(ctx, d_keep));
+      if (ctx->world > 1) TRY(build_label_major(ctx, d_keep, true));
+      lap("label-major");
+    }
   }
   CU(cudaStreamSynchronize(ctx->st));
   return GSMART_OK;
