@@ -205,8 +205,11 @@ cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t
 
 // label-major lists from (s, p, o) keys already stably sorted by p: ls/lo and
 // entries per label (warp-aggregated counts)
+// (csc_keys, optional: the same entries re-laid out as (o, p, s) keys — the
+// object on top, so a stable pass on its digits sees zeros above it)
 __global__ void k_unpack_spo_lm(const uint64_t* __restrict__ keys, uint64_t n, int nb, int pb,
-                                uint32_t* __restrict__ ls, uint32_t* __restrict__ lo, uint32_t* __restrict__ counts) {
+                                uint32_t* __restrict__ ls, uint32_t* __restrict__ lo, uint32_t* __restrict__ counts,
+                                uint64_t* __restrict__ csc_keys) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t m = (1ull << nb) - 1, pm = (1ull << pb) - 1;
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += stride) {
@@ -216,8 +219,10 @@ __global__ void k_unpack_spo_lm(const uint64_t* __restrict__ keys, uint64_t n, i
     if (valid) {  // (p, s, o) layout
       const uint64_t k = keys[i];
       l = (uint32_t)((k >> (2 * nb)) & pm);
-      ls[i] = (uint32_t)((k >> nb) & m);
-      lo[i] = (uint32_t)(k & m);
+      const uint32_t sv = (uint32_t)((k >> nb) & m), ov = (uint32_t)(k & m);
+      ls[i] = sv;
+      lo[i] = ov;
+      if (csc_keys) csc_keys[i] = ((uint64_t)ov << (nb + pb)) | ((uint64_t)l << nb) | sv;
     }
     const uint32_t peers = __match_any_sync(GSM_FULL, l);
     const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));
@@ -226,12 +231,12 @@ __global__ void k_unpack_spo_lm(const uint64_t* __restrict__ keys, uint64_t n, i
 }
 
 cudaError_t launch_unpack_spo_lm(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* ls, uint32_t* lo,
-                                 uint32_t* counts, cudaStream_t st) {
-  k_unpack_spo_lm<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, nb, pb, ls, lo, counts);
+                                 uint32_t* counts, cudaStream_t st, uint64_t* csc_keys) {
+  k_unpack_spo_lm<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(keys, n, nb, pb, ls, lo, counts, csc_keys);
   return cudaGetLastError();
 }
 
-// CSC entries from (p, s, o)-layout keys in (o, p, s) order: row o, label p,
+// CSC entries from (o, p, s)-layout keys in (o, p, s) order: row o, label p,
 // column s; warp-aggregated row counts
 template <typename PT>
 __global__ void k_unpack_lm_csc(const uint64_t* __restrict__ keys, uint64_t n, int nb, int pb,
@@ -242,11 +247,11 @@ __global__ void k_unpack_lm_csc(const uint64_t* __restrict__ keys, uint64_t n, i
     const uint64_t i = base + threadIdx.x;
     const bool valid = i < n;
     uint32_t row = 0xffffffffu;
-    if (valid) {
+    if (valid) {  // (o, p, s) layout
       const uint64_t k = keys[i];
-      row = (uint32_t)(k & m);
-      col[i] = (uint32_t)((k >> nb) & m);
-      pred[i] = (PT)((k >> (2 * nb)) & pm);
+      row = (uint32_t)(k >> (nb + pb));
+      col[i] = (uint32_t)(k & m);
+      pred[i] = (PT)((k >> nb) & pm);
     }
     const uint32_t peers = __match_any_sync(GSM_FULL, row);
     const uint32_t cnt = __popc(peers & __ballot_sync(GSM_FULL, valid));

@@ -100,7 +100,7 @@ cudaError_t launch_pack_pso(const uint32_t* s, const uint32_t* p, const uint32_t
 cudaError_t launch_compact_keys(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb, int pb,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_unpack_spo_lm(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* ls, uint32_t* lo,
-                                 uint32_t* counts, cudaStream_t st);
+                                 uint32_t* counts, cudaStream_t st, uint64_t* csc_keys = nullptr);
 cudaError_t launch_unpack_lm_csc(const uint64_t* keys, uint64_t n, int nb, int pb, uint32_t* col, void* pred,
                                  int pred_bytes, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_unpack_pso(const uint64_t* keys, uint64_t n, const uint32_t* pos, int drop_bit, int nb,

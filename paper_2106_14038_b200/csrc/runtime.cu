@@ -641,13 +641,19 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
     TRY(dalloc(ctx, &L.s, M + 4));  // +4: k_push_edge's 16-byte loads may overrun the last label
     TRY(dalloc(ctx, &L.o, M + 4));
     uint64_t* sorted = second ? k1 : ctx->lm_keys;
-    CU(launch_unpack_spo_lm(sorted, M, nb, pb, L.s, L.o, cnt, ctx->st));
+    uint64_t* other = second ? ctx->lm_keys : k1;
+    // keep_keys: the entries re-laid out as (o, p, s) keys go into the other buffer —
+    // in (p, s, o) order, the CSC is one stable sort on the object away
+    CU(launch_unpack_spo_lm(sorted, M, nb, pb, L.s, L.o, cnt, ctx->st, keep_keys ? other : nullptr));
     std::vector<uint32_t> h(ctx->P + 2);
     CU(cudaMemcpyAsync(h.data(), cnt, h.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
     CU(cudaStreamSynchronize(ctx->st));
-    dfree(ctx, second ? ctx->lm_keys : k1);
-    ctx->lm_keys = keep_keys ? sorted : nullptr;  // the CSC is one stable sort on the object away
-    if (!keep_keys) dfree(ctx, sorted);
+    dfree(ctx, sorted);
+    if (keep_keys) ctx->lm_keys = other;
+    else {
+      dfree(ctx, other);
+      ctx->lm_keys = nullptr;
+    }
     L.off.assign(ctx->P + 2, 0);
     for (uint32_t l = 0; l + 1 < ctx->P + 2; l++) L.off[l + 1] = L.off[l] + h[l];
     L.M = M;
@@ -674,9 +680,9 @@ static gsmart_status build_label_major(gsmart_ctx* ctx, const uint8_t* d_keep, b
   return GSMART_OK;
 }
 
-// CSC from the label-major keys ((p, s, o) layout, in (p, s, o) order): a stable
-// LSD sort on the object field alone gives (o, p, s) order — the CSC's entry
-// order — in nb/8 passes instead of a full sort of freshly packed keys
+// CSC from the label-major entries ((o, p, s)-layout keys in (p, s, o) order): a
+// stable LSD sort on the object field alone (zeros above it) gives (o, p, s)
+// order — the CSC's entry order — in nb/8 passes instead of a full sort
 static gsmart_status build_csc_from_lm(gsmart_ctx* ctx) {
   Lspm& L = ctx->f[1];
   const uint32_t N = ctx->N;
@@ -689,7 +695,7 @@ static gsmart_status build_csc_from_lm(gsmart_ctx* ctx) {
   const size_t rb = radix_tmp_bytes(M);
   TRY(sc.get((char**)&rtmp, rb));
   int second = 0;
-  CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, 0, nb, rtmp, rb, ctx->st, &second, nullptr, true));
+  CU(radix_sort_keys_u64(ctx->lm_keys, k1, M, nb + pb, 2 * nb + pb, rtmp, rb, ctx->st, &second, nullptr, true));
   TRY(dalloc(ctx, &L.rp, (uint64_t)N + 1));
   TRY(dalloc(ctx, &L.col, M));
   TRY(dalloc(ctx, (uint8_t**)&L.pred, M * ctx->pred_bytes + 64));
