@@ -752,6 +752,24 @@ static gsmart_status build_lspm_masks(gsmart_ctx* ctx, const std::vector<uint8_t
   free_lspm(ctx);
   ctx->keep[0] = kcsr;
   ctx->keep[1] = kcsc;
+  // Warm the context's pool to the build's peak once: the pool keeps freed memory
+  // (release threshold = max), so the build's many large temporaries are carved
+  // from memory it already holds instead of mapping new physical memory per call
+  // (which made repeated builds vary 2-10x)
+  if (!ctx->cfg.alloc) {
+    const uint64_t want = ctx->n_triples * 48ull + (uint64_t)ctx->N * 24ull + (64ull << 20);
+    uint64_t have = 0;
+    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &have);
+    if (have < want) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if (want - have + (4ull << 30) < fr) {
+        void* w = nullptr;
+        if (cudaMallocFromPoolAsync(&w, want - have, ctx->pool, ctx->st) == cudaSuccess) cudaFreeAsync(w, ctx->st);
+        cudaGetLastError();
+      }
+    }
+  }
   Scratch sc(ctx);
   uint8_t *d_keep = nullptr, *d_kf[2] = {nullptr, nullptr};
   TRY(sc.get(&d_keep, keep.size()));
