@@ -313,6 +313,7 @@ struct Exec {
   };
   bool fact = false;
   std::vector<Occ> occ;
+  std::vector<uint8_t> fused_lv;  // per level: expanded by the fused functional kernel
   uint32_t n_omega = 0;
   std::vector<uint64_t> om_off, om_mask;  // per occurrence: its key set in sl.om (second occurrences only)
   // key sets of the first occurrences, one per second occurrence, sized for the
@@ -797,6 +798,7 @@ struct Exec {
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
       if (a.tree && functional_edge(a.dir & 1, Lv.label)) {  // <= 1 child per parent: one fused pass
+        fused_lv[k] = 1;
         prof.begin(K_EXPAND_EMIT);
         CU(launch_expand_func(a, ctx->pred_bytes, smc, sl.st));
         launches[K_EXPAND_EMIT]++;
@@ -918,6 +920,7 @@ struct Exec {
       a.ctr = sl.d_ctr;
       a.lb = next_lb(sl);
       if (a.tree && !a.om_tab && functional_edge(a.dir & 1, oc.label)) {  // <= 1 child per parent
+        fused_lv[o] = 1;
         prof.begin(K_EXPAND_EMIT);
         CU(launch_expand_func(a, ctx->pred_bytes, smc, sl.st));
         launches[K_EXPAND_EMIT]++;
@@ -1415,6 +1418,14 @@ struct Exec {
     } else {
       plan_ancestors();
     }
+    // levels the fused functional kernel expands (the same decision the launch
+    // paths take; kept for the byte accounting, which also runs after graph replays)
+    fused_lv.assign(L, 0);
+    for (uint32_t k = 1; k < L; k++) {
+      if (fact) fused_lv[k] = occ[k].tree && occ[k].same < 0 && functional_edge(occ[k].dir == OUT ? 0u : 1u, occ[k].label);
+      else fused_lv[k] = plan->levels[k].tree_edge >= 0 &&
+                         functional_edge(plan->levels[k].dir == OUT ? 0u : 1u, plan->levels[k].label);
+    }
     TRY(decide_push());
     TRY(ensure_workspace());
     TRY(begin_seq(ctx, sl));
@@ -1787,10 +1798,18 @@ struct Exec {
                          8ull * (filter_main - skipped) * W +
                          8 * c[C_PUSH] + 12ull * push_and * W;  // push: (s, o) per entry; AND: cand r/w + sat
     st.bytes[K_SEED] = 4 * c[C_SEED];
-    for (uint32_t k = 0; k + 1 < st.n_levels && k + 1 < GSMART_MAX_LEVELS; k++) parents += st.level_nodes[k];
-    for (uint32_t k = 1; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) children += st.level_nodes[k];
+    // per expanded level: its parents (the previous trie level, or the parent
+    // occurrence) — a fused functional level does the segment work in the emit kernel
+    uint64_t parents_fused = 0;
+    for (uint32_t k = 1; k < st.n_levels && k < GSMART_MAX_LEVELS; k++) {
+      const uint32_t pk = fact ? (uint32_t)occ[k].par : k - 1;
+      const uint64_t np = st.level_nodes[pk];
+      if (k < fused_lv.size() && fused_lv[k]) parents_fused += np;
+      else parents += np;
+      children += st.level_nodes[k];
+    }
     st.bytes[K_EXPAND_SEG] = 12 * parents;
-    st.bytes[K_EXPAND_EMIT] = 4 * c[C_EXPAND] + 9 * children + 8 * parents;
+    st.bytes[K_EXPAND_EMIT] = 4 * c[C_EXPAND] + 9 * children + 8 * parents + 12 * parents_fused;
     // a5: every compaction reads this rank's bitmap range once and writes 4 B per id
     // (row lists of the groups + level 0); initialisation writes the bitmaps once
     const uint64_t range_bytes = 4ull * (whi - wlo);
