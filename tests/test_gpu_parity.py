@@ -446,6 +446,48 @@ def test_lubm_full_size_sampled_parity(G, U):
         e.close()
 
 
+def _row_hash(rows):
+    """Order-independent 128-bit digest of a row set: the sum and
+    the xor of splitmix64 over each row's packed columns."""
+    M = (1 << 64) - 1
+    s = x = 0
+    for r in np.asarray(rows, dtype=np.uint64).tolist():
+        h = 0
+        for v in r:
+            z = (h ^ v) + 0x9E3779B97F4A7C15 & M
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & M
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EB & M
+            h = z ^ (z >> 31)
+        s = (s + h) & M
+        x ^= h
+    return s, x
+
+
+def test_lubm1000_l1_l7_full_oracle(G):
+    """LUBM-1000 (~1.3e8 triples): the data-intensive triangles L1 and L7 against
+    the C oracle's complete answer — every row, plus the order-independent
+    128-bit digest — in bench.py's launch configuration (device input, batch)."""
+    import torch
+    d = lubm.generate(1000, seed=lubm.SEED_LUBM10K, device="cuda")
+    qs = [q for q in lubm.queries(d) if q.name in ("L1", "L7")]
+    e = G.Engine(0)
+    try:
+        G.gsmart_load_triples(e.ctx, d.s, d.p, d.o, d.n_entities, d.n_predicates)
+        G.gsmart_build_lspm(e.ctx)
+        got = e.query_batch(qs)
+        s, p, o = d.s.cpu().numpy(), d.p.cpu().numpy(), d.o.cpu().numpy()
+        del d
+        torch.cuda.empty_cache()
+        ix = OracleIndex(s, p, o)
+        for q, g in zip(qs, got):
+            exp = ix.query(q)
+            assert len(exp) > 1000, q.name
+            assert g.shape == exp.shape and np.array_equal(g, exp), q.name
+            assert _row_hash(g) == _row_hash(exp)
+    finally:
+        e.close()
+
+
 def test_graph_replay_matches(G, eng):
     """Plans executed repeatedly replay their captured phase-1 CUDA graph (fresh
     look-back epochs each time); interleaved plans, batches and NO_GRAPH give
