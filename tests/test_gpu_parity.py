@@ -488,6 +488,30 @@ def test_lubm1000_l1_l7_full_oracle(G):
         e.close()
 
 
+def test_watdiv100m_full_size_parity(G):
+    """configs[2] at full size (scale 2.1, ~1.08e8 triples) in bench.py's launch
+    configuration (device-resident generated input, the 11 queries as one
+    gsmart_execute_batch): every row of every query == the C oracle."""
+    import torch
+    from synth import watdiv
+    d = watdiv.generate(watdiv.SCALE_100M, device="cuda")
+    qs = watdiv.queries(d)
+    e = G.Engine(0)
+    try:
+        G.gsmart_load_triples(e.ctx, d.s, d.p, d.o, d.n_entities, d.n_predicates)
+        G.gsmart_build_lspm(e.ctx)
+        got = e.query_batch(qs)
+        s, p, o = d.s.cpu().numpy(), d.p.cpu().numpy(), d.o.cpu().numpy()
+        del d
+        torch.cuda.empty_cache()
+        ix = OracleIndex(s, p, o)
+        for q, g in zip(qs, got):
+            exp = ix.query(q)
+            assert g.shape == exp.shape and np.array_equal(g, exp), q.name
+    finally:
+        e.close()
+
+
 def test_graph_replay_matches(G, eng):
     """Plans executed repeatedly replay their captured phase-1 CUDA graph (fresh
     look-back epochs each time); interleaved plans, batches and NO_GRAPH give
