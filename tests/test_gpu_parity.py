@@ -501,13 +501,15 @@ def test_watdiv100m_full_size_parity(G):
         G.gsmart_load_triples(e.ctx, d.s, d.p, d.o, d.n_entities, d.n_predicates)
         G.gsmart_build_lspm(e.ctx)
         got = e.query_batch(qs)
+        fact = e.query_batch(qs, flags=G.GSMART_FACTORISED)  # f2: rows read off the factorised trees
         s, p, o = d.s.cpu().numpy(), d.p.cpu().numpy(), d.o.cpu().numpy()
         del d
         torch.cuda.empty_cache()
         ix = OracleIndex(s, p, o)
-        for q, g in zip(qs, got):
+        for q, g, gf in zip(qs, got, fact):
             exp = ix.query(q)
             assert g.shape == exp.shape and np.array_equal(g, exp), q.name
+            assert gf.shape == exp.shape and np.array_equal(gf, exp), q.name
     finally:
         e.close()
 
