@@ -71,7 +71,7 @@ typedef enum {
 /* execute flags */
 #define GSMART_COUNT_ONLY 1u      /* stop after pruning: n_rows only, no row enumeration */
 #define GSMART_KEEP_ON_DEVICE 2u  /* do not copy rows to host (use gsmart_result_rows_device) */
-#define GSMART_NO_REFINE 4u       /* skip the backward group re-evaluation */
+#define GSMART_NO_REFINE 4u       /* no backward group re-evaluation (the default since ABI 3; wins over GSMART_REFINE) */
 #define GSMART_PROFILE 8u         /* per-kernel CUDA-event timing into gsmart_stats (no graph replay) */
 #define GSMART_KEEP_CANDIDATES 16u /* keep the candidate bitmaps for gsmart_result_candidates */
 #define GSMART_NO_GRAPH 32u       /* launch kernels one by one instead of replaying the plan's CUDA graph */
@@ -79,6 +79,9 @@ typedef enum {
 #define GSMART_BACK_EDGES 128u    /* every evaluation of a group also tests the center's already-evaluated patterns
                                      against the earlier centers' bitmaps (Eq. 16 over Eq. 14 binding vectors,
                                      DESIGN.md R-back): tighter candidate sets, more work per group */
+#define GSMART_REFINE 512u        /* after the groups in plan order (each evaluated once), re-evaluate them in
+                                     reverse plan order (DESIGN.md R-refine): tighter candidate sets before the
+                                     expansion, same rows; measured slower on WatDiv-100M (3.80 vs 3.47 ms) */
 #define GSMART_FACTORISED 256u    /* f2: factorised binding trees (§7.1, per-path trees that
                                      share their DFS prefix) instead of the prefix trie: one level per occurrence of
                                      a variable, hanging off its tree parent's level; a pattern that closes onto a
@@ -249,7 +252,7 @@ gsmart_status gsmart_plan_describe(const gsmart_plan_t* plan, char* buf, size_t 
 void gsmart_plan_free(gsmart_plan_t* plan);
 
 /* Execute plan on the built LSpM: seeds -> grouped incident-edge evaluation
- * (forward, then backward re-evaluation unless GSMART_NO_REFINE) -> trie
+ * (in plan order; with GSMART_REFINE also backward) -> trie
  * expansion with pre-pruning and closing-edge checks -> bottom-up prune ->
  * row enumeration + lexicographic sort.  Collective when world > 1.
  * Synchronises the ctx stream before returning. */

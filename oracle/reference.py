@@ -546,7 +546,7 @@ def keep_sets(q, plan=None, back_edges=False):
 # --------------------------------------------------------------------------
 
 
-def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True, back_edges=False):
+def filter_schedule(s, p, o, n_entities, q, plan=None, refine=False, back_edges=False):
     """Candidate sets per variable after the schedule DESIGN.md states:
       1. cand_v = [0, N) for every variable (Eq. 4/5 with no constraint yet);
       2. each seed edge in edge-index order (light edges):
@@ -567,8 +567,10 @@ def filter_schedule(s, p, o, n_entities, q, plan=None, refine=True, back_edges=F
          neighbours' binding vectors as the diag(.) selections of Eqs.
          15-16); for back edges (evaluated at an earlier center c) it is
          Eq. 16's restriction of x's rows to c's Eq. 14 binding vector;
-      4. if refine: revise(x) for the centers in reverse plan order, the last
-         one skipped (nothing it reads changed after it).
+      4. if refine (GSMART_REFINE, reading R-refine; off by default: the paper
+         evaluates each group once): revise(x) for the centers in
+         reverse plan order, the last one skipped (nothing it reads changed
+         after it).
     Returns ({var: np.bool_ array of length N}, guards_hold)."""
     N = int(n_entities)
     T = triple_set(s, p, o)

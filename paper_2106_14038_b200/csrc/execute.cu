@@ -1292,7 +1292,7 @@ struct Exec {
     // this rank initialised and seeded them
     if (peer_mode()) TRY(rank_barrier());
     for (size_t i = 0; i < plan->groups.size(); i++) TRY(eval_group(plan->groups[i], i));
-    if (!(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
+    if ((flags & GSMART_REFINE) && !(flags & GSMART_NO_REFINE) && plan->groups.size() > 1)
       for (size_t i = plan->groups.size() - 1; i-- > 0;) TRY(eval_group(plan->groups[i], i));
     return launch_expansion(true);
   }
@@ -1368,7 +1368,7 @@ struct Exec {
 
   // phase 1 = seeds + grouped evaluation + expansion (graph key: uid, tag 0)
   gsmart_status run_phase1() {
-    return run_cached(plan->uid << 3, flags & (GSMART_NO_REFINE | GSMART_BACK_EDGES | GSMART_FACTORISED),
+    return run_cached(plan->uid << 3, flags & (GSMART_NO_REFINE | GSMART_REFINE | GSMART_BACK_EDGES | GSMART_FACTORISED),
                       [&] { return phase1_kernels(); });
   }
 

@@ -24,6 +24,7 @@ GSMART_KEEP_CANDIDATES, GSMART_NO_GRAPH = 16, 32
 GSMART_NO_SPECULATE = 64
 GSMART_BACK_EDGES = 128
 GSMART_FACTORISED = 256
+GSMART_REFINE = 512
 NKERNELS, MAX_LEVELS = 16, 32
 
 

@@ -98,7 +98,7 @@ def test_fig78_trees(G, eng, golden_fig):
     eng.load(s, p, o, 8, 4)
     q = fixtures.fig2_query()
     g = golden_fig["fig8_trees_root1"]
-    for flags in (G.GSMART_NO_REFINE, 0):
+    for flags in (G.GSMART_NO_REFINE, G.GSMART_REFINE):
         rows, n, st, occ = _run(G, eng, q, G.GSMART_FACTORISED | flags)
         assert _rows(rows) == [tuple(r) for r in golden_fig["solution_rows"]]
         assert st["factorised"] == 1 and st["n_omega"] == 1

@@ -64,7 +64,7 @@ def test_fig12_rows_and_level0(G, eng, golden_fig):
     assert _rows(rows) == [tuple(r) for r in golden_fig["solution_rows"]]
     root = golden_fig["root"]
     assert sorted(_bits_to_set(cs[root], 8)) == golden_fig["level0_candidates"]  # Ex. 7.2
-    rows2, cs2, st = _cands(G, eng, q, 0)
+    rows2, cs2, st = _cands(G, eng, q, G.GSMART_REFINE)
     assert _rows(rows2) == [tuple(r) for r in golden_fig["solution_rows"]]
     assert sorted(_bits_to_set(cs2[root], 8)) == [1]
     assert st["level_alive"][-1] == 2
@@ -165,8 +165,8 @@ def test_random_tiny_rows_and_candidates(G, eng, chunk):
         (s, p, o), n, P, q = tiny.random_case(seed)
         eng.load(s, p, o, n, P)
         exp = R.brute_force(s, p, o, n, q)
-        for flags, refine, back in ((0, True, False), (G.GSMART_NO_REFINE, False, False),
-                                    (G.GSMART_BACK_EDGES, True, True)):
+        for flags, refine, back in ((G.GSMART_REFINE, True, False), (0, False, False),
+                                    (G.GSMART_REFINE | G.GSMART_BACK_EDGES, True, True)):
             rows, cs, _ = _cands(G, eng, q, flags)
             assert _rows(rows) == exp, (seed, q)
             ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=back)
@@ -230,7 +230,7 @@ def test_direction_plans_rows_and_candidates(G, eng, golden_fig):
         eng.load(s, p, o, n, P)
         exp = R.brute_force(s, p, o, n, q)
         plan = R.plan_direction(q)
-        for flags, refine in ((0, True), (G.GSMART_NO_REFINE, False)):
+        for flags, refine in ((G.GSMART_REFINE, True), (0, False)):
             pl = G.gsmart_plan(eng.ctx, q, G.GSMART_DIRECTION)
             r = G.gsmart_execute(eng.ctx, pl, flags | G.GSMART_KEEP_CANDIDATES)
             try:
@@ -605,7 +605,7 @@ def test_absent_constants_candidates(G, eng):
               Query((None, None, 8), ((0, 2, 1), (1, 1, 2), (1, 1, 0))),
               Query((None, None, 8, 3), ((0, 3, 1), (2, 1, 3))),
               Query((None, None, 1, 3), ((0, 3, 1), (2, 1, 3)))):
-        rows, cs, _ = _cands(G, eng, q, 0)
+        rows, cs, _ = _cands(G, eng, q, G.GSMART_REFINE)
         assert _rows(rows) == R.brute_force(s, p, o, 8, q), q
         ref, _ = R.filter_schedule(s, p, o, 8, q, refine=True)
         for v in q.variables:
@@ -708,8 +708,8 @@ def test_push_form_tiny_rows_and_candidates(G, eng_push):
         (s, p, o), n, P, q = tiny.random_case(seed)
         eng_push.load(s, p, o, n, P)
         exp = R.brute_force(s, p, o, n, q)
-        for flags, refine, back in ((0, True, False), (G.GSMART_NO_REFINE, False, False),
-                                    (G.GSMART_BACK_EDGES, True, True)):
+        for flags, refine, back in ((G.GSMART_REFINE, True, False), (0, False, False),
+                                    (G.GSMART_REFINE | G.GSMART_BACK_EDGES, True, True)):
             rows, cs, _ = _cands(G, eng_push, q, flags)
             assert _rows(rows) == exp, (seed, q)
             ref, _ = R.filter_schedule(s, p, o, n, q, refine=refine, back_edges=back)
