@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="watdiv100m", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--mode", default="partitioned", choices=["replicas", "partitioned"],
                     help="N>1: partitioned = one batch over the 1-D vertex-range partition of the LSpM "
                          "(strong scaling, default); replicas = every GPU serves its own copy of the batch")
@@ -428,7 +428,7 @@ def main():
                             ("rows_d2h", t4, t5)):
                 stages[k].append(1000 * (b - a))
         d2h = nbytes
-    e2e_s = statistics.mean(e2e_times)
+    e2e_s = statistics.median(e2e_times)  # median of the e2e steps (robust to a slow outlier step)
     e2e_value = copies * sum(E) / e2e_s
 
     cpu = None
@@ -461,7 +461,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(3 * 4 * len(s_h)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * e2e_s,
-                    "stages_ms": {k: statistics.mean(v) for k, v in stages.items()}},
+                    "stages_ms": {k: statistics.median(v) for k, v in stages.items()}, "aggregate": "median over e2e steps"},
             "gpu_launches": int(launches_per_step * args.steps),
             "roofline": roofline,
             "cpu_baseline": cpu,
